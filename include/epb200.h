@@ -1,0 +1,210 @@
+/*
+ * epb200 — B200-native expert-parallel dispatch/combine (C ABI).
+ *
+ * Drop-in replacement for the engine/fabric layer of the reference simulator
+ * `epsim` (arxiv 2603.13606, NCCL EP).  The reference's Python API layer
+ * (pkg/src/epsim/api.py) maps onto these entry points one-to-one:
+ *
+ *   reference                                   | here
+ *   --------------------------------------------+-------------------------------
+ *   ll_regions / ht_regions (ll.py:107, ht.py:167)| epb_window_geometry
+ *   Fabric.register_window (fabric.py:120)       | epb_group_create
+ *   _Rendezvous.exchange (api.py:82-94)          | epb_group_ipc_desc + epb_group_open_peers
+ *                                                |  (descriptors all-gathered by the host)
+ *   per-token routing loops (ll.py:255-259,      | epb_routing_layout            (K1)
+ *     292-296; ht.py:299-307; api.py:150-170)    |
+ *   LLRank.dispatch send (ll.py:227-308)         | epb_ll_dispatch_send          (K2)
+ *   LLRank.complete_dispatch (ll.py:310-400)     | epb_ll_dispatch_recv          (K3)
+ *   LLRank.combine (ll.py:404-462)               | epb_ll_combine_send           (K4a)
+ *   LLRank.complete_combine (ll.py:464-507)      | epb_ll_combine_recv           (K4b)
+ *   HTRank.exchange_metadata (ht.py:291-331)     | epb_ht_meta_send / _recv      (K5a)
+ *   HTRank.dispatch + _assemble (ht.py:381-583)  | epb_ht_dispatch_send / _recv  (K5b)
+ *   HTRank.combine (ht.py:587-735)               | epb_ht_combine_send / _recv   (K6)
+ *   quantize_block / dequantize_block            | epb_fp8_quantize / _dequantize (K7)
+ *     (core.py:127-162)                          |
+ *   fabric.shutdown / wait timeout               | epb_group_poll_error (device error word)
+ *
+ * Conventions
+ *  - Every function returns 0 on success or an epb_status code whose order
+ *    follows epsim.core.ErrorCode (core.py:21-28); epb_last_error() gives the
+ *    detail string of the last failure on the calling thread.
+ *  - All tensor pointers are DEVICE pointers; calls are asynchronous on the
+ *    given stream (a cudaStream_t passed as void*).  The library never frees
+ *    caller memory.
+ *  - send/recv halves are separate launches so that N ranks emulated on ONE
+ *    GPU never run two kernels that wait on each other: all ranks' sends are
+ *    enqueued before any rank's recv.  With one process per GPU the recv
+ *    half spins (acquire loads, bounded by a timeout) on flags the peers'
+ *    send kernels store over NVLink.
+ *  - Sequence tags replace the reference's counter resets (ll.py:351-353):
+ *    every flag carries the round's tag, so double-buffer parities are reused
+ *    without a reset race.
+ */
+#ifndef EPB200_H
+#define EPB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* ---- status codes: 1..7 = epsim ErrorCode order (core.py:21-28) -------- */
+typedef enum {
+  EPB_OK = 0,
+  EPB_INVALID_ARGUMENT = 1,
+  EPB_SHAPE_MISMATCH = 2,
+  EPB_TAG_MISMATCH = 3,
+  EPB_CONFIG_MISMATCH = 4,
+  EPB_CAPACITY_EXCEEDED = 5,
+  EPB_HANDLE_STATE_ERROR = 6,
+  EPB_TRANSPORT_CLOSED = 7,
+  EPB_CUDA_ERROR = 8
+} epb_status;
+
+/* element kinds (epsim Dtype, core.py:45-56) */
+enum { EPB_F32 = 0, EPB_BF16 = 1, EPB_F16 = 2, EPB_FP8 = 3 };
+enum { EPB_LL = 0, EPB_HT = 1 };
+enum { EPB_LAYOUT_OPTIMIZED = 0, EPB_LAYOUT_LEGACY = 1 };
+
+/* static group geometry (epsim EpConfig, core.py:325-383) */
+typedef struct epb_config {
+  int32_t algorithm;        /* EPB_LL | EPB_HT */
+  int32_t num_ranks;
+  int32_t ranks_per_node;
+  int32_t num_experts;
+  int32_t top_k;
+  int32_t hidden;
+  int32_t max_tokens_per_rank;
+  int32_t token_dtype;      /* wire dtype, EPB_F32..EPB_FP8 */
+  int32_t with_scales;      /* FP8 block-128 scales on the wire */
+  int32_t layout;           /* LL slot layout */
+  int32_t ht_chunk_tokens;  /* kept for fingerprint parity */
+  int32_t ht_fifo_depth;
+  int32_t combine_dtype;    /* LL combine wire dtype; -1 = token_dtype (reference) */
+} epb_config;
+
+typedef struct epb_window_info {
+  uint64_t physical_bytes;  /* bytes this library needs (16-B aligned slots) */
+  uint64_t logical_bytes;   /* the reference's window_bytes (footprint parity) */
+} epb_window_info;
+
+/* per-handle routing layout; caller-owned device buffers (K1 outputs) */
+typedef struct epb_layout {
+  int32_t* expert_count;    /* [E]    m(e, self)                       */
+  int32_t* rank_count;      /* [N]    q(self, d): tokens touching d    */
+  int32_t* tok_rank;        /* [b*K]  rank of t among tokens -> e_tk    */
+  int32_t* tok_slot;        /* [b*N]  dedup slot of t at rank d, or -1  */
+  int32_t num_tokens;       /* b */
+} epb_layout;
+
+/* IPC descriptor exchanged by the host bootstrap (NCCL/gloo all-gather) */
+typedef struct epb_ipc_desc {
+  uint8_t handle[64];       /* cudaIpcMemHandle_t of the allocation     */
+  uint64_t offset;          /* window offset inside that allocation     */
+  uint64_t bytes;
+  int32_t device;
+  int32_t pid;
+} epb_ipc_desc;
+
+typedef struct epb_group epb_group;
+
+int epb_version(void);
+const char* epb_last_error(void);
+
+int epb_window_geometry(const epb_config* cfg, epb_window_info* out);
+
+/* window: device pointer of >= physical_bytes, or NULL to let the library
+ * cudaMalloc it.  The window is zeroed on `stream`. */
+int epb_group_create(const epb_config* cfg, int rank, void* window,
+                     uint64_t window_bytes, void* stream, epb_group** out);
+int epb_group_window(epb_group* g, void** window, uint64_t* bytes);
+int epb_group_ipc_desc(epb_group* g, epb_ipc_desc* out);
+/* process mode: open every peer's window through CUDA IPC */
+int epb_group_open_peers(epb_group* g, const epb_ipc_desc* descs);
+/* single-process emulation: peer windows are plain device pointers */
+int epb_group_set_peers(epb_group* g, const uint64_t* peer_windows);
+int epb_group_set_timeout(epb_group* g, uint64_t timeout_ns);
+/* reads (and with clear!=0 resets) the device error word; synchronises */
+int epb_group_poll_error(epb_group* g, int clear, int32_t* code);
+int epb_group_destroy(epb_group* g);
+
+/* K1: validation + counts + dedup slots + per-expert ranks */
+int epb_routing_layout(epb_group* g, const int64_t* topk_idx, int32_t b,
+                       const epb_layout* lay, void* stream);
+
+/* K2: LL dispatch send.  x: [b, H] in x_dtype (EPB_FP8 requires x_scales
+ * [b, H/128]); converted to the wire dtype (fused FP8 block quantisation). */
+int epb_ll_dispatch_send(epb_group* g, uint32_t seq, const void* x,
+                         int32_t x_dtype, const float* x_scales,
+                         const int64_t* topk_idx, const epb_layout* lay,
+                         void* stream);
+/* K3: LL dispatch recv.  out: [L, N*B, H] in out_dtype (EPB_F32 = the
+ * reference boundary, or the wire dtype with out_scales [L, N*B, H/128]);
+ * counts_f32/counts_i32: [L, N]; src_info: [L, N*B] = t*K + k. */
+int epb_ll_dispatch_recv(epb_group* g, uint32_t seq, void* out,
+                         int32_t out_dtype, float* out_scales,
+                         float* counts_f32, int32_t* counts_i32,
+                         int32_t* src_info, void* stream);
+/* K4a: LL combine send; expert_out [L, N*B, H] f32|bf16 */
+int epb_ll_combine_send(epb_group* g, uint32_t seq, const void* expert_out,
+                        int32_t in_dtype, const int32_t* counts_i32,
+                        const int32_t* src_info, void* stream);
+/* K4b: LL combine recv; out [b, H] f32|bf16 */
+int epb_ll_combine_recv(epb_group* g, uint32_t seq, const float* weights,
+                        int32_t b, void* out, int32_t out_dtype, void* stream);
+
+/* K5a: HT metadata all-gather over the windows */
+int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay,
+                     void* stream);
+/* meta_out: [N, E+N] i32 (m rows then q rows); offsets: [E, N] i32 row
+ * offset of group (e, src) on owner(e); recv_total: [1] i32 */
+int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out,
+                     int32_t* offsets, int32_t* recv_total, void* stream);
+/* K5b: HT dispatch.  x [b, H] x_dtype, weights [b, K] f32 */
+int epb_ht_dispatch_send(epb_group* g, uint32_t round, const void* x,
+                         int32_t x_dtype, const float* weights,
+                         const int64_t* topk_idx, const epb_layout* lay,
+                         const int32_t* offsets, void* stream);
+/* out [recv_total, H] out_dtype; origin [recv_total, 4] = (e, src, t, k);
+ * origin_w [recv_total] f32 */
+int epb_ht_dispatch_recv(epb_group* g, uint32_t round, void* out,
+                         int32_t out_dtype, int32_t* origin, float* origin_w,
+                         void* stream);
+/* K6: HT combine.  expert_rows [recv_total, H] f32|bf16 */
+int epb_ht_combine_send(epb_group* g, uint32_t round, const void* expert_rows,
+                        int32_t in_dtype, const int32_t* origin,
+                        int32_t recv_total, void* stream);
+int epb_ht_combine_recv(epb_group* g, uint32_t round, const int64_t* topk_idx,
+                        const float* weights, int32_t b, void* out,
+                        int32_t out_dtype, void* stream);
+/* device-side check that combine weights equal the dispatched ones
+ * (ht.py:605-609); sets EPB_INVALID_ARGUMENT in the error word */
+int epb_weights_equal(epb_group* g, const float* a, const float* b, int64_t n,
+                      void* stream);
+
+/* K7: standalone block-128 FP8 (E4M3, reference tie rule) */
+int epb_fp8_quantize(const void* x, int32_t x_dtype, int64_t rows, int32_t h,
+                     uint8_t* codes, float* scales, void* stream);
+int epb_fp8_dequantize(const uint8_t* codes, const float* scales, int64_t rows,
+                       int32_t h, float* out, void* stream);
+/* elementwise E4M3 encode without scales (combine-wire form) */
+int epb_e4m3_encode(const float* x, int64_t n, uint8_t* codes, void* stream);
+/* generic wire conversion f32<->dtype (NDTensor read_f32/write_f32) */
+int epb_convert(const void* src, int32_t src_dtype, void* dst,
+                int32_t dst_dtype, int64_t n, void* stream);
+/* sets *flag (device int32) to 1 if any element is non-finite
+ * (quantize_block's InvalidArgument check, core.py:143-144) */
+int epb_check_finite(const float* x, int64_t n, int32_t* flag, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPB200_H */

@@ -1,0 +1,705 @@
+"""Group / handle lifecycle of the reference API (epsim api.py), driving the
+sm_100a kernels of libepb200.
+
+Same names, argument meaning and error behaviour as epsim.api:
+create_group / EpGroup / EpHandle / HandleState / AllocationHooks and the
+module-level dispatch / combine / complete / get_num_recv_tokens /
+create_handle / destroy_handle / destroy_group.  Tagged-tensor validation
+runs on the host before any kernel is launched (api.py:116-170, 386-426);
+routing validation (ids in range, distinct per row) runs in the routing
+layout kernel and is raised from create_handle.
+
+Extensions (all opt-in through tensor dtypes, the reference forms keep
+working unchanged):
+* dispatch TOKENS input may be f32/bf16/f16 under an FP8 config: the send
+  kernel quantises (block 128, reference tie rule) — no SCALES input then;
+* dispatch TOKENS output may be the wire dtype instead of f32 (plus a SCALES
+  output [L, N*B, H/128] for FP8 with scales) — no f32 widening pass;
+* combine TOKENS input may be bf16 and the combine output f32 or bf16.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from dataclasses import dataclass
+from enum import Enum
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import (FP8_BLOCK, Algorithm, Dtype, EpConfig, EpError, ErrorCode, NDTensor,
+                   TensorTag, raise_status)
+
+ALLOC_ALIGNMENT = 256
+LAYOUTS = ("optimized", "legacy")
+
+
+@dataclass
+class AllocationHooks:
+    """Caller-supplied provider of the group window (api.py:43-55).
+
+    allocate(nbytes, alignment) must return a CUDA uint8 tensor of at least
+    nbytes (or an integer device pointer), or None to refuse; release(buffer)
+    is called once at group destruction or failed setup."""
+
+    allocate: Callable[[int, int], object]
+    release: Callable[[object], None]
+
+
+class HandleState(Enum):
+    CREATED = "Created"
+    DISPATCH_STAGED = "DispatchStaged"
+    DISPATCHED = "Dispatched"
+    COMBINE_STAGED = "CombineStaged"
+    COMBINED = "Combined"
+    DESTROYED = "Destroyed"
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _by_tag(tensors: Sequence[NDTensor], wanted: set, where: str) -> dict:
+    found: dict = {}
+    for t in tensors:
+        if not isinstance(t, NDTensor):
+            raise EpError(ErrorCode.INVALID_ARGUMENT, f"{where}: expected NDTensor, got {type(t).__name__}")
+        if t.tag in found:
+            raise EpError(ErrorCode.TAG_MISMATCH, f"{where}: duplicate tensor for tag {t.tag.value}")
+        found[t.tag] = t
+    missing = wanted - found.keys()
+    if missing:
+        raise EpError(ErrorCode.TAG_MISMATCH, f"{where}: missing {sorted(t.value for t in missing)}")
+    extra = found.keys() - wanted
+    if extra:
+        raise EpError(ErrorCode.TAG_MISMATCH, f"{where}: unexpected {sorted(t.value for t in extra)}")
+    return found
+
+
+def _expect_dtype(t: NDTensor, dtypes, what: str) -> None:
+    dtypes = dtypes if isinstance(dtypes, tuple) else (dtypes,)
+    if t.dtype not in dtypes:
+        raise EpError(ErrorCode.TAG_MISMATCH,
+                      f"{what}: dtype {t.dtype.value}, want {'|'.join(d.value for d in dtypes)}")
+
+
+def _expect_shape(t: NDTensor, shape, what: str) -> None:
+    if tuple(t.shape) != tuple(shape):
+        raise EpError(ErrorCode.SHAPE_MISMATCH, f"{what}: shape {tuple(t.shape)}, want {tuple(shape)}")
+
+
+def _peek_tag(tensors, tag):
+    for t in tensors:
+        if isinstance(t, NDTensor) and t.tag is tag:
+            return t
+    return None
+
+
+@dataclass
+class LLDispatchResult:
+    recv: torch.Tensor          # [L, N*B, H] (valid rows per counts)
+    counts: torch.Tensor        # [L, N] int32 (device)
+    src_info: torch.Tensor      # [L, N*B] int32: t*K + k of each valid row
+    scales: Optional[torch.Tensor] = None
+    _total: Optional[int] = None
+
+    @property
+    def recv_total(self) -> int:
+        if self._total is None:
+            self._total = int(self.counts.sum().item())
+        return self._total
+
+
+@dataclass
+class HTDispatchResult:
+    rows: torch.Tensor          # [recv_total, H] sorted by (expert, src, token)
+    origin: torch.Tensor        # [recv_total, 4] int32 (e, src, t, k)
+    origin_w: torch.Tensor      # [recv_total] f32 weights
+    meta_m: np.ndarray          # [N, E] tokens_per_expert
+    meta_q: np.ndarray          # [N, N] records_per_pair
+    recv_total: int
+
+
+class EpGroup:
+    """One rank's context: config, window, peers, handles (api.py:178-253)."""
+
+    def __init__(self, fabric, rank: int, config: EpConfig, layout: str, cgroup: ctypes.c_void_p,
+                 logical_bytes: int, physical_bytes: int, hooks, hook_buffer, strict: bool):
+        self.fabric = fabric
+        self.rank = rank
+        self.config = config
+        self.layout = layout
+        self._g = cgroup
+        self._logical = logical_bytes
+        self._physical = physical_bytes
+        self._hooks = hooks
+        self._buffer = hook_buffer
+        self._handles: list = []
+        self._next_seq = 0
+        self._ht_round = 0
+        self._ht_open = None
+        self._alive = True
+        self.strict = strict
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    # -- properties -----------------------------------------------------------
+    @property
+    def alive(self) -> bool:
+        return self._alive
+
+    @property
+    def buffer_bytes(self) -> int:
+        """The reference's window size for this config (ll.py:107-121,
+        ht.py:167-174) — footprint parity with the paper."""
+        return self._logical
+
+    @property
+    def physical_bytes(self) -> int:
+        """Bytes actually registered on the device (16-B padded slots)."""
+        return self._physical
+
+    @property
+    def stream(self) -> torch.cuda.Stream:
+        return self.fabric.stream(self.rank)
+
+    def _check_alive(self) -> None:
+        if not self._alive:
+            raise EpError(ErrorCode.HANDLE_STATE_ERROR, "group has been destroyed")
+
+    def _alloc_seq(self) -> int:
+        seq = self._next_seq
+        self._next_seq += 1
+        return seq
+
+    def check(self) -> None:
+        """Synchronise and raise any error the kernels recorded (timeouts,
+        routing validation, weight mismatch)."""
+        code = ctypes.c_int32(0)
+        _lib.call("epb_group_poll_error", self._g, 1, ctypes.byref(code))
+        if code.value:
+            raise_status(code.value, "device-side failure recorded by the EP kernels")
+
+    def set_timeout(self, seconds: float) -> None:
+        _lib.call("epb_group_set_timeout", self._g, int(seconds * 1e9))
+
+    # -- handles ----------------------------------------------------------------
+    def create_handle(self, topk_idx) -> "EpHandle":
+        """Snapshot a routing decision (api.py:218-239).  LL: local; HT:
+        collective (metadata exchange), receive count known on return."""
+        self._check_alive()
+        routing = _validated_routing(topk_idx, self.config, self.device)
+        handle = EpHandle(self, routing)
+        with torch.cuda.stream(self.stream):
+            handle._run_layout()
+            if self.config.algorithm is Algorithm.HT:
+                self._open_ht_round(handle)
+            elif self.strict:
+                self.check()
+        self._handles.append(handle)
+        return handle
+
+    def _open_ht_round(self, handle: "EpHandle") -> None:
+        if self._ht_open is not None and self._ht_open() is not None and self._ht_open()._round_open:
+            raise EpError(ErrorCode.HANDLE_STATE_ERROR, "previous round still open; combine first")
+        rnd = self._ht_round
+        self._ht_round += 1
+        handle._open_round(rnd)
+        self._ht_open = weakref.ref(handle)
+
+    def destroy(self) -> None:
+        """Release the window; all handles must be destroyed (api.py:241-253)."""
+        self._check_alive()
+        live = [h for h in self._handles if h.state is not HandleState.DESTROYED]
+        if live:
+            raise EpError(ErrorCode.HANDLE_STATE_ERROR, f"group still owns {len(live)} live handle(s)")
+        self._alive = False
+        torch.cuda.synchronize(self.device)
+        _lib.call("epb_group_destroy", self._g)
+        self.fabric.registered[self.rank] = 0
+        if self._hooks is not None:
+            self._hooks.release(self._buffer)
+
+
+def _validated_routing(topk_idx, cfg: EpConfig, device) -> torch.Tensor:
+    """Host-side shape/dtype/capacity checks (api.py:150-170); range and
+    distinctness are checked by the routing-layout kernel."""
+    if isinstance(topk_idx, torch.Tensor):
+        r = topk_idx
+        integral = not (r.is_floating_point() or r.is_complex() or r.dtype == torch.bool)
+    else:
+        arr = np.asarray(topk_idx)
+        integral = np.issubdtype(arr.dtype, np.integer) or arr.size == 0
+        r = arr
+    if r.ndim != 2 or r.shape[1] != cfg.top_k:
+        raise EpError(ErrorCode.INVALID_ARGUMENT,
+                      f"topk_idx shape {tuple(r.shape)}, want (tokens, {cfg.top_k})")
+    if r.shape[0] and not integral:
+        raise EpError(ErrorCode.INVALID_ARGUMENT, f"topk_idx dtype {r.dtype} is not integral")
+    b = r.shape[0]
+    if b > cfg.max_tokens_per_rank:
+        raise EpError(ErrorCode.INVALID_ARGUMENT,
+                      f"{b} routed tokens exceed max_tokens_per_rank {cfg.max_tokens_per_rank}")
+    if isinstance(r, np.ndarray):
+        r = torch.from_numpy(np.ascontiguousarray(r.astype(np.int64, copy=False)))
+    return r.to(device=device, dtype=torch.int64).contiguous().clone()
+
+
+def create_group(fabric, rank: int, config: EpConfig, hooks: Optional[AllocationHooks] = None,
+                 layout: str = "optimized", strict: bool = True) -> EpGroup:
+    """Collectively create one rank's group (api.py:256-319).
+
+    Every rank must call with an identical config and layout, or all fail
+    with ConfigMismatch.  The fingerprints are agreed BEFORE any device
+    memory is registered; then each rank allocates its window (library
+    cudaMalloc or `hooks`), the window descriptors are all-gathered and
+    every peer window is mapped (CUDA IPC across processes)."""
+    if not 0 <= rank < config.num_ranks:
+        raise EpError(ErrorCode.INVALID_ARGUMENT, f"rank {rank} outside 0..{config.num_ranks - 1}")
+    topo = fabric.topology
+    if topo.num_ranks != config.num_ranks or topo.ranks_per_node != config.ranks_per_node:
+        raise EpError(ErrorCode.INVALID_ARGUMENT, "fabric topology does not match the config")
+    if layout not in LAYOUTS:
+        raise EpError(ErrorCode.INVALID_ARGUMENT, f"unknown layout {layout!r}")
+    fingerprint = config.fingerprint() + layout.encode()
+    prints = fabric.exchange(rank, fingerprint)
+    if any(p != fingerprint for p in prints):
+        raise EpError(ErrorCode.CONFIG_MISMATCH, "ranks disagree on group config/layout")
+
+    ccfg = config.to_c(layout)
+    info = _lib.WindowInfo()
+    _lib.call("epb_window_geometry", ctypes.byref(ccfg), ctypes.byref(info))
+    buffer, wptr, wbytes = None, 0, 0
+    if hooks is not None:
+        buffer = hooks.allocate(int(info.physical_bytes), ALLOC_ALIGNMENT)
+        if buffer is None:
+            raise EpError(ErrorCode.CAPACITY_EXCEEDED, f"allocation hook refused {info.physical_bytes} bytes")
+        if isinstance(buffer, torch.Tensor):
+            if not buffer.is_cuda:
+                hooks.release(buffer)
+                raise EpError(ErrorCode.INVALID_ARGUMENT, "allocation hook must return device memory")
+            wptr, wbytes = buffer.data_ptr(), buffer.numel() * buffer.element_size()
+        else:
+            wptr, wbytes = int(buffer), int(info.physical_bytes)
+    stream = fabric.stream(rank)
+    cg = ctypes.c_void_p()
+    try:
+        _lib.call("epb_group_create", ctypes.byref(ccfg), rank, ctypes.c_void_p(wptr), wbytes,
+                  ctypes.c_void_p(stream.cuda_stream), ctypes.byref(cg))
+    except BaseException:
+        if hooks is not None:
+            hooks.release(buffer)
+        raise
+    try:
+        if fabric.process_mode:
+            desc = _lib.IpcDesc()
+            _lib.call("epb_group_ipc_desc", cg, ctypes.byref(desc))
+            descs = fabric.exchange(rank, bytes(desc))
+            arr = (_lib.IpcDesc * config.num_ranks)()
+            for r, blob in enumerate(descs):
+                ctypes.memmove(ctypes.byref(arr[r]), blob, ctypes.sizeof(_lib.IpcDesc))
+            _lib.call("epb_group_open_peers", cg, arr)
+            fabric.barrier()
+        else:
+            win, nb = ctypes.c_void_p(), ctypes.c_uint64()
+            _lib.call("epb_group_window", cg, ctypes.byref(win), ctypes.byref(nb))
+            ptrs = fabric.exchange(rank, int(win.value))
+            arr = (ctypes.c_uint64 * config.num_ranks)(*ptrs)
+            _lib.call("epb_group_set_peers", cg, arr)
+    except BaseException:
+        _lib.call("epb_group_destroy", cg)
+        if hooks is not None:
+            hooks.release(buffer)
+        raise
+    fabric.registered[rank] = int(info.physical_bytes)
+    return EpGroup(fabric, rank, config, layout, cg, int(info.logical_bytes), int(info.physical_bytes),
+                   hooks, buffer, strict)
+
+
+def destroy_group(group: EpGroup) -> None:
+    group.destroy()
+
+
+# ---------------------------------------------------------------------------
+# handles
+# ---------------------------------------------------------------------------
+
+
+class EpHandle:
+    """A routing snapshot moving through dispatch/combine rounds
+    (api.py:331-581); owns the state machine and the per-round device state
+    (routing layout, counts, source info / origin)."""
+
+    def __init__(self, group: EpGroup, routing: torch.Tensor):
+        self.group = group
+        self.routing = routing
+        self.state = HandleState.CREATED
+        cfg = group.config
+        dev = group.device
+        self._b = routing.shape[0]
+        n, e, k = cfg.num_ranks, cfg.num_experts, cfg.top_k
+        self._m = torch.empty(e, dtype=torch.int32, device=dev)
+        self._q = torch.empty(n, dtype=torch.int32, device=dev)
+        self._tok_rank = torch.empty(max(self._b, 1) * k, dtype=torch.int32, device=dev)
+        self._tok_slot = torch.empty(max(self._b, 1) * n, dtype=torch.int32, device=dev)
+        self._lay = _lib.Layout(self._m.data_ptr(), self._q.data_ptr(), self._tok_rank.data_ptr(),
+                                self._tok_slot.data_ptr(), self._b)
+        self._seq: Optional[int] = None
+        self._round: Optional[int] = None
+        self._round_open = False
+        self._meta = None
+        self._staged = None
+        self._dispatch_result = None
+        self._combine_stats = None
+        self._weights = None
+        # LL per-round device state
+        self._counts_i32 = None
+        self._src_info = None
+
+    @property
+    def config(self) -> EpConfig:
+        return self.group.config
+
+    @property
+    def num_tokens(self) -> int:
+        return self._b
+
+    def _require(self, states: tuple, verb: str) -> None:
+        if self.state not in states:
+            raise EpError(ErrorCode.HANDLE_STATE_ERROR, f"cannot {verb} in state {self.state.value}")
+
+    def _sp(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p(self.group.stream.cuda_stream)
+
+    def _run_layout(self) -> None:
+        _lib.call("epb_routing_layout", self.group._g, _ptr(self.routing), self._b,
+                  ctypes.byref(self._lay), self._sp())
+
+    # -- HT metadata round ------------------------------------------------------
+    def _open_round(self, rnd: int) -> None:
+        g = self.group
+        cfg = g.config
+        n, e = cfg.num_ranks, cfg.num_experts
+        dev = g.device
+        self._round = rnd
+        meta = torch.empty((n, e + n), dtype=torch.int32, device=dev)
+        offsets = torch.empty((e, n), dtype=torch.int32, device=dev)
+        total = torch.empty(1, dtype=torch.int32, device=dev)
+        _lib.call("epb_ht_meta_send", g._g, rnd, ctypes.byref(self._lay), self._sp())
+        g.fabric.phase(g.rank)
+        _lib.call("epb_ht_meta_recv", g._g, rnd, _ptr(meta), _ptr(offsets), _ptr(total), self._sp())
+        g.check()  # synchronises: receive shapes are host-known on return (api.py:235-237)
+        meta_h = meta.cpu().numpy()
+        self._meta = dict(m=meta_h[:, :e].astype(np.int64), q=meta_h[:, e:].astype(np.int64),
+                          recv_total=int(total.item()), offsets=offsets)
+        self._round_open = True
+
+    # -- staging helpers ----------------------------------------------------------
+    def _dev_in(self, t: NDTensor) -> torch.Tensor:
+        v = t.view()
+        if v.device != self.group.device:
+            v = v.to(self.group.device, non_blocking=True)
+        return v.contiguous()
+
+    def _dev_out(self, t: NDTensor):
+        """(device tensor to write, needs_copy_back)."""
+        v = t.view()
+        if v.device == self.group.device and v.is_contiguous():
+            return v, False
+        # rows the kernels do not write keep the caller's contents
+        return v.to(self.group.device, non_blocking=True).contiguous(), True
+
+    # -- dispatch -----------------------------------------------------------------
+    def dispatch(self, inputs: Sequence[NDTensor], outputs: Sequence[NDTensor],
+                 send_only: bool = False) -> None:
+        """Move tokens to their experts (api.py:361-453)."""
+        cfg = self.config
+        g = self.group
+        g._check_alive()
+        self._require((HandleState.CREATED, HandleState.COMBINED), "dispatch")
+        ht = cfg.algorithm is Algorithm.HT
+        if ht and send_only:
+            raise EpError(ErrorCode.INVALID_ARGUMENT, "send_only staging is an LL feature")
+        b = self._b
+        tok_peek = _peek_tag(inputs, TensorTag.TOKENS)
+        quant_in_kernel = (cfg.token_dtype is Dtype.FP8 and tok_peek is not None
+                           and tok_peek.dtype in (Dtype.F32, Dtype.BF16, Dtype.F16))
+        in_want = {TensorTag.TOKENS}
+        if cfg.with_scales and not quant_in_kernel:
+            in_want.add(TensorTag.SCALES)
+        if ht:
+            in_want.add(TensorTag.TOPK_WEIGHTS)
+        named_in = _by_tag(inputs, in_want, "dispatch input")
+        out_peek = _peek_tag(outputs, TensorTag.TOKENS)
+        wire_out = out_peek is not None and out_peek.dtype is cfg.token_dtype and \
+            cfg.token_dtype is not Dtype.F32
+        counter_tag = TensorTag.TOKENS_PER_EXPERTS if ht else (
+            TensorTag.RECV_EXPERT_COUNTER_DEVICE
+            if _peek_tag(outputs, TensorTag.RECV_EXPERT_COUNTER_DEVICE) is not None
+            else TensorTag.RECV_EXPERT_COUNTER_HOST)
+        out_want = {TensorTag.TOKENS, counter_tag}
+        if wire_out and cfg.with_scales:
+            out_want.add(TensorTag.SCALES)
+        named_out = _by_tag(outputs, out_want, "dispatch output")
+
+        tokens = named_in[TensorTag.TOKENS]
+        if quant_in_kernel:
+            _expect_dtype(tokens, (Dtype.F32, Dtype.BF16, Dtype.F16), "dispatch TOKENS input")
+        else:
+            _expect_dtype(tokens, cfg.token_dtype, "dispatch TOKENS input")
+        _expect_shape(tokens, (b, cfg.hidden), "dispatch TOKENS input")
+        scales = None
+        if TensorTag.SCALES in named_in:
+            scales = named_in[TensorTag.SCALES]
+            _expect_dtype(scales, Dtype.F32, "SCALES")
+            _expect_shape(scales, (b, cfg.hidden // FP8_BLOCK), "SCALES")
+        weights = None
+        if ht:
+            weights = named_in[TensorTag.TOPK_WEIGHTS]
+            _expect_dtype(weights, Dtype.F32, "TOPK_WEIGHTS")
+            _expect_shape(weights, (b, cfg.top_k), "TOPK_WEIGHTS")
+        ell, n = cfg.experts_per_rank, cfg.num_ranks
+        out_tokens = named_out[TensorTag.TOKENS]
+        out_counts = named_out[counter_tag]
+        _expect_dtype(out_tokens, (Dtype.F32, cfg.token_dtype), "dispatch TOKENS output")
+        _expect_dtype(out_counts, Dtype.F32, f"{counter_tag.value} output")
+        _expect_shape(out_counts, (ell, n), f"{counter_tag.value} output")
+        out_scales = named_out.get(TensorTag.SCALES)
+        if ht:
+            if not self._round_open:
+                # handle reuse (e.g. backward): a fresh collective round
+                with torch.cuda.stream(g.stream):
+                    g._open_ht_round(self)
+            _expect_shape(out_tokens, (self._meta["recv_total"], cfg.hidden), "dispatch TOKENS output")
+        else:
+            _expect_shape(out_tokens, (ell, n * cfg.max_tokens_per_rank, cfg.hidden),
+                          "dispatch TOKENS output")
+        if out_scales is not None:
+            _expect_dtype(out_scales, Dtype.F32, "SCALES output")
+            _expect_shape(out_scales, tuple(out_tokens.shape[:-1]) + (cfg.hidden // FP8_BLOCK,),
+                          "SCALES output")
+
+        with torch.cuda.stream(g.stream):
+            if ht:
+                self._ht_dispatch(tokens, weights, out_tokens, out_counts)
+                return
+            x = self._dev_in(tokens)
+            xs = self._dev_in(scales) if scales is not None else None
+            seq = g._alloc_seq()
+            self._seq = seq
+            x_code = tokens.dtype.code
+            _lib.call("epb_ll_dispatch_send", g._g, seq, _ptr(x), x_code, _ptr(xs), _ptr(self.routing),
+                      ctypes.byref(self._lay), self._sp())
+            self._keep_alive = (x, xs)
+            self._staged = (out_tokens, out_counts, out_scales)
+            if send_only:
+                self.state = HandleState.DISPATCH_STAGED
+                return
+            g.fabric.phase(g.rank)
+            self._ll_recv()
+
+    def _ll_recv(self) -> None:
+        g = self.group
+        cfg = g.config
+        out_tokens, out_counts, out_scales = self._staged
+        self._staged = None
+        ell, n = cfg.experts_per_rank, cfg.num_ranks
+        dev = g.device
+        out_t, back_t = self._dev_out(out_tokens)
+        out_s, back_s = self._dev_out(out_scales) if out_scales is not None else (None, False)
+        cnt_f, back_c = self._dev_out(out_counts)
+        self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
+        self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
+        _lib.call("epb_ll_dispatch_recv", g._g, self._seq, _ptr(out_t), out_tokens.dtype.code, _ptr(out_s),
+                  _ptr(cnt_f), _ptr(self._counts_i32), _ptr(self._src_info), self._sp())
+        if g.strict:
+            g.check()
+        if back_t:
+            out_tokens.view().copy_(out_t)
+        if back_s:
+            out_scales.view().copy_(out_s)
+        if back_c:
+            out_counts.view().copy_(cnt_f)
+        self._dispatch_result = LLDispatchResult(out_t, self._counts_i32, self._src_info, out_s)
+        self._keep_alive = None
+        self.state = HandleState.DISPATCHED
+
+    def _ht_dispatch(self, tokens, weights, out_tokens, out_counts) -> None:
+        g = self.group
+        cfg = g.config
+        meta = self._meta
+        x = self._dev_in(tokens)
+        w = self._dev_in(weights)
+        self._weights = w.clone()
+        rnd = self._round
+        _lib.call("epb_ht_dispatch_send", g._g, rnd, _ptr(x), tokens.dtype.code, _ptr(w), _ptr(self.routing),
+                  ctypes.byref(self._lay), _ptr(meta["offsets"]), self._sp())
+        g.fabric.phase(g.rank)
+        total = meta["recv_total"]
+        out_t, back_t = self._dev_out(out_tokens)
+        origin = torch.empty((max(total, 1), 4), dtype=torch.int32, device=g.device)
+        origin_w = torch.empty(max(total, 1), dtype=torch.float32, device=g.device)
+        _lib.call("epb_ht_dispatch_recv", g._g, rnd, _ptr(out_t), out_tokens.dtype.code, _ptr(origin),
+                  _ptr(origin_w), self._sp())
+        if g.strict:
+            g.check()
+        if back_t:
+            out_tokens.view().copy_(out_t)
+        ell, n = cfg.experts_per_rank, cfg.num_ranks
+        lo = g.rank * ell
+        hi = min(lo + ell, cfg.num_experts)
+        counts = np.zeros((ell, n), dtype=np.float32)
+        counts[:hi - lo] = meta["m"][:, lo:hi].T
+        out_counts.view().copy_(torch.from_numpy(counts))
+        self._round_open = False
+        self._dispatch_result = HTDispatchResult(out_t, origin[:total], origin_w[:total], meta["m"],
+                                                 meta["q"], total)
+        self.state = HandleState.DISPATCHED
+
+    # -- combine ------------------------------------------------------------------
+    def combine(self, inputs: Sequence[NDTensor], outputs: Sequence[NDTensor],
+                send_only: bool = False) -> None:
+        """Return weighted expert outputs to this rank's tokens (api.py:463-519)."""
+        cfg = self.config
+        g = self.group
+        g._check_alive()
+        self._require((HandleState.DISPATCHED,), "combine")
+        ht = cfg.algorithm is Algorithm.HT
+        if ht and send_only:
+            raise EpError(ErrorCode.INVALID_ARGUMENT, "send_only staging is an LL feature")
+        b = self._b
+        named_in = _by_tag(inputs, {TensorTag.TOKENS, TensorTag.TOPK_WEIGHTS}, "combine input")
+        named_out = _by_tag(outputs, {TensorTag.TOKENS}, "combine output")
+        rows_in = named_in[TensorTag.TOKENS]
+        _expect_dtype(rows_in, (Dtype.F32, Dtype.BF16), "combine TOKENS input")
+        wt = named_in[TensorTag.TOPK_WEIGHTS]
+        _expect_dtype(wt, Dtype.F32, "TOPK_WEIGHTS")
+        _expect_shape(wt, (b, cfg.top_k), "TOPK_WEIGHTS")
+        out = named_out[TensorTag.TOKENS]
+        _expect_dtype(out, (Dtype.F32, Dtype.BF16), "combine TOKENS output")
+        _expect_shape(out, (b, cfg.hidden), "combine TOKENS output")
+        ell, n = cfg.experts_per_rank, cfg.num_ranks
+        if ht:
+            _expect_shape(rows_in, (self._meta["recv_total"], cfg.hidden), "combine TOKENS input")
+        else:
+            _expect_shape(rows_in, (ell, n * cfg.max_tokens_per_rank, cfg.hidden), "combine TOKENS input")
+        with torch.cuda.stream(g.stream):
+            y = self._dev_in(rows_in)
+            w = self._dev_in(wt)
+            if ht:
+                self._ht_combine(y, rows_in.dtype, w, out)
+                return
+            _lib.call("epb_ll_combine_send", g._g, self._seq, _ptr(y), rows_in.dtype.code,
+                      _ptr(self._counts_i32), _ptr(self._src_info), self._sp())
+            self._staged = (out, w, y)
+            if send_only:
+                self.state = HandleState.COMBINE_STAGED
+                return
+            g.fabric.phase(g.rank)
+            self._ll_combine_recv()
+
+    def _ll_combine_recv(self) -> None:
+        g = self.group
+        out, w, _y = self._staged
+        self._staged = None
+        o, back = self._dev_out(out)
+        _lib.call("epb_ll_combine_recv", g._g, self._seq, _ptr(w), self._b, _ptr(o), out.dtype.code,
+                  self._sp())
+        if g.strict:
+            g.check()
+        if back:
+            out.view().copy_(o)
+        self._combine_stats = {"op": "combine"}
+        self.state = HandleState.COMBINED
+
+    def _ht_combine(self, y, y_dtype, w, out) -> None:
+        g = self.group
+        res = self._dispatch_result
+        # combine weights must equal the dispatched ones (ht.py:605-609),
+        # checked on the device before any combine traffic
+        _lib.call("epb_weights_equal", g._g, _ptr(w), _ptr(self._weights), w.numel(), self._sp())
+        if g.strict:
+            g.check()
+        _lib.call("epb_ht_combine_send", g._g, self._round, _ptr(y), y_dtype.code, _ptr(res.origin),
+                  res.recv_total, self._sp())
+        g.fabric.phase(g.rank)
+        o, back = self._dev_out(out)
+        _lib.call("epb_ht_combine_recv", g._g, self._round, _ptr(self.routing), _ptr(w), self._b, _ptr(o),
+                  out.dtype.code, self._sp())
+        if g.strict:
+            g.check()
+        if back:
+            out.view().copy_(o)
+        self._combine_stats = {"op": "combine"}
+        self.state = HandleState.COMBINED
+
+    def complete(self) -> None:
+        """Finish a staged LL dispatch or combine (api.py:521-540)."""
+        g = self.group
+        g._check_alive()
+        if self.state is HandleState.DISPATCH_STAGED:
+            with torch.cuda.stream(g.stream):
+                g.fabric.phase(g.rank)
+                self._ll_recv()
+            return
+        if self.state is HandleState.COMBINE_STAGED:
+            with torch.cuda.stream(g.stream):
+                g.fabric.phase(g.rank)
+                self._ll_combine_recv()
+            return
+        raise EpError(ErrorCode.HANDLE_STATE_ERROR, f"nothing staged to complete in state {self.state.value}")
+
+    # -- queries --------------------------------------------------------------------
+    def get_num_recv_tokens(self) -> int:
+        """HT: known at creation; LL: after dispatch completes (api.py:544-559)."""
+        if self.state is HandleState.DESTROYED:
+            raise EpError(ErrorCode.HANDLE_STATE_ERROR, "handle destroyed")
+        if self.config.algorithm is Algorithm.HT:
+            return self._meta["recv_total"]
+        valid = (HandleState.DISPATCHED, HandleState.COMBINE_STAGED, HandleState.COMBINED)
+        if self.state not in valid or self._dispatch_result is None:
+            raise EpError(ErrorCode.HANDLE_STATE_ERROR, "LL receive count is known after dispatch completes")
+        return self._dispatch_result.recv_total
+
+    @property
+    def dispatch_result(self):
+        return self._dispatch_result
+
+    @property
+    def combine_stats(self):
+        return self._combine_stats
+
+    def destroy(self) -> None:
+        """Retire the handle; legal only with no round in flight."""
+        self._require((HandleState.CREATED, HandleState.COMBINED), "destroy handle")
+        if self._round_open:
+            self._round_open = False  # metadata went out, payload never followed
+        self.state = HandleState.DESTROYED
+
+
+def create_handle(group: EpGroup, topk_idx) -> EpHandle:
+    return group.create_handle(topk_idx)
+
+
+def destroy_handle(handle: EpHandle) -> None:
+    handle.destroy()
+
+
+def dispatch(handle: EpHandle, inputs, outputs, send_only: bool = False) -> None:
+    handle.dispatch(inputs, outputs, send_only=send_only)
+
+
+def combine(handle: EpHandle, inputs, outputs, send_only: bool = False) -> None:
+    handle.combine(inputs, outputs, send_only=send_only)
+
+
+def complete(handle: EpHandle) -> None:
+    handle.complete()
+
+
+def get_num_recv_tokens(handle: EpHandle) -> int:
+    return handle.get_num_recv_tokens()

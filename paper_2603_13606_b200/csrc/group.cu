@@ -1,0 +1,239 @@
+// Group lifecycle: window allocation, CUDA-IPC peer mapping, error word.
+// Replaces epsim's Fabric.register_window + _Rendezvous (fabric.py:120-132,
+// api.py:67-94, 256-319): the host all-gathers epb_ipc_desc records (over a
+// torch.distributed group) and every rank maps every peer window once.
+#include <cuda.h>
+#include <stdio.h>
+#include <string.h>
+#include <unistd.h>
+
+#include <string>
+
+#include "internal.h"
+
+namespace epb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  return fail(EPB_CUDA_ERROR, m);
+}
+
+static int validate_config(const epb_config* c) {
+  if (!c) return fail(EPB_INVALID_ARGUMENT, "null config");
+  if (c->num_ranks < 1 || c->num_ranks > kMaxRanksHost)
+    return fail(EPB_INVALID_ARGUMENT, "num_ranks outside [1, 64]");
+  if (c->top_k < 1 || c->top_k > c->num_experts || c->top_k > 32)
+    return fail(EPB_INVALID_ARGUMENT, "top_k outside [1, min(E, 32)]");
+  if (c->ranks_per_node < 1 || c->num_ranks % c->ranks_per_node)
+    return fail(EPB_INVALID_ARGUMENT, "ranks_per_node must divide num_ranks");
+  if (c->num_experts < c->num_ranks) return fail(EPB_INVALID_ARGUMENT, "num_experts < num_ranks");
+  if (c->hidden < 1 || c->max_tokens_per_rank < 1)
+    return fail(EPB_INVALID_ARGUMENT, "hidden / max_tokens_per_rank < 1");
+  if (c->max_tokens_per_rank >= (1 << 20))
+    return fail(EPB_INVALID_ARGUMENT, "max_tokens_per_rank must be < 2^20");
+  if (c->token_dtype < EPB_F32 || c->token_dtype > EPB_FP8)
+    return fail(EPB_INVALID_ARGUMENT, "token_dtype");
+  if (c->with_scales && (c->token_dtype != EPB_FP8 || c->hidden % 128))
+    return fail(EPB_INVALID_ARGUMENT, "with_scales requires fp8 and hidden % 128 == 0");
+  if (c->algorithm == EPB_HT && c->token_dtype == EPB_FP8)
+    return fail(EPB_INVALID_ARGUMENT, "fp8 token dtype is not supported by the HT algorithm");
+  if (c->algorithm != EPB_LL && c->algorithm != EPB_HT)
+    return fail(EPB_INVALID_ARGUMENT, "algorithm");
+  if (c->combine_dtype < -1 || c->combine_dtype > EPB_FP8)
+    return fail(EPB_INVALID_ARGUMENT, "combine_dtype");
+  if (c->layout != EPB_LAYOUT_OPTIMIZED && c->layout != EPB_LAYOUT_LEGACY)
+    return fail(EPB_INVALID_ARGUMENT, "layout");
+  return EPB_OK;
+}
+
+}  // namespace epb
+
+using namespace epb;
+
+extern "C" {
+
+int epb_version(void) { return 1; }
+
+const char* epb_last_error(void) { return g_last_error.c_str(); }
+
+int epb_window_geometry(const epb_config* cfg, epb_window_info* out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (cfg->algorithm == EPB_LL) {
+    LLGeom g;
+    make_ll_geom(*cfg, g);
+    out->physical_bytes = g.window_bytes;
+    out->logical_bytes = g.logical_bytes;
+  } else {
+    HTGeom g;
+    make_ht_geom(*cfg, g);
+    out->physical_bytes = g.window_bytes;
+    out->logical_bytes = g.logical_bytes;
+  }
+  return EPB_OK;
+}
+
+int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t window_bytes,
+                     void* stream, epb_group** out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (rank < 0 || rank >= cfg->num_ranks) return fail(EPB_INVALID_ARGUMENT, "rank out of range");
+  epb_group* g = new epb_group();
+  g->cfg = *cfg;
+  g->rank = rank;
+  make_ll_geom(*cfg, g->ll);
+  make_ht_geom(*cfg, g->ht);
+  const uint64_t need = cfg->algorithm == EPB_LL ? g->ll.window_bytes : g->ht.window_bytes;
+  cudaGetDevice(&g->device);
+  cudaStream_t s = as_stream(stream);
+  auto cleanup = [&](int code) {
+    if (g->owns_window && g->window) cudaFree(g->window);
+    if (g->d_peers) cudaFree(g->d_peers);
+    if (g->d_err) cudaFree(g->d_err);
+    if (g->d_done) cudaFree(g->d_done);
+    if (g->d_scratch) cudaFree(g->d_scratch);
+    delete g;
+    return code;
+  };
+  if (window) {
+    if (window_bytes < need)
+      return cleanup(fail(EPB_CAPACITY_EXCEEDED, "window smaller than the physical geometry"));
+    if (reinterpret_cast<uintptr_t>(window) % 256)
+      return cleanup(fail(EPB_INVALID_ARGUMENT, "window must be 256-byte aligned"));
+    g->window = reinterpret_cast<uint8_t*>(window);
+    g->window_bytes = window_bytes;
+  } else {
+    cudaError_t e = cudaMalloc(&g->window, need);
+    if (e != cudaSuccess) return cleanup(cuda_check(e, "cudaMalloc(window)"));
+    g->owns_window = true;
+    g->window_bytes = need;
+  }
+  const int n = cfg->num_ranks;
+  const int l = experts_per_rank(cfg->num_experts, n);
+  cudaError_t e = cudaMalloc(&g->d_peers, sizeof(uint64_t) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_err, sizeof(int) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_done, sizeof(int) * 4 * n);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_scratch, sizeof(int) * (8 * n + 2 * l * n + 64));
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->window, 0, g->window_bytes, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->d_err, 0, sizeof(int) * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->d_done, 0, sizeof(int) * 4 * n, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->d_scratch, 0, sizeof(int) * (8 * n + 2 * l * n + 64), s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cleanup(cuda_check(e, "group setup"));
+  if (const char* t = getenv("EPB_TIMEOUT_MS")) g->timeout_ns = strtoull(t, nullptr, 10) * 1000000ull;
+  // a single rank is its own peer
+  if (n == 1) {
+    uint64_t self = reinterpret_cast<uint64_t>(g->window);
+    e = cudaMemcpy(g->d_peers, &self, sizeof(self), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cleanup(cuda_check(e, "peer table"));
+    g->peers_ready = true;
+  }
+  *out = g;
+  return EPB_OK;
+}
+
+int epb_group_window(epb_group* g, void** window, uint64_t* bytes) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  *window = g->window;
+  *bytes = g->window_bytes;
+  return EPB_OK;
+}
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int epb_group_ipc_desc(epb_group* g, epb_ipc_desc* out) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  memset(out, 0, sizeof(*out));
+  void* base = g->window;
+  if (!g->owns_window) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    EPB_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn) return fail(EPB_CUDA_ERROR, "cuMemGetAddressRange unavailable");
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (((PFN_getAddressRange)fn)(&b, &sz, reinterpret_cast<CUdeviceptr>(g->window)) != CUDA_SUCCESS)
+      return fail(EPB_CUDA_ERROR, "cuMemGetAddressRange failed");
+    base = reinterpret_cast<void*>(b);
+  }
+  g->alloc_base = base;
+  cudaIpcMemHandle_t h;
+  EPB_CUDA(cudaIpcGetMemHandle(&h, base));
+  memcpy(out->handle, &h, sizeof(h));
+  out->offset = reinterpret_cast<uint8_t*>(g->window) - reinterpret_cast<uint8_t*>(base);
+  out->bytes = g->window_bytes;
+  out->device = g->device;
+  out->pid = (int32_t)getpid();
+  return EPB_OK;
+}
+
+int epb_group_open_peers(epb_group* g, const epb_ipc_desc* descs) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  const int n = g->cfg.num_ranks;
+  std::vector<uint64_t> ptrs(n);
+  for (int r = 0; r < n; ++r) {
+    if (r == g->rank) {
+      ptrs[r] = reinterpret_cast<uint64_t>(g->window);
+      continue;
+    }
+    if (descs[r].bytes < g->window_bytes)
+      return fail(EPB_CONFIG_MISMATCH, "peer window smaller than ours");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, descs[r].handle, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_check(e, "cudaIpcOpenMemHandle");
+    g->ipc_opened.push_back(p);
+    ptrs[r] = reinterpret_cast<uint64_t>(p) + descs[r].offset;
+  }
+  EPB_CUDA(cudaMemcpy(g->d_peers, ptrs.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice));
+  g->peers_ready = true;
+  return EPB_OK;
+}
+
+int epb_group_set_peers(epb_group* g, const uint64_t* peer_windows) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  EPB_CUDA(cudaMemcpy(g->d_peers, peer_windows, sizeof(uint64_t) * g->cfg.num_ranks,
+                      cudaMemcpyHostToDevice));
+  g->peers_ready = true;
+  return EPB_OK;
+}
+
+int epb_group_set_timeout(epb_group* g, uint64_t timeout_ns) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  g->timeout_ns = timeout_ns;
+  return EPB_OK;
+}
+
+int epb_group_poll_error(epb_group* g, int clear, int32_t* code) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  int v = 0;
+  EPB_CUDA(cudaMemcpy(&v, g->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  *code = v;
+  if (clear && v) EPB_CUDA(cudaMemset(g->d_err, 0, sizeof(int)));
+  return EPB_OK;
+}
+
+int epb_group_destroy(epb_group* g) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  cudaDeviceSynchronize();
+  for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (g->owns_window) cudaFree(g->window);
+  cudaFree(g->d_peers);
+  cudaFree(g->d_err);
+  cudaFree(g->d_done);
+  cudaFree(g->d_scratch);
+  delete g;
+  return EPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,657 @@
+// High-Throughput dispatch/combine kernels (K5a meta, K5b dispatch, K6 combine).
+//
+// Reference semantics (epsim ht.py):
+//  * metadata (ht.py:291-331): every rank all-gathers m_row[E] (tokens per
+//    expert) and q_row[N] (dedup tokens per destination) before any payload;
+//    receive shapes and the sorted-output offsets follow from them
+//    (HTMeta.expert_offsets, ht.py:185-193).
+//  * dispatch (ht.py:381-468, 553-583): one record per (token, destination
+//    rank) = header + K f32 weights + row; the receiver places a copy of the
+//    row for every local expert it names, sorted by (local expert, src, t).
+//    Here the sender also writes, per k, the final output row on the owner
+//    (offset(e, src) + rank of t within (e, src)), so the receiver's
+//    placement is a parallel scatter that never depends on arrival order.
+//  * combine (ht.py:587-735): p = f32(w * y) from the f32 expert row; per
+//    token, per node holding its experts (ascending), a partial = first p
+//    then f32 adds in ascending k; out = f32(0 + partial_0) + partial_1 ...
+//    Expert rows travel in their own dtype (f32, or bf16 which widens
+//    exactly) and the home rank forms p, so the product is bit-identical.
+//  * single-node transport only: the reference's rail FIFOs / forwarders
+//    (ht.py:479-551) are out of scope on one NVSwitch domain, but the
+//    hierarchical SUM ORDER is reproduced for any ranks_per_node.
+#include "common.cuh"
+#include "internal.h"
+
+namespace epb {
+
+EPB_DEV uint8_t* hpeer(const uint64_t* peers, int r) { return reinterpret_cast<uint8_t*>(peers[r]); }
+
+EPB_DEV void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// K5a: metadata all-gather over the windows
+// ---------------------------------------------------------------------------
+struct HTMetaSend {
+  const int32_t* m;
+  const int32_t* q;
+  const uint64_t* peers;
+  HTGeom g;
+  int rank, parity;
+  uint32_t tag;
+};
+
+__global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
+  const HTGeom& g = p.g;
+  const int C = g.E + g.N;
+  const uint64_t row_off = g.meta + ((uint64_t)p.parity * g.N + p.rank) * C * 4;
+  for (int i = threadIdx.x; i < g.N * C; i += blockDim.x) {
+    const int d = i / C, c = i % C;
+    const int32_t v = c < g.E ? p.m[c] : p.q[c - g.E];
+    reinterpret_cast<int32_t*>(hpeer(p.peers, d) + row_off)[c] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < g.N) {
+    fence_sys();
+    uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, threadIdx.x) + g.meta_flag) +
+                     p.parity * g.N + p.rank;
+    st_relaxed_sys_u64(flag, (uint64_t)p.tag);
+  }
+}
+
+struct HTMetaRecv {
+  const uint8_t* win;
+  int32_t* meta_out;
+  int32_t* offsets;
+  int32_t* recv_total;
+  int* err;
+  HTGeom g;
+  uint64_t timeout_ns;
+  int rank, parity;
+  uint32_t tag;
+};
+
+__global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
+  extern __shared__ int32_t s_meta[];  // [N][C]
+  __shared__ int s_fail;
+  const HTGeom& g = p.g;
+  const int N = g.N, E = g.E, C = E + N, L = g.L;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.meta_flag) + p.parity * N;
+  for (int s = threadIdx.x; s < N; s += blockDim.x) {
+    uint64_t v;
+    if (!wait_tag(&flags[s], p.tag, 0, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+  }
+  __syncthreads();
+  if (s_fail) return;
+  const int32_t* rows = reinterpret_cast<const int32_t*>(p.win + g.meta + (uint64_t)p.parity * N * C * 4);
+  for (int i = threadIdx.x; i < N * C; i += blockDim.x) {
+    const int32_t v = *reinterpret_cast<const volatile int32_t*>(&rows[i]);
+    s_meta[i] = v;
+    p.meta_out[i] = v;
+  }
+  __syncthreads();
+  // offsets[e, s]: row of group (e, s) inside owner(e)'s sorted output
+  // = (rows of earlier local experts of owner(e)) + (rows of e from src < s)
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int lo = (e / L) * L;
+    int base = 0;
+    for (int e2 = lo; e2 < e; ++e2)
+      for (int s = 0; s < N; ++s) base += s_meta[s * C + e2];
+    for (int s = 0; s < N; ++s) {
+      p.offsets[e * N + s] = base;
+      base += s_meta[s * C + e];
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int lo = p.rank * L, hi = min(lo + L, E);
+    int tot = 0;
+    for (int e = lo; e < hi; ++e)
+      for (int s = 0; s < N; ++s) tot += s_meta[s * C + e];
+    *p.recv_total = tot;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5b: dispatch
+// ---------------------------------------------------------------------------
+struct HTSend {
+  const void* x;
+  const float* w;
+  const int64_t* topk;
+  const int32_t* q;
+  const int32_t* tok_rank;
+  const int32_t* tok_slot;
+  const int32_t* offsets;  // [E, N]
+  const uint64_t* peers;
+  int* done;
+  HTGeom g;
+  int b, rank;
+  uint32_t tag;
+};
+
+EPB_DEV void ht_publish_records(const HTSend& p, int d) {
+  uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, d) + p.g.dflag) + p.rank;
+  st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | (uint32_t)p.q[d]);
+}
+
+template <int XT, int WT>
+__global__ void __launch_bounds__(512) ht_dispatch_send_kernel(HTSend p) {
+  __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks], s_nd;
+  __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
+  __shared__ float s_w[kMaxTopK];
+  __shared__ int s_cnt[kMaxRanks];
+  const HTGeom& g = p.g;
+  const int K = g.K, N = g.N, H = g.H, L = g.L;
+  if (threadIdx.x < N) s_cnt[threadIdx.x] = 0;
+  for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int nd = 0;
+      for (int d = 0; d < N; ++d) {
+        const int j = p.tok_slot[(int64_t)t * N + d];
+        if (j >= 0) { s_dst[nd] = d; s_j[nd] = j; ++nd; s_cnt[d] += 1; }
+      }
+      s_nd = nd;
+      s_hdr[0] = (uint32_t)t;
+      s_hdr[1] = (uint32_t)K;
+    }
+    if (threadIdx.x < K) {
+      const int e = (int)p.topk[(int64_t)t * K + threadIdx.x];
+      s_hdr[2 + threadIdx.x] = (uint32_t)e;
+      s_hdr[2 + K + threadIdx.x] =
+          (uint32_t)(p.offsets[e * N + p.rank] + p.tok_rank[(int64_t)t * K + threadIdx.x]);
+      s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
+    }
+    __syncthreads();
+    const int nd = s_nd;
+    const int64_t rec0 = (int64_t)p.rank * g.B;
+    // weights + header + positions
+    for (int wd = threadIdx.x; wd < K + 2 + 2 * K; wd += blockDim.x) {
+      for (int i = 0; i < nd; ++i) {
+        uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
+        if (wd < K) reinterpret_cast<float*>(rec + g.RBp)[wd] = s_w[wd];
+        else reinterpret_cast<uint32_t*>(rec + g.RBp + g.WBp)[wd - K] = s_hdr[wd - K];
+      }
+    }
+    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * dtype_width(XT);
+    if ((H & 15) == 0) {
+      constexpr int EPC = Elems<WT>::n;
+      for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
+        float f[EPC];
+        load_elems_vec<XT, EPC>(xrow, (int64_t)c * EPC, f);
+        const int4 v = pack16<WT>(f);
+        for (int i = 0; i < nd; ++i) {
+          uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
+          st_na_v4(rec + (int64_t)c * 16, v);
+        }
+      }
+    } else {
+      for (int el = threadIdx.x; el < H; el += blockDim.x) {
+        const float f = load_elem(xrow, XT, el);
+        for (int i = 0; i < nd; ++i) {
+          uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
+          store_elem(rec, WT, el, f);
+        }
+      }
+    }
+    (void)L;
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    const int d = threadIdx.x;
+    const int c = s_cnt[d];
+    if (c > 0) {
+      fence_sys();
+      const int old = atomicAdd(&p.done[d], c);
+      if (old + c == p.q[d]) {
+        p.done[d] = 0;
+        fence_sys();
+        ht_publish_records(p, d);
+      }
+    } else if (blockIdx.x == 0 && p.q[d] == 0) {
+      ht_publish_records(p, d);
+    }
+  }
+}
+
+struct HTRecv {
+  void* out;
+  int32_t* origin;
+  float* origin_w;
+  const uint8_t* win;
+  int* err;
+  HTGeom g;
+  uint64_t timeout_ns;
+  int rank;
+  uint32_t tag;
+};
+
+template <int WT, int OT>
+__global__ void __launch_bounds__(256) ht_dispatch_recv_kernel(HTRecv p) {
+  __shared__ int s_pre[kMaxRanks + 1], s_q[kMaxRanks];
+  __shared__ int s_fail;
+  const HTGeom& g = p.g;
+  const int N = g.N, K = g.K, H = g.H, L = g.L;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
+  for (int s = threadIdx.x; s < N; s += blockDim.x) {
+    uint64_t v = 0;
+    if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    s_q[s] = (int)(v & 0xFFFFFFFFu);
+  }
+  __syncthreads();
+  if (s_fail) return;
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int s = 0; s < N; ++s) { s_pre[s] = run; run += s_q[s]; }
+    s_pre[N] = run;
+  }
+  __syncthreads();
+  const int total = s_pre[N];
+  const int lo = p.rank * L, hi = min(lo + L, g.E);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int ob = dtype_width(OT);
+  for (int f = blockIdx.x * nw + warp; f < total; f += gridDim.x * nw) {
+    int s = 0;
+    while (s_pre[s + 1] <= f) ++s;
+    const int j = f - s_pre[s];
+    const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
+    const float* wts = reinterpret_cast<const float*>(rec + g.RBp);
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
+    const uint32_t t = hdr[0];
+    for (int k = 0; k < K; ++k) {
+      const int e = (int)hdr[2 + k];
+      if (e < lo || e >= hi) continue;
+      const int64_t pos = hdr[2 + K + k];
+      if (lane == 0) {
+        p.origin[pos * 4 + 0] = e;
+        p.origin[pos * 4 + 1] = s;
+        p.origin[pos * 4 + 2] = (int32_t)t;
+        p.origin[pos * 4 + 3] = k;
+        p.origin_w[pos] = wts[k];
+      }
+      uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + pos * H * ob;
+      if ((H & 15) == 0) {
+        constexpr int EPC = Elems<WT>::n;
+        if constexpr (OT == WT) {
+          for (int c = lane; c < H / EPC; c += 32) st_v4(orow + (int64_t)c * 16, ld_v4(rec + (int64_t)c * 16));
+        } else {
+          for (int c = lane; c < H / EPC; c += 32) {
+            float fv[EPC];
+            unpack16<WT>(ld_v4(rec + (int64_t)c * 16), fv);
+            store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, fv);
+          }
+        }
+      } else {
+        for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: combine
+// ---------------------------------------------------------------------------
+struct HTCombSend {
+  const void* y;
+  const int32_t* origin;
+  const int32_t* meta;  // [N][E+N] (m rows)
+  const uint64_t* peers;
+  int* done;
+  HTGeom g;
+  int rows, rank, in_dtype;
+  uint32_t tag;
+};
+
+EPB_DEV int ht_rows_to(const HTCombSend& p, int s) {
+  const int C = p.g.E + p.g.N;
+  const int lo = p.rank * p.g.L, hi = min(lo + p.g.L, p.g.E);
+  int c = 0;
+  for (int e = lo; e < hi; ++e) c += p.meta[s * C + e];
+  return c;
+}
+
+EPB_DEV void ht_publish_comb(const HTCombSend& p, int s, int count) {
+  uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, s) + p.g.cflag) + p.rank;
+  st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | ((uint64_t)p.in_dtype << 28) | (uint32_t)count);
+}
+
+template <int IT>
+__global__ void __launch_bounds__(256) ht_combine_send_kernel(HTCombSend p) {
+  __shared__ int s_cnt[kMaxRanks];
+  const HTGeom& g = p.g;
+  const int N = g.N, K = g.K, H = g.H;
+  if (threadIdx.x < N) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int per = (p.rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(p.rows, r0 + per);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int ib = IT == EPB_F32 ? 4 : 2;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    const int s = p.origin[(int64_t)r * 4 + 1];
+    const int t = p.origin[(int64_t)r * 4 + 2];
+    const int k = p.origin[(int64_t)r * 4 + 3];
+    uint8_t* dst = hpeer(p.peers, s) + g.crow + ((int64_t)t * K + k) * g.crow_stride;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.y) + (int64_t)r * H * ib;
+    const int bytes = H * ib;
+    if ((bytes & 15) == 0) {
+      for (int c = lane; c < bytes / 16; c += 32) st_na_v4(dst + (int64_t)c * 16, ld_nc_v4(src + (int64_t)c * 16));
+    } else {
+      for (int c = lane; c < bytes / 4; c += 32)
+        reinterpret_cast<uint32_t*>(dst)[c] = reinterpret_cast<const uint32_t*>(src)[c];
+      if (lane == 0 && (bytes & 3))
+        reinterpret_cast<uint16_t*>(dst)[bytes / 2 - 1] = reinterpret_cast<const uint16_t*>(src)[bytes / 2 - 1];
+    }
+    if (lane == 0) atomicAdd(&s_cnt[s], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    const int s = threadIdx.x;
+    const int c = s_cnt[s];
+    const int want = ht_rows_to(p, s);
+    if (c > 0) {
+      fence_sys();
+      const int old = atomicAdd(&p.done[s], c);
+      if (old + c == want) {
+        p.done[s] = 0;
+        fence_sys();
+        ht_publish_comb(p, s, want);
+      }
+    } else if (blockIdx.x == 0 && want == 0) {
+      ht_publish_comb(p, s, 0);
+    }
+  }
+}
+
+struct HTCombRecv {
+  const int64_t* topk;
+  const float* w;
+  void* out;
+  const uint8_t* win;
+  int* err;
+  HTGeom g;
+  uint64_t timeout_ns;
+  int b;
+  uint32_t tag;
+};
+
+template <int OT>
+__global__ void __launch_bounds__(256) ht_combine_recv_kernel(HTCombRecv p) {
+  __shared__ int s_dt[kMaxRanks];
+  __shared__ int s_fail;
+  __shared__ float s_w[kMaxTopK];
+  __shared__ int s_node[kMaxTopK], s_kdt[kMaxTopK], s_nodes[kMaxTopK], s_nn;
+  const HTGeom& g = p.g;
+  const int N = g.N, K = g.K, H = g.H, L = g.L;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.cflag);
+  for (int s = threadIdx.x; s < N; s += blockDim.x) {
+    uint64_t v = 0;
+    if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    s_dt[s] = (int)((v >> 28) & 0xF);
+  }
+  __syncthreads();
+  if (s_fail) return;
+  const uint8_t* crow = p.win + g.crow;
+  for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
+    if (threadIdx.x < K) {
+      const int e = (int)p.topk[(int64_t)t * K + threadIdx.x];
+      const int owner = e / L;
+      s_node[threadIdx.x] = owner / g.rpn;
+      s_kdt[threadIdx.x] = s_dt[owner];
+      s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // distinct nodes of this token, ascending (ht.py:718-719)
+      int nn = 0;
+      for (int k = 0; k < K; ++k) {
+        const int nd = s_node[k];
+        int pos = 0;
+        while (pos < nn && s_nodes[pos] < nd) ++pos;
+        if (pos < nn && s_nodes[pos] == nd) continue;
+        for (int j = nn; j > pos; --j) s_nodes[j] = s_nodes[j - 1];
+        s_nodes[pos] = nd;
+        ++nn;
+      }
+      s_nn = nn;
+    }
+    __syncthreads();
+    const int nn = s_nn;
+    uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
+    const uint8_t* tslots = crow + (int64_t)t * K * g.crow_stride;
+    if ((H & 7) == 0) {
+      for (int c = threadIdx.x; c < H / 8; c += blockDim.x) {
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        for (int ni = 0; ni < nn; ++ni) {
+          const int nd = s_nodes[ni];
+          float part[8];
+          bool started = false;
+          for (int k = 0; k < K; ++k) {
+            if (s_node[k] != nd) continue;
+            float y[8];
+            const uint8_t* sl = tslots + (int64_t)k * g.crow_stride;
+            if (s_kdt[k] == EPB_F32) {
+              unpack16<EPB_F32>(ld_v4(sl + (int64_t)c * 32), y);
+              unpack16<EPB_F32>(ld_v4(sl + (int64_t)c * 32 + 16), y + 4);
+            } else {
+              unpack16<EPB_BF16>(ld_v4(sl + (int64_t)c * 16), y);
+            }
+            const float wk = s_w[k];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float pk = __fmul_rn(wk, y[i]);
+              part[i] = started ? __fadd_rn(part[i], pk) : pk;
+            }
+            started = true;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], part[i]);
+        }
+        store_f32_chunk<OT, 8>(orow, (int64_t)c * 8, acc);
+      }
+    } else {
+      for (int el = threadIdx.x; el < H; el += blockDim.x) {
+        float acc = 0.0f;
+        for (int ni = 0; ni < nn; ++ni) {
+          const int nd = s_nodes[ni];
+          float part = 0.0f;
+          bool started = false;
+          for (int k = 0; k < K; ++k) {
+            if (s_node[k] != nd) continue;
+            const float y = load_elem(tslots + (int64_t)k * g.crow_stride, s_kdt[k], el);
+            const float pk = __fmul_rn(s_w[k], y);
+            part = started ? __fadd_rn(part, pk) : pk;
+            started = true;
+          }
+          acc = __fadd_rn(acc, part);
+        }
+        store_elem(orow, OT, el, acc);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void weights_equal_kernel(const float* a, const float* b, int64_t n, int* err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (__float_as_uint(a[i]) != __float_as_uint(b[i]) && !(a[i] == b[i])) atomicCAS(err, 0, EPB_INVALID_ARGUMENT);
+}
+
+}  // namespace epb
+
+using namespace epb;
+
+namespace {
+
+uint32_t ht_tag(uint32_t round) { return (round % 0xFFFFFFFu) + 1u; }
+
+int hsm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int check_ht(epb_group* g) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  if (g->cfg.algorithm != EPB_HT) return fail(EPB_HANDLE_STATE_ERROR, "group is not HT");
+  if (!g->peers_ready) return fail(EPB_HANDLE_STATE_ERROR, "peer windows not mapped");
+  return EPB_OK;
+}
+
+template <int XT, int WT>
+cudaError_t launch_hsend(const HTSend& p, cudaStream_t s) {
+  const int grid = max(1, min(p.b, 2 * hsm_count()));
+  ht_dispatch_send_kernel<XT, WT><<<grid, 512, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int XT>
+cudaError_t launch_hsend_x(const HTSend& p, cudaStream_t s) {
+  switch (p.g.wire) {
+    case EPB_F32: return launch_hsend<XT, EPB_F32>(p, s);
+    case EPB_BF16: return launch_hsend<XT, EPB_BF16>(p, s);
+    default: return launch_hsend<XT, EPB_F16>(p, s);
+  }
+}
+
+template <int WT, int OT>
+cudaError_t launch_hrecv(const HTRecv& p, cudaStream_t s) {
+  ht_dispatch_recv_kernel<WT, OT><<<2 * hsm_count(), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay, void* stream) {
+  if (int rc = check_ht(g)) return rc;
+  HTMetaSend p;
+  p.m = lay->expert_count; p.q = lay->rank_count; p.peers = g->d_peers; p.g = g->ht;
+  p.rank = g->rank; p.parity = round & 1; p.tag = ht_tag(round);
+  ht_meta_send_kernel<<<1, 256, 0, as_stream(stream)>>>(p);
+  EPB_LAUNCH_CHECK();
+  return EPB_OK;
+}
+
+int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out, int32_t* offsets,
+                     int32_t* recv_total, void* stream) {
+  if (int rc = check_ht(g)) return rc;
+  HTMetaRecv p;
+  p.win = g->window; p.meta_out = meta_out; p.offsets = offsets; p.recv_total = recv_total;
+  p.err = g->d_err; p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank;
+  p.parity = round & 1; p.tag = ht_tag(round);
+  const size_t smem = sizeof(int32_t) * g->ht.N * (g->ht.E + g->ht.N);
+  if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "metadata too large");
+  EPB_CUDA(cudaFuncSetAttribute(ht_meta_recv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ht_meta_recv_kernel<<<1, 1024, smem, as_stream(stream)>>>(p);
+  EPB_LAUNCH_CHECK();
+  return EPB_OK;
+}
+
+int epb_ht_dispatch_send(epb_group* g, uint32_t round, const void* x, int32_t x_dtype,
+                         const float* weights, const int64_t* topk_idx, const epb_layout* lay,
+                         const int32_t* offsets, void* stream) {
+  if (int rc = check_ht(g)) return rc;
+  if (lay->num_tokens > 0 && (reinterpret_cast<uintptr_t>(x) & 15))
+    return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
+  HTSend p;
+  p.x = x; p.w = weights; p.topk = topk_idx; p.q = lay->rank_count; p.tok_rank = lay->tok_rank;
+  p.tok_slot = lay->tok_slot; p.offsets = offsets; p.peers = g->d_peers; p.done = g->d_done;
+  p.g = g->ht; p.b = lay->num_tokens; p.rank = g->rank; p.tag = ht_tag(round);
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e;
+  switch (x_dtype) {
+    case EPB_F32: e = launch_hsend_x<EPB_F32>(p, s); break;
+    case EPB_BF16: e = launch_hsend_x<EPB_BF16>(p, s); break;
+    case EPB_F16: e = launch_hsend_x<EPB_F16>(p, s); break;
+    default: return fail(EPB_TAG_MISMATCH, "HT dispatch input must be f32/bf16/f16");
+  }
+  if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_send");
+  return EPB_OK;
+}
+
+int epb_ht_dispatch_recv(epb_group* g, uint32_t round, void* out, int32_t out_dtype, int32_t* origin,
+                         float* origin_w, void* stream) {
+  if (int rc = check_ht(g)) return rc;
+  const int wire = g->cfg.token_dtype;
+  if (out_dtype != EPB_F32 && out_dtype != wire)
+    return fail(EPB_TAG_MISMATCH, "dispatch output must be f32 or the wire dtype");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
+  HTRecv p;
+  p.out = out; p.origin = origin; p.origin_w = origin_w; p.win = g->window; p.err = g->d_err;
+  p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank; p.tag = ht_tag(round);
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e;
+  switch (wire) {
+    case EPB_F32: e = launch_hrecv<EPB_F32, EPB_F32>(p, s); break;
+    case EPB_BF16:
+      e = out_dtype == EPB_F32 ? launch_hrecv<EPB_BF16, EPB_F32>(p, s) : launch_hrecv<EPB_BF16, EPB_BF16>(p, s);
+      break;
+    default:
+      e = out_dtype == EPB_F32 ? launch_hrecv<EPB_F16, EPB_F32>(p, s) : launch_hrecv<EPB_F16, EPB_F16>(p, s);
+  }
+  if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_recv");
+  return EPB_OK;
+}
+
+int epb_ht_combine_send(epb_group* g, uint32_t round, const void* expert_rows, int32_t in_dtype,
+                        const int32_t* origin, int32_t recv_total, void* stream) {
+  if (int rc = check_ht(g)) return rc;
+  if (in_dtype != EPB_F32 && in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
+  if (recv_total > 0 && (reinterpret_cast<uintptr_t>(expert_rows) & 15))
+    return fail(EPB_INVALID_ARGUMENT, "expert rows must be 16-byte aligned");
+  // the metadata rows of this round live in the window (parity = round & 1)
+  HTCombSend p;
+  p.y = expert_rows; p.origin = origin;
+  p.meta = reinterpret_cast<const int32_t*>(g->window + g->ht.meta +
+                                            (uint64_t)(round & 1) * g->ht.N * (g->ht.E + g->ht.N) * 4);
+  p.peers = g->d_peers; p.done = g->d_done + g->cfg.num_ranks; p.g = g->ht; p.rows = recv_total;
+  p.rank = g->rank; p.in_dtype = in_dtype; p.tag = ht_tag(round);
+  const int grid = max(1, min(2 * hsm_count(), (recv_total + 7) / 8));
+  cudaStream_t s = as_stream(stream);
+  if (in_dtype == EPB_F32) ht_combine_send_kernel<EPB_F32><<<grid, 256, 0, s>>>(p);
+  else ht_combine_send_kernel<EPB_BF16><<<grid, 256, 0, s>>>(p);
+  EPB_LAUNCH_CHECK();
+  return EPB_OK;
+}
+
+int epb_ht_combine_recv(epb_group* g, uint32_t round, const int64_t* topk_idx, const float* weights,
+                        int32_t b, void* out, int32_t out_dtype, void* stream) {
+  if (int rc = check_ht(g)) return rc;
+  if (out_dtype != EPB_F32 && out_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine output f32|bf16");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
+  HTCombRecv p;
+  p.topk = topk_idx; p.w = weights; p.out = out; p.win = g->window; p.err = g->d_err; p.g = g->ht;
+  p.timeout_ns = g->timeout_ns; p.b = b; p.tag = ht_tag(round);
+  const int grid = max(1, min(b, 4 * hsm_count()));
+  cudaStream_t s = as_stream(stream);
+  if (out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_F32><<<grid, 256, 0, s>>>(p);
+  else ht_combine_recv_kernel<EPB_BF16><<<grid, 256, 0, s>>>(p);
+  EPB_LAUNCH_CHECK();
+  return EPB_OK;
+}
+
+int epb_weights_equal(epb_group* g, const float* a, const float* b, int64_t n, void* stream) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  if (n <= 0) return EPB_OK;
+  const int grid = (int)std::min<int64_t>(1024, (n + 255) / 256);
+  weights_equal_kernel<<<grid, 256, 0, as_stream(stream)>>>(a, b, n, g->d_err);
+  EPB_LAUNCH_CHECK();
+  return EPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// Library-internal state shared by the translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/epb200.h"
+#include "geometry.h"
+
+struct epb_group {
+  epb_config cfg;
+  int rank;
+  int device;
+  uint8_t* window = nullptr;
+  uint64_t window_bytes = 0;
+  bool owns_window = false;
+  void* alloc_base = nullptr;   // allocation holding `window` (for IPC)
+  uint64_t* d_peers = nullptr;  // [N] window bases as seen from this GPU
+  std::vector<void*> ipc_opened;
+  int* d_err = nullptr;         // device error word
+  int* d_done = nullptr;        // [2*N] arrival counters (dispatch, combine)
+  int* d_scratch = nullptr;     // [4*N + 2*L*N + 64] small per-call state
+  epb::LLGeom ll;
+  epb::HTGeom ht;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  bool peers_ready = false;
+};
+
+namespace epb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace epb
+
+#define EPB_CUDA(call)                                          \
+  do {                                                          \
+    cudaError_t _e = (call);                                    \
+    if (_e != cudaSuccess) return epb::cuda_check(_e, #call);   \
+  } while (0)
+
+#define EPB_LAUNCH_CHECK() EPB_CUDA(cudaGetLastError())

@@ -1,0 +1,169 @@
+"""Rank groups and their bootstrap (replaces epsim fabric.py + the
+_Rendezvous of api.py:67-94).
+
+The reference's Fabric is a simulated one-sided transport between threads.
+Here the transport is NVLink load/store between GPUs, done inside the CUDA
+kernels; what remains on the host is:
+
+* `exchange(rank, obj)`  — collective all-gather used once per group to agree
+  on the config fingerprint and to trade window descriptors;
+* `phase(rank)`          — the point between a collective's send half and its
+  receive half.  One process per GPU needs nothing there (peers run
+  concurrently); N ranks emulated on ONE GPU must have every rank's send
+  kernel enqueued before any rank's receive kernel, so the local fabric
+  barriers its rank threads;
+* `stream(rank)`         — where a rank's kernels go.
+
+Two fabrics:
+  Fabric(topology)                       N ranks as threads on one GPU
+                                         (the reference's test model,
+                                          harness.py:20-67)
+  ProcessFabric(topology, process_group) one process per GPU, torch.distributed
+                                         (NCCL or gloo) for bootstrap only
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import torch
+
+from .core import EpError, ErrorCode
+
+
+@dataclass(frozen=True)
+class NodeTopology:
+    """Which ranks share a node (fabric.py:25-50)."""
+
+    num_ranks: int
+    ranks_per_node: int
+
+    def __post_init__(self):
+        if self.num_ranks < 1 or self.ranks_per_node < 1 or self.num_ranks % self.ranks_per_node:
+            raise EpError(ErrorCode.INVALID_ARGUMENT,
+                          f"bad topology ({self.num_ranks} ranks, {self.ranks_per_node} per node)")
+
+    @property
+    def num_nodes(self) -> int:
+        return self.num_ranks // self.ranks_per_node
+
+    def node_of(self, rank: int) -> int:
+        return rank // self.ranks_per_node
+
+    def rail_of(self, rank: int) -> int:
+        return rank % self.ranks_per_node
+
+    def same_node(self, a: int, b: int) -> bool:
+        return self.node_of(a) == self.node_of(b)
+
+
+class _Barrier:
+    def __init__(self, n: int, timeout: float):
+        self._b = threading.Barrier(n)
+        self._timeout = timeout
+
+    def wait(self):
+        try:
+            self._b.wait(self._timeout)
+        except threading.BrokenBarrierError:
+            raise EpError(ErrorCode.TRANSPORT_CLOSED, "fabric shut down or a rank stopped participating")
+
+    def abort(self):
+        self._b.abort()
+
+
+class Fabric:
+    """N emulated ranks on one GPU, one host thread per rank.
+
+    Every rank's window lives on the same device; kernels store into peer
+    windows through plain device pointers, exactly as they store into
+    CUDA-IPC-mapped windows of other GPUs in ProcessFabric."""
+
+    process_mode = False
+
+    def __init__(self, topology: NodeTopology, seed: int = 0, device=None, timeout: float = 120.0):
+        self.topology = topology
+        self.seed = seed
+        n = topology.num_ranks
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._stream = torch.cuda.Stream(device=self.device) if n > 1 else None
+        self._barrier = _Barrier(n, timeout)
+        self._lock = threading.Lock()
+        self._calls = {}
+        self._slots = {}
+        self._closed = False
+        self.registered = [0] * n  # bytes of live windows per rank (fabric.registered_bytes)
+
+    # -- collectives ----------------------------------------------------------
+    def exchange(self, rank: int, value) -> list:
+        if self._closed:
+            raise EpError(ErrorCode.TRANSPORT_CLOSED, "fabric shut down")
+        with self._lock:
+            gen = self._calls.get(rank, 0)
+            self._calls[rank] = gen + 1
+            self._slots.setdefault(gen, {})[rank] = value
+        self._barrier.wait()
+        with self._lock:
+            slot = self._slots[gen]
+            out = [slot[r] for r in range(self.topology.num_ranks)]
+        self._barrier.wait()
+        return out
+
+    def phase(self, rank: int) -> None:
+        if self.topology.num_ranks > 1:
+            self._barrier.wait()
+
+    def stream(self, rank: int):
+        return self._stream if self._stream is not None else torch.cuda.current_stream(self.device)
+
+    def registered_bytes(self, rank: int) -> int:
+        return self.registered[rank]
+
+    def shutdown(self) -> None:
+        self._closed = True
+        self._barrier.abort()
+
+
+class ProcessFabric:
+    """One process per GPU; `process_group` (torch.distributed) carries only
+    the bootstrap all-gather and barriers — never token data."""
+
+    process_mode = True
+
+    def __init__(self, topology: NodeTopology, process_group=None):
+        import torch.distributed as dist
+
+        self.topology = topology
+        self.group = process_group
+        self._dist = dist
+        world = dist.get_world_size(process_group)
+        if world != topology.num_ranks:
+            raise EpError(ErrorCode.INVALID_ARGUMENT,
+                          f"process group has {world} ranks, topology {topology.num_ranks}")
+        self.rank = dist.get_rank(process_group)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
+            else torch.device("cpu")
+        self.registered = [0] * topology.num_ranks
+
+    def exchange(self, rank: int, value) -> list:
+        if rank != self.rank:
+            raise EpError(ErrorCode.INVALID_ARGUMENT, f"rank {rank} is not this process ({self.rank})")
+        out = [None] * self.topology.num_ranks
+        self._dist.all_gather_object(out, value, group=self.group)
+        return out
+
+    def phase(self, rank: int) -> None:
+        return None
+
+    def barrier(self) -> None:
+        self._dist.barrier(group=self.group)
+
+    def stream(self, rank: int):
+        return torch.cuda.current_stream()
+
+    def registered_bytes(self, rank: int) -> int:
+        return self.registered[rank] if rank == self.rank else 0
+
+    def shutdown(self) -> None:
+        return None
