@@ -137,25 +137,30 @@ int epb_group_destroy(epb_group* g);
 int epb_routing_layout(epb_group* g, const int64_t* topk_idx, int32_t b,
                        const epb_layout* lay, void* stream);
 
-/* K2: LL dispatch send.  x: [b, H] in x_dtype (EPB_FP8 requires x_scales
+/* LL rounds are sequenced ON THE DEVICE (graph-replayable): dispatch_send
+ * reads the group's round counter, stores it into *hseq (a caller-owned
+ * device u32 per handle) and advances the counter; the recv/combine calls
+ * of the round take the same hseq.  Parity = seq & 1 (ll.py:250).
+ *
+ * K2: LL dispatch send.  x: [b, H] in x_dtype (EPB_FP8 requires x_scales
  * [b, H/128]); converted to the wire dtype (fused FP8 block quantisation). */
-int epb_ll_dispatch_send(epb_group* g, uint32_t seq, const void* x,
+int epb_ll_dispatch_send(epb_group* g, uint32_t* hseq, const void* x,
                          int32_t x_dtype, const float* x_scales,
                          const int64_t* topk_idx, const epb_layout* lay,
                          void* stream);
 /* K3: LL dispatch recv.  out: [L, N*B, H] in out_dtype (EPB_F32 = the
  * reference boundary, or the wire dtype with out_scales [L, N*B, H/128]);
  * counts_f32/counts_i32: [L, N]; src_info: [L, N*B] = t*K + k. */
-int epb_ll_dispatch_recv(epb_group* g, uint32_t seq, void* out,
+int epb_ll_dispatch_recv(epb_group* g, const uint32_t* hseq, void* out,
                          int32_t out_dtype, float* out_scales,
                          float* counts_f32, int32_t* counts_i32,
                          int32_t* src_info, void* stream);
 /* K4a: LL combine send; expert_out [L, N*B, H] f32|bf16 */
-int epb_ll_combine_send(epb_group* g, uint32_t seq, const void* expert_out,
+int epb_ll_combine_send(epb_group* g, const uint32_t* hseq, const void* expert_out,
                         int32_t in_dtype, const int32_t* counts_i32,
                         const int32_t* src_info, void* stream);
 /* K4b: LL combine recv; out [b, H] f32|bf16 */
-int epb_ll_combine_recv(epb_group* g, uint32_t seq, const float* weights,
+int epb_ll_combine_recv(epb_group* g, const uint32_t* hseq, const float* weights,
                         int32_t b, void* out, int32_t out_dtype, void* stream);
 
 /* K5a: HT metadata all-gather over the windows */

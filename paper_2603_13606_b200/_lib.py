@@ -62,10 +62,10 @@ SIGNATURES = {
     "epb_group_poll_error": [_P, ctypes.c_int, ctypes.POINTER(_I)],
     "epb_group_destroy": [_P],
     "epb_routing_layout": [_P, _P, _I, ctypes.POINTER(Layout), _P],
-    "epb_ll_dispatch_send": [_P, _U, _P, _I, _P, _P, ctypes.POINTER(Layout), _P],
-    "epb_ll_dispatch_recv": [_P, _U, _P, _I, _P, _P, _P, _P, _P],
-    "epb_ll_combine_send": [_P, _U, _P, _I, _P, _P, _P],
-    "epb_ll_combine_recv": [_P, _U, _P, _I, _P, _I, _P],
+    "epb_ll_dispatch_send": [_P, _P, _P, _I, _P, _P, ctypes.POINTER(Layout), _P],
+    "epb_ll_dispatch_recv": [_P, _P, _P, _I, _P, _P, _P, _P, _P],
+    "epb_ll_combine_send": [_P, _P, _P, _I, _P, _P, _P],
+    "epb_ll_combine_recv": [_P, _P, _P, _I, _P, _I, _P],
     "epb_ht_meta_send": [_P, _U, ctypes.POINTER(Layout), _P],
     "epb_ht_meta_recv": [_P, _U, _P, _P, _P, _P],
     "epb_ht_dispatch_send": [_P, _U, _P, _I, _P, _P, ctypes.POINTER(Layout), _P, _P],

@@ -145,6 +145,7 @@ class EpGroup:
         self._ht_open = None
         self._alive = True
         self.strict = strict
+        self._marks = None
         self.device = torch.device("cuda", torch.cuda.current_device())
 
     # -- properties -----------------------------------------------------------
@@ -186,6 +187,23 @@ class EpGroup:
 
     def set_timeout(self, seconds: float) -> None:
         _lib.call("epb_group_set_timeout", self._g, int(seconds * 1e9))
+
+    # -- kernel launches (optionally bracketed by timing marks) -------------
+    def trace_phases(self, marks: Optional[list]) -> None:
+        """With a list, every kernel launch of this group is preceded by a
+        timing event (external, so it survives CUDA-graph capture) appended
+        as (kernel name, event); pass None to stop."""
+        self._marks = marks
+
+    def mark(self, name: str) -> None:
+        if getattr(self, "_marks", None) is not None:
+            ev = torch.cuda.Event(enable_timing=True, external=True)
+            ev.record(self.stream)
+            self._marks.append((name, ev))
+
+    def _launch(self, name: str, *args) -> None:
+        self.mark(name)
+        _lib.call(name, *args)
 
     # -- handles ----------------------------------------------------------------
     def create_handle(self, topk_idx) -> "EpHandle":
@@ -348,7 +366,7 @@ class EpHandle:
         self._tok_slot = torch.empty(max(self._b, 1) * n, dtype=torch.int32, device=dev)
         self._lay = _lib.Layout(self._m.data_ptr(), self._q.data_ptr(), self._tok_rank.data_ptr(),
                                 self._tok_slot.data_ptr(), self._b)
-        self._seq: Optional[int] = None
+        self._hseq = torch.zeros(1, dtype=torch.int32, device=dev)  # LL round sequence (device)
         self._round: Optional[int] = None
         self._round_open = False
         self._meta = None
@@ -376,7 +394,7 @@ class EpHandle:
         return ctypes.c_void_p(self.group.stream.cuda_stream)
 
     def _run_layout(self) -> None:
-        _lib.call("epb_routing_layout", self.group._g, _ptr(self.routing), self._b,
+        self.group._launch("epb_routing_layout", self.group._g, _ptr(self.routing), self._b,
                   ctypes.byref(self._lay), self._sp())
 
     # -- HT metadata round ------------------------------------------------------
@@ -389,9 +407,9 @@ class EpHandle:
         meta = torch.empty((n, e + n), dtype=torch.int32, device=dev)
         offsets = torch.empty((e, n), dtype=torch.int32, device=dev)
         total = torch.empty(1, dtype=torch.int32, device=dev)
-        _lib.call("epb_ht_meta_send", g._g, rnd, ctypes.byref(self._lay), self._sp())
+        g._launch("epb_ht_meta_send", g._g, rnd, ctypes.byref(self._lay), self._sp())
         g.fabric.phase(g.rank)
-        _lib.call("epb_ht_meta_recv", g._g, rnd, _ptr(meta), _ptr(offsets), _ptr(total), self._sp())
+        g._launch("epb_ht_meta_recv", g._g, rnd, _ptr(meta), _ptr(offsets), _ptr(total), self._sp())
         g.check()  # synchronises: receive shapes are host-known on return (api.py:235-237)
         meta_h = meta.cpu().numpy()
         self._meta = dict(m=meta_h[:, :e].astype(np.int64), q=meta_h[:, e:].astype(np.int64),
@@ -405,11 +423,14 @@ class EpHandle:
             v = v.to(self.group.device, non_blocking=True)
         return v.contiguous()
 
-    def _dev_out(self, t: NDTensor):
-        """(device tensor to write, needs_copy_back)."""
+    def _dev_out(self, t: NDTensor, full: bool = False):
+        """(device tensor to write, needs_copy_back).  `full`: the kernel
+        overwrites every element, so a host output needs no upload."""
         v = t.view()
         if v.device == self.group.device and v.is_contiguous():
             return v, False
+        if full:
+            return torch.empty(t.shape, dtype=t.dtype.torch_dtype, device=self.group.device), True
         # rows the kernels do not write keep the caller's contents
         return v.to(self.group.device, non_blocking=True).contiguous(), True
 
@@ -489,10 +510,9 @@ class EpHandle:
                 return
             x = self._dev_in(tokens)
             xs = self._dev_in(scales) if scales is not None else None
-            seq = g._alloc_seq()
-            self._seq = seq
+            g._alloc_seq()
             x_code = tokens.dtype.code
-            _lib.call("epb_ll_dispatch_send", g._g, seq, _ptr(x), x_code, _ptr(xs), _ptr(self.routing),
+            g._launch("epb_ll_dispatch_send", g._g, _ptr(self._hseq), _ptr(x), x_code, _ptr(xs), _ptr(self.routing),
                       ctypes.byref(self._lay), self._sp())
             self._keep_alive = (x, xs)
             self._staged = (out_tokens, out_counts, out_scales)
@@ -511,10 +531,10 @@ class EpHandle:
         dev = g.device
         out_t, back_t = self._dev_out(out_tokens)
         out_s, back_s = self._dev_out(out_scales) if out_scales is not None else (None, False)
-        cnt_f, back_c = self._dev_out(out_counts)
+        cnt_f, back_c = self._dev_out(out_counts, full=True)
         self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
         self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
-        _lib.call("epb_ll_dispatch_recv", g._g, self._seq, _ptr(out_t), out_tokens.dtype.code, _ptr(out_s),
+        g._launch("epb_ll_dispatch_recv", g._g, _ptr(self._hseq), _ptr(out_t), out_tokens.dtype.code, _ptr(out_s),
                   _ptr(cnt_f), _ptr(self._counts_i32), _ptr(self._src_info), self._sp())
         if g.strict:
             g.check()
@@ -536,14 +556,14 @@ class EpHandle:
         w = self._dev_in(weights)
         self._weights = w.clone()
         rnd = self._round
-        _lib.call("epb_ht_dispatch_send", g._g, rnd, _ptr(x), tokens.dtype.code, _ptr(w), _ptr(self.routing),
+        g._launch("epb_ht_dispatch_send", g._g, rnd, _ptr(x), tokens.dtype.code, _ptr(w), _ptr(self.routing),
                   ctypes.byref(self._lay), _ptr(meta["offsets"]), self._sp())
         g.fabric.phase(g.rank)
         total = meta["recv_total"]
-        out_t, back_t = self._dev_out(out_tokens)
+        out_t, back_t = self._dev_out(out_tokens, full=True)
         origin = torch.empty((max(total, 1), 4), dtype=torch.int32, device=g.device)
         origin_w = torch.empty(max(total, 1), dtype=torch.float32, device=g.device)
-        _lib.call("epb_ht_dispatch_recv", g._g, rnd, _ptr(out_t), out_tokens.dtype.code, _ptr(origin),
+        g._launch("epb_ht_dispatch_recv", g._g, rnd, _ptr(out_t), out_tokens.dtype.code, _ptr(origin),
                   _ptr(origin_w), self._sp())
         if g.strict:
             g.check()
@@ -593,7 +613,7 @@ class EpHandle:
             if ht:
                 self._ht_combine(y, rows_in.dtype, w, out)
                 return
-            _lib.call("epb_ll_combine_send", g._g, self._seq, _ptr(y), rows_in.dtype.code,
+            g._launch("epb_ll_combine_send", g._g, _ptr(self._hseq), _ptr(y), rows_in.dtype.code,
                       _ptr(self._counts_i32), _ptr(self._src_info), self._sp())
             self._staged = (out, w, y)
             if send_only:
@@ -606,8 +626,8 @@ class EpHandle:
         g = self.group
         out, w, _y = self._staged
         self._staged = None
-        o, back = self._dev_out(out)
-        _lib.call("epb_ll_combine_recv", g._g, self._seq, _ptr(w), self._b, _ptr(o), out.dtype.code,
+        o, back = self._dev_out(out, full=True)
+        g._launch("epb_ll_combine_recv", g._g, _ptr(self._hseq), _ptr(w), self._b, _ptr(o), out.dtype.code,
                   self._sp())
         if g.strict:
             g.check()
@@ -621,14 +641,14 @@ class EpHandle:
         res = self._dispatch_result
         # combine weights must equal the dispatched ones (ht.py:605-609),
         # checked on the device before any combine traffic
-        _lib.call("epb_weights_equal", g._g, _ptr(w), _ptr(self._weights), w.numel(), self._sp())
+        g._launch("epb_weights_equal", g._g, _ptr(w), _ptr(self._weights), w.numel(), self._sp())
         if g.strict:
             g.check()
-        _lib.call("epb_ht_combine_send", g._g, self._round, _ptr(y), y_dtype.code, _ptr(res.origin),
+        g._launch("epb_ht_combine_send", g._g, self._round, _ptr(y), y_dtype.code, _ptr(res.origin),
                   res.recv_total, self._sp())
         g.fabric.phase(g.rank)
-        o, back = self._dev_out(out)
-        _lib.call("epb_ht_combine_recv", g._g, self._round, _ptr(self.routing), _ptr(w), self._b, _ptr(o),
+        o, back = self._dev_out(out, full=True)
+        g._launch("epb_ht_combine_recv", g._g, self._round, _ptr(self.routing), _ptr(w), self._b, _ptr(o),
                   out.dtype.code, self._sp())
         if g.strict:
             g.check()
@@ -679,6 +699,10 @@ class EpHandle:
         if self._round_open:
             self._round_open = False  # metadata went out, payload never followed
         self.state = HandleState.DESTROYED
+        try:
+            self.group._handles.remove(self)
+        except ValueError:
+            pass
 
 
 def create_handle(group: EpGroup, topk_idx) -> EpHandle:

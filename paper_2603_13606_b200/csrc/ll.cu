@@ -32,11 +32,19 @@ struct LLSend {
   const uint64_t* peers;
   int* done;
   int* err;
+  uint32_t* dseq;       // group round counter (device)
+  int* drd;             // arrivals of CTAs that read dseq
+  uint32_t* hseq;       // out: this round's sequence (handle-owned)
   LLGeom g;
-  uint64_t parity_off;
   int b, rank;
-  uint32_t tag;
 };
+
+// Round sequence numbers live on the device so a captured CUDA graph can be
+// replayed: the dispatch-send kernel reads the group counter, the last CTA
+// to read it stores it into the handle's word and advances the counter;
+// every later kernel of the round derives tag and parity from that word.
+EPB_DEV uint32_t ll_tag_of(uint32_t seq) { return (seq % 0xFFFFFFu) + 1u; }
+EPB_DEV uint32_t ld_volatile_u32(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
 
 EPB_DEV uint8_t* peer_base(const uint64_t* peers, int r) {
   return reinterpret_cast<uint8_t*>(peers[r]);
@@ -47,14 +55,15 @@ EPB_DEV void st_relaxed_sys(uint64_t* p, uint64_t v) {
 }
 
 // counters of pair (l, src=rank) at destination d: m(e, rank) with the tag
-EPB_DEV void ll_write_disp_counters(const LLSend& p, int d, int lane, int nlanes) {
+EPB_DEV void ll_write_disp_counters(const LLSend& p, int d, int lane, int nlanes, uint64_t parity_off,
+                                    uint32_t tag) {
   const LLGeom& g = p.g;
-  uint64_t* ctr = reinterpret_cast<uint64_t*>(peer_base(p.peers, d) + p.parity_off + g.disp_ctr);
+  uint64_t* ctr = reinterpret_cast<uint64_t*>(peer_base(p.peers, d) + parity_off + g.disp_ctr);
   const uint64_t qd = (uint64_t)p.q[d];
   for (int l = lane; l < g.L; l += nlanes) {
     const int e = d * g.L + l;
     const uint64_t m = e < g.E ? (uint64_t)p.m[e] : 0ull;
-    st_relaxed_sys(&ctr[l * g.N + p.rank], ((uint64_t)p.tag << 40) | (qd << 20) | m);
+    st_relaxed_sys(&ctr[l * g.N + p.rank], ((uint64_t)tag << 40) | (qd << 20) | m);
   }
 }
 
@@ -63,9 +72,12 @@ template <int XT, int EPC>
 EPB_DEV void load_input_chunk(const uint8_t* xrow, const float* xsc, int64_t e0, float* f) {
   load_elems_vec<XT, EPC>(xrow, e0, f);
   if constexpr (XT == EPB_FP8) {
-    // fp8 input carries block scales: dequantise (core.py:153-162)
+    // fp8 input with block scales: dequantise (core.py:153-162); without
+    // scales the codes are plain E4M3 values (implicit scale 1)
+    if (xsc != nullptr) {
 #pragma unroll
-    for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[(e0 + i) >> 7]);
+      for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[(e0 + i) >> 7]);
+    }
   }
 }
 
@@ -76,6 +88,20 @@ __global__ void __launch_bounds__(256) ll_dispatch_send_kernel(LLSend p) {
   const LLGeom& g = p.g;
   const int t = blockIdx.x;
   const int K = g.K, N = g.N, H = g.H;
+  __shared__ uint32_t s_seq;
+  if (threadIdx.x == 0) {
+    const uint32_t seq = ld_volatile_u32(p.dseq);
+    s_seq = seq;
+    __threadfence();
+    if (atomicAdd(p.drd, 1) == (int)gridDim.x - 1) {
+      *p.drd = 0;
+      *p.hseq = seq;
+      *p.dseq = seq + 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t tag = ll_tag_of(s_seq);
+  const uint64_t parity_off = (uint64_t)(s_seq & 1) * g.parity_bytes;
   if (t < p.b) {
     if (threadIdx.x == 0) {
       int nd = 0;
@@ -93,7 +119,7 @@ __global__ void __launch_bounds__(256) ll_dispatch_send_kernel(LLSend p) {
     }
     __syncthreads();
     const int nd = s_nd;
-    const uint64_t slot_off = p.parity_off + g.disp_slot;
+    const uint64_t slot_off = parity_off + g.disp_slot;
     const int64_t slot_idx = (int64_t)p.rank * g.B;
     // header words
     for (int w = threadIdx.x; w < 2 + 2 * K; w += blockDim.x) {
@@ -139,7 +165,9 @@ __global__ void __launch_bounds__(256) ll_dispatch_send_kernel(LLSend p) {
       // unaligned hidden: element path (no scales possible: H % 128 != 0)
       for (int el = threadIdx.x; el < H; el += blockDim.x) {
         float f = load_elem(xrow, XT, el);
-        if constexpr (XT == EPB_FP8) f = __fmul_rn(f, xsc[el >> 7]);
+        if constexpr (XT == EPB_FP8) {
+          if (xsc != nullptr) f = __fmul_rn(f, xsc[el >> 7]);
+        }
         for (int i = 0; i < nd; ++i) {
           uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_idx + s_j[i]) * g.slot_stride;
           store_elem(slot, WT, el, f);
@@ -161,7 +189,7 @@ __global__ void __launch_bounds__(256) ll_dispatch_send_kernel(LLSend p) {
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
           fence_sys();
-          ll_write_disp_counters(p, d, threadIdx.x, 32);
+          ll_write_disp_counters(p, d, threadIdx.x, 32, parity_off, tag);
         }
       }
     }
@@ -169,7 +197,7 @@ __global__ void __launch_bounds__(256) ll_dispatch_send_kernel(LLSend p) {
   // ranks this rank sends nothing to still get their (m = 0) counters
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     for (int d = 0; d < N; ++d)
-      if (p.q[d] == 0) ll_write_disp_counters(p, d, threadIdx.x, 32);
+      if (p.q[d] == 0) ll_write_disp_counters(p, d, threadIdx.x, 32, parity_off, tag);
   }
 }
 
@@ -182,11 +210,10 @@ struct LLRecv {
   int32_t* src_info;
   const uint8_t* win;
   int* err;
+  const uint32_t* hseq;
   LLGeom g;
-  uint64_t parity_off;
   uint64_t timeout_ns;
   int rank;
-  uint32_t tag;
 };
 
 // copy one received wire row (WT, optional scales) to an output row (OT)
@@ -245,10 +272,13 @@ __global__ void __launch_bounds__(256) ll_dispatch_recv_kernel(LLRecv p) {
   if (threadIdx.x == 0) s_fail = 0;
   if (threadIdx.x < N) s_q[threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t* ctr = reinterpret_cast<const uint64_t*>(p.win + p.parity_off + g.disp_ctr);
+  const uint32_t seq = ld_volatile_u32(p.hseq);
+  const uint32_t tag = ll_tag_of(seq);
+  const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+  const uint64_t* ctr = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.disp_ctr);
   for (int i = threadIdx.x; i < nloc * N; i += blockDim.x) {
     uint64_t v = 0;
-    if (!wait_tag(&ctr[i], p.tag, 40, 0xFFFFFFu, p.timeout_ns, p.err, &v)) {
+    if (!wait_tag(&ctr[i], tag, 40, 0xFFFFFFu, p.timeout_ns, p.err, &v)) {
       s_fail = 1;
       continue;
     }
@@ -283,7 +313,7 @@ __global__ void __launch_bounds__(256) ll_dispatch_recv_kernel(LLRecv p) {
     int s = 0;
     while (s_pre[s + 1] <= f) ++s;
     const int j = f - s_pre[s];
-    const uint8_t* slot = p.win + p.parity_off + g.disp_slot + ((int64_t)s * B + j) * g.slot_stride;
+    const uint8_t* slot = p.win + parity_off + g.disp_slot + ((int64_t)s * B + j) * g.slot_stride;
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
     const uint32_t t = hdr[0];
     for (int k = 0; k < K; ++k) {
@@ -306,18 +336,17 @@ struct LLCombSend {
   const uint64_t* peers;
   int* done;
   int* err;
+  const uint32_t* hseq;
   LLGeom g;
-  uint64_t parity_off;
   int rank;
-  uint32_t tag;
 };
 
-EPB_DEV void ll_write_comb_counters(const LLCombSend& p, int s) {
+EPB_DEV void ll_write_comb_counters(const LLCombSend& p, int s, uint64_t parity_off, uint32_t tag) {
   const LLGeom& g = p.g;
-  uint64_t* ctr = reinterpret_cast<uint64_t*>(peer_base(p.peers, s) + p.parity_off + g.comb_ctr);
+  uint64_t* ctr = reinterpret_cast<uint64_t*>(peer_base(p.peers, s) + parity_off + g.comb_ctr);
   const int lo = p.rank * g.L;
   const int hi = min(lo + g.L, g.E);
-  for (int e = lo; e < hi; ++e) st_relaxed_sys(&ctr[e], (uint64_t)p.tag);
+  for (int e = lo; e < hi; ++e) st_relaxed_sys(&ctr[e], (uint64_t)tag);
 }
 
 template <int IT, int WT>
@@ -327,6 +356,9 @@ __global__ void __launch_bounds__(256) ll_combine_send_kernel(LLCombSend p) {
   const LLGeom& g = p.g;
   const int N = g.N, L = g.L, B = g.B, H = g.H;
   const int P = L * N;
+  const uint32_t seq = ld_volatile_u32(p.hseq);
+  const uint32_t tag = ll_tag_of(seq);
+  const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
   if (threadIdx.x < N) { s_rows_to[threadIdx.x] = 0; s_cnt[threadIdx.x] = 0; }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -355,7 +387,7 @@ __global__ void __launch_bounds__(256) ll_combine_send_kernel(LLCombSend p) {
     const int l = pair / N, s = pair % N, i = r - s_pre[pair];
     const int64_t row = (int64_t)l * N * B + (int64_t)s * B + i;
     const int info = p.src_info[row];
-    uint8_t* dst = peer_base(p.peers, s) + p.parity_off + g.comb_slot + (int64_t)info * g.comb_stride;
+    uint8_t* dst = peer_base(p.peers, s) + parity_off + g.comb_slot + (int64_t)info * g.comb_stride;
     const uint8_t* yrow = reinterpret_cast<const uint8_t*>(p.y) + row * H * ib;
     if ((H & 15) == 0) {
       constexpr int EPC = Elems<WT>::n;
@@ -379,10 +411,10 @@ __global__ void __launch_bounds__(256) ll_combine_send_kernel(LLCombSend p) {
       if (old + c == s_rows_to[s]) {
         p.done[s] = 0;
         fence_sys();
-        ll_write_comb_counters(p, s);
+        ll_write_comb_counters(p, s, parity_off, tag);
       }
     } else if (blockIdx.x == 0 && s_rows_to[s] == 0) {
-      ll_write_comb_counters(p, s);
+      ll_write_comb_counters(p, s, parity_off, tag);
     }
   }
 }
@@ -393,11 +425,10 @@ struct LLCombRecv {
   void* out;
   const uint8_t* win;
   int* err;
+  const uint32_t* hseq;
   LLGeom g;
-  uint64_t parity_off;
   uint64_t timeout_ns;
   int b;
-  uint32_t tag;
 };
 
 template <int WT, int OT>
@@ -408,14 +439,17 @@ __global__ void __launch_bounds__(256) ll_combine_recv_kernel(LLCombRecv p) {
   const int K = g.K, H = g.H;
   if (threadIdx.x == 0) s_fail = 0;
   __syncthreads();
-  const uint64_t* ctr = reinterpret_cast<const uint64_t*>(p.win + p.parity_off + g.comb_ctr);
+  const uint32_t seq = ld_volatile_u32(p.hseq);
+  const uint32_t tag = ll_tag_of(seq);
+  const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+  const uint64_t* ctr = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.comb_ctr);
   for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
     uint64_t v;
-    if (!wait_tag(&ctr[e], p.tag, 0, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    if (!wait_tag(&ctr[e], tag, 0, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
   }
   __syncthreads();
   if (s_fail) return;
-  const uint8_t* slots = p.win + p.parity_off + g.comb_slot;
+  const uint8_t* slots = p.win + parity_off + g.comb_slot;
   for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
     if (threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
     __syncthreads();
@@ -453,8 +487,6 @@ using namespace epb;
 
 namespace {
 
-uint64_t parity_offset(const epb_group* g, uint32_t seq) { return (uint64_t)(seq & 1) * g->ll.parity_bytes; }
-uint32_t ll_tag(uint32_t seq) { return (seq % 0xFFFFFFu) + 1u; }
 
 int sm_count() {
   static int n = 0;
@@ -538,19 +570,18 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 extern "C" {
 
-int epb_ll_dispatch_send(epb_group* g, uint32_t seq, const void* x, int32_t x_dtype,
+int epb_ll_dispatch_send(epb_group* g, uint32_t* hseq, const void* x, int32_t x_dtype,
                          const float* x_scales, const int64_t* topk_idx, const epb_layout* lay,
                          void* stream) {
   if (int rc = check_ll(g)) return rc;
   if (!lay) return fail(EPB_INVALID_ARGUMENT, "null layout");
-  if (x_dtype == EPB_FP8 && !x_scales) return fail(EPB_TAG_MISMATCH, "fp8 input needs scales");
-  if (x_dtype == EPB_FP8 && g->cfg.hidden % 128) return fail(EPB_INVALID_ARGUMENT, "fp8 input needs H % 128 == 0");
+  if (x_scales && g->cfg.hidden % 128) return fail(EPB_INVALID_ARGUMENT, "scaled fp8 input needs H % 128 == 0");
   if (lay->num_tokens > 0 && !aligned16(x)) return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
   LLSend p;
   p.x = x; p.x_scales = x_scales; p.topk = topk_idx; p.m = lay->expert_count; p.q = lay->rank_count;
   p.tok_rank = lay->tok_rank; p.tok_slot = lay->tok_slot; p.peers = g->d_peers; p.done = g->d_done;
-  p.err = g->d_err; p.g = g->ll; p.parity_off = parity_offset(g, seq); p.b = lay->num_tokens;
-  p.rank = g->rank; p.tag = ll_tag(seq);
+  p.err = g->d_err; p.g = g->ll; p.b = lay->num_tokens; p.rank = g->rank;
+  p.dseq = reinterpret_cast<uint32_t*>(g->d_scratch); p.drd = g->d_scratch + 1; p.hseq = hseq;
   cudaStream_t s = as_stream(stream);
   cudaError_t e;
   switch (x_dtype) {
@@ -564,7 +595,7 @@ int epb_ll_dispatch_send(epb_group* g, uint32_t seq, const void* x, int32_t x_dt
   return EPB_OK;
 }
 
-int epb_ll_dispatch_recv(epb_group* g, uint32_t seq, void* out, int32_t out_dtype, float* out_scales,
+int epb_ll_dispatch_recv(epb_group* g, const uint32_t* hseq, void* out, int32_t out_dtype, float* out_scales,
                          float* counts_f32, int32_t* counts_i32, int32_t* src_info, void* stream) {
   if (int rc = check_ll(g)) return rc;
   const int wire = g->cfg.token_dtype;
@@ -577,8 +608,7 @@ int epb_ll_dispatch_recv(epb_group* g, uint32_t seq, void* out, int32_t out_dtyp
   LLRecv p;
   p.out = out; p.out_scales = out_scales; p.counts_f32 = counts_f32; p.counts_i32 = counts_i32;
   p.src_info = src_info; p.win = g->window; p.err = g->d_err; p.g = g->ll;
-  p.parity_off = parity_offset(g, seq); p.timeout_ns = g->timeout_ns; p.rank = g->rank;
-  p.tag = ll_tag(seq);
+  p.hseq = hseq; p.timeout_ns = g->timeout_ns; p.rank = g->rank;
   const int grid = max(1, min(2 * sm_count(), (int)((g->ll.n_disp + 7) / 8)));
   cudaStream_t s = as_stream(stream);
   cudaError_t e;
@@ -594,14 +624,14 @@ int epb_ll_dispatch_recv(epb_group* g, uint32_t seq, void* out, int32_t out_dtyp
   return EPB_OK;
 }
 
-int epb_ll_combine_send(epb_group* g, uint32_t seq, const void* expert_out, int32_t in_dtype,
+int epb_ll_combine_send(epb_group* g, const uint32_t* hseq, const void* expert_out, int32_t in_dtype,
                         const int32_t* counts_i32, const int32_t* src_info, void* stream) {
   if (int rc = check_ll(g)) return rc;
   if (!aligned16(expert_out)) return fail(EPB_INVALID_ARGUMENT, "expert_out must be 16-byte aligned");
   LLCombSend p;
   p.y = expert_out; p.counts = counts_i32; p.src_info = src_info; p.peers = g->d_peers;
   p.done = g->d_done + g->cfg.num_ranks; p.err = g->d_err; p.g = g->ll;
-  p.parity_off = parity_offset(g, seq); p.rank = g->rank; p.tag = ll_tag(seq);
+  p.hseq = hseq; p.rank = g->rank;
   const int P = g->ll.L * g->ll.N;
   const size_t smem = sizeof(int) * (P + 1);
   const int grid = max(1, min(2 * sm_count(), (g->ll.B * g->ll.K + 7) / 8 + 1));
@@ -617,7 +647,7 @@ int epb_ll_combine_send(epb_group* g, uint32_t seq, const void* expert_out, int3
   return EPB_OK;
 }
 
-int epb_ll_combine_recv(epb_group* g, uint32_t seq, const float* weights, int32_t b, void* out,
+int epb_ll_combine_recv(epb_group* g, const uint32_t* hseq, const float* weights, int32_t b, void* out,
                         int32_t out_dtype, void* stream) {
   if (int rc = check_ll(g)) return rc;
   if (b < 0 || b > g->cfg.max_tokens_per_rank) return fail(EPB_CAPACITY_EXCEEDED, "token count");
@@ -625,7 +655,7 @@ int epb_ll_combine_recv(epb_group* g, uint32_t seq, const float* weights, int32_
   if (!aligned16(out)) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
   LLCombRecv p;
   p.w = weights; p.out = out; p.win = g->window; p.err = g->d_err; p.g = g->ll;
-  p.parity_off = parity_offset(g, seq); p.timeout_ns = g->timeout_ns; p.b = b; p.tag = ll_tag(seq);
+  p.hseq = hseq; p.timeout_ns = g->timeout_ns; p.b = b;
   cudaStream_t s = as_stream(stream);
   cudaError_t e;
   switch (g->ll.cwire) {

@@ -91,7 +91,7 @@ def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="referen
                                 recv_total=hd.get_num_recv_tokens(), rows=rows))
                 hd.destroy()
         finally:
-            g.destroy()
+            _teardown(g)
         return res if rounds > 1 else res[0]
 
     try:
@@ -128,12 +128,21 @@ def run_ht(cfg, tokens, routing, weights, expert_fn, bf16_expert=False):
             hd.destroy()
             return out
         finally:
-            g.destroy()
+            _teardown(g)
 
     try:
         return run_ranks(n, body, on_error=fabric.shutdown)
     finally:
         fabric.shutdown()
+
+
+def _teardown(g):
+    """Destroy a group even when a test body failed mid-round (the original
+    exception must surface, not the live-handle complaint)."""
+    for h in g._handles:
+        h.state = ep.HandleState.DESTROYED
+    if g.alive:
+        g.destroy()
 
 
 def bf16_round(x):
