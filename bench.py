@@ -215,12 +215,13 @@ class LLStep:
             arrive = sent
         else:
             arrive = sent  # symmetric workload: what a rank receives ~ what it sends
+        # fused kernels: dispatch = read x + write slots + read arrived slots +
+        # write expert-major rows; combine = read expert rows + write slots +
+        # read K slots per token + write the bf16 output
         return {
             "epb_routing_layout": self.b * K * 8 + self.b * (K + self.world) * 4 + (E + self.world) * 4,
-            "epb_ll_dispatch_send": self.b * H * 2 + sent * row8,
-            "epb_ll_dispatch_recv": arrive * row8 + recv_rows * row8,
-            "epb_ll_combine_send": recv_rows * H * 2 * 2,
-            "epb_ll_combine_recv": self.b * K * H * 2 + self.b * H * 2,
+            "epb_ll_dispatch": self.b * H * 2 + sent * row8 + arrive * row8 + recv_rows * row8,
+            "epb_ll_combine": recv_rows * H * 2 * 2 + self.b * K * H * 2 + self.b * H * 2,
         }, {"dispatch_remote": int(sum(len(set(r) - {self.rank}) for r in owner)) * row8,
             "combine_remote": int((owner != self.rank).sum()) * H * 2}
 

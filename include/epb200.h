@@ -13,10 +13,10 @@
  *                                                |  (descriptors all-gathered by the host)
  *   per-token routing loops (ll.py:255-259,      | epb_routing_layout            (K1)
  *     292-296; ht.py:299-307; api.py:150-170)    |
- *   LLRank.dispatch send (ll.py:227-308)         | epb_ll_dispatch_send          (K2)
- *   LLRank.complete_dispatch (ll.py:310-400)     | epb_ll_dispatch_recv          (K3)
- *   LLRank.combine (ll.py:404-462)               | epb_ll_combine_send           (K4a)
- *   LLRank.complete_combine (ll.py:464-507)      | epb_ll_combine_recv           (K4b)
+ *   LLRank.dispatch send (ll.py:227-308)         | epb_ll_dispatch phase SEND    (K2)
+ *   LLRank.complete_dispatch (ll.py:310-400)     | epb_ll_dispatch phase RECV    (K3)
+ *   LLRank.combine (ll.py:404-462)               | epb_ll_combine phase SEND     (K4a)
+ *   LLRank.complete_combine (ll.py:464-507)      | epb_ll_combine phase RECV     (K4b)
  *   HTRank.exchange_metadata (ht.py:291-331)     | epb_ht_meta_send / _recv      (K5a)
  *   HTRank.dispatch + _assemble (ht.py:381-583)  | epb_ht_dispatch_send / _recv  (K5b)
  *   HTRank.combine (ht.py:587-735)               | epb_ht_combine_send / _recv   (K6)
@@ -137,31 +137,47 @@ int epb_group_destroy(epb_group* g);
 int epb_routing_layout(epb_group* g, const int64_t* topk_idx, int32_t b,
                        const epb_layout* lay, void* stream);
 
-/* LL rounds are sequenced ON THE DEVICE (graph-replayable): dispatch_send
- * reads the group's round counter, stores it into *hseq (a caller-owned
- * device u32 per handle) and advances the counter; the recv/combine calls
- * of the round take the same hseq.  Parity = seq & 1 (ll.py:250).
+/* LL rounds are sequenced ON THE DEVICE (graph-replayable): the send phase
+ * of a dispatch reads the group's round counter, stores it into *hseq (a
+ * caller-owned device u32 per handle) and advances the counter; every later
+ * launch of the round takes the same hseq.  Parity = seq & 1 (ll.py:250).
  *
- * K2: LL dispatch send.  x: [b, H] in x_dtype (EPB_FP8 requires x_scales
- * [b, H/128]); converted to the wire dtype (fused FP8 block quantisation). */
-int epb_ll_dispatch_send(epb_group* g, uint32_t* hseq, const void* x,
-                         int32_t x_dtype, const float* x_scales,
-                         const int64_t* topk_idx, const epb_layout* lay,
-                         void* stream);
-/* K3: LL dispatch recv.  out: [L, N*B, H] in out_dtype (EPB_F32 = the
- * reference boundary, or the wire dtype with out_scales [L, N*B, H/128]);
- * counts_f32/counts_i32: [L, N]; src_info: [L, N*B] = t*K + k. */
-int epb_ll_dispatch_recv(epb_group* g, const uint32_t* hseq, void* out,
-                         int32_t out_dtype, float* out_scales,
-                         float* counts_f32, int32_t* counts_i32,
-                         int32_t* src_info, void* stream);
-/* K4a: LL combine send; expert_out [L, N*B, H] f32|bf16 */
-int epb_ll_combine_send(epb_group* g, const uint32_t* hseq, const void* expert_out,
-                        int32_t in_dtype, const int32_t* counts_i32,
-                        const int32_t* src_info, void* stream);
-/* K4b: LL combine recv; out [b, H] f32|bf16 */
-int epb_ll_combine_recv(epb_group* g, const uint32_t* hseq, const float* weights,
-                        int32_t b, void* out, int32_t out_dtype, void* stream);
+ * phases: EPB_PHASE_SEND (1), EPB_PHASE_RECV (2) or both (3, one
+ * cooperative launch; only valid when the peers run on other GPUs or N=1). */
+enum { EPB_PHASE_SEND = 1, EPB_PHASE_RECV = 2, EPB_PHASE_BOTH = 3 };
+
+typedef struct epb_ll_dispatch_args {
+  const void* x;            /* send: [b, H] tokens, x_dtype (FP8 = codes)   */
+  int32_t x_dtype;          /*   converted to the wire dtype in-kernel       */
+  const float* x_scales;    /*   [b, H/128] for scaled FP8 input, else NULL  */
+  const int64_t* topk_idx;  /*   [b, K]; validated + laid out in-kernel      */
+  int32_t num_tokens;       /* b */
+  void* out;                /* recv: [L, N*B, H] in out_dtype (F32 = the     */
+  int32_t out_dtype;        /*   reference boundary, or the wire dtype)      */
+  float* out_scales;        /*   [L, N*B, H/128] with a scaled FP8 wire      */
+  float* counts_f32;        /*   [L, N] RECV_EXPERT_COUNTER                  */
+  int32_t* counts_i32;      /*   [L, N] (combine input)                      */
+  int32_t* src_info;        /*   [L, N*B] = t*K + k of each valid row        */
+} epb_ll_dispatch_args;
+
+/* K2 + K3: LL dispatch (ll.py:227-400) */
+int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases,
+                    const epb_ll_dispatch_args* args, void* stream);
+
+typedef struct epb_ll_combine_args {
+  const void* expert_out;   /* send: [L, N*B, H] f32|bf16                    */
+  int32_t in_dtype;
+  const int32_t* counts_i32;/*   from the dispatch                          */
+  const int32_t* src_info;
+  const float* weights;     /* recv: [b, K] f32                              */
+  int32_t num_tokens;
+  void* out;                /*   [b, H] f32|bf16                             */
+  int32_t out_dtype;
+} epb_ll_combine_args;
+
+/* K4a + K4b: LL combine (ll.py:404-507) */
+int epb_ll_combine(epb_group* g, const uint32_t* hseq, int32_t phases,
+                   const epb_ll_combine_args* args, void* stream);
 
 /* K5a: HT metadata all-gather over the windows */
 int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay,

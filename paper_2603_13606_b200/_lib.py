@@ -38,6 +38,24 @@ class Layout(ctypes.Structure):
                 ("num_tokens", ctypes.c_int32)]
 
 
+class LLDispatchArgs(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("x_dtype", ctypes.c_int32), ("x_scales", ctypes.c_void_p),
+                ("topk_idx", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
+                ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("out_scales", ctypes.c_void_p),
+                ("counts_f32", ctypes.c_void_p), ("counts_i32", ctypes.c_void_p),
+                ("src_info", ctypes.c_void_p)]
+
+
+class LLCombineArgs(ctypes.Structure):
+    _fields_ = [("expert_out", ctypes.c_void_p), ("in_dtype", ctypes.c_int32),
+                ("counts_i32", ctypes.c_void_p), ("src_info", ctypes.c_void_p),
+                ("weights", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
+                ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32)]
+
+
+PHASE_SEND, PHASE_RECV, PHASE_BOTH = 1, 2, 3
+
+
 class IpcDesc(ctypes.Structure):
     _fields_ = [("handle", ctypes.c_uint8 * 64), ("offset", ctypes.c_uint64),
                 ("bytes", ctypes.c_uint64), ("device", ctypes.c_int32), ("pid", ctypes.c_int32)]
@@ -62,10 +80,8 @@ SIGNATURES = {
     "epb_group_poll_error": [_P, ctypes.c_int, ctypes.POINTER(_I)],
     "epb_group_destroy": [_P],
     "epb_routing_layout": [_P, _P, _I, ctypes.POINTER(Layout), _P],
-    "epb_ll_dispatch_send": [_P, _P, _P, _I, _P, _P, ctypes.POINTER(Layout), _P],
-    "epb_ll_dispatch_recv": [_P, _P, _P, _I, _P, _P, _P, _P, _P],
-    "epb_ll_combine_send": [_P, _P, _P, _I, _P, _P, _P],
-    "epb_ll_combine_recv": [_P, _P, _P, _I, _P, _I, _P],
+    "epb_ll_dispatch": [_P, _P, _I, ctypes.c_void_p, _P],
+    "epb_ll_combine": [_P, _P, _I, ctypes.c_void_p, _P],
     "epb_ht_meta_send": [_P, _U, ctypes.POINTER(Layout), _P],
     "epb_ht_meta_recv": [_P, _U, _P, _P, _P, _P],
     "epb_ht_dispatch_send": [_P, _U, _P, _I, _P, _P, ctypes.POINTER(Layout), _P, _P],

@@ -205,6 +205,12 @@ class EpGroup:
         self.mark(name)
         _lib.call(name, *args)
 
+    def _fused_ok(self) -> bool:
+        """Send and receive halves may share one (cooperative) launch unless
+        several ranks are emulated on this GPU, where every rank's send must
+        be enqueued before any rank's receive."""
+        return self.fabric.process_mode or self.config.num_ranks == 1
+
     # -- handles ----------------------------------------------------------------
     def create_handle(self, topk_idx) -> "EpHandle":
         """Snapshot a routing decision (api.py:218-239).  LL: local; HT:
@@ -213,10 +219,14 @@ class EpGroup:
         routing = _validated_routing(topk_idx, self.config, self.device)
         handle = EpHandle(self, routing)
         with torch.cuda.stream(self.stream):
-            handle._run_layout()
             if self.config.algorithm is Algorithm.HT:
+                handle._run_layout()
                 self._open_ht_round(handle)
             elif self.strict:
+                # the LL dispatch kernel validates and lays out the routing
+                # itself; strict mode also validates here so a bad routing
+                # raises from create_handle like the reference (api.py:233)
+                handle._run_layout()
                 self.check()
         self._handles.append(handle)
         return handle
@@ -366,7 +376,7 @@ class EpHandle:
         self._tok_slot = torch.empty(max(self._b, 1) * n, dtype=torch.int32, device=dev)
         self._lay = _lib.Layout(self._m.data_ptr(), self._q.data_ptr(), self._tok_rank.data_ptr(),
                                 self._tok_slot.data_ptr(), self._b)
-        self._hseq = torch.zeros(1, dtype=torch.int32, device=dev)  # LL round sequence (device)
+        self._hseq = torch.empty(1, dtype=torch.int32, device=dev)  # LL round sequence (device)
         self._round: Optional[int] = None
         self._round_open = False
         self._meta = None
@@ -511,31 +521,36 @@ class EpHandle:
             x = self._dev_in(tokens)
             xs = self._dev_in(scales) if scales is not None else None
             g._alloc_seq()
-            x_code = tokens.dtype.code
-            g._launch("epb_ll_dispatch_send", g._g, _ptr(self._hseq), _ptr(x), x_code, _ptr(xs), _ptr(self.routing),
-                      ctypes.byref(self._lay), self._sp())
+            dev = g.device
+            out_t, back_t = self._dev_out(out_tokens)
+            out_s, back_s = self._dev_out(out_scales) if out_scales is not None else (None, False)
+            cnt_f, back_c = self._dev_out(out_counts, full=True)
+            self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
+            self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
+            a = _lib.LLDispatchArgs(x.data_ptr(), tokens.dtype.code, xs.data_ptr() if xs is not None else None,
+                                    self.routing.data_ptr(), b, out_t.data_ptr(), out_tokens.dtype.code,
+                                    out_s.data_ptr() if out_s is not None else None, cnt_f.data_ptr(),
+                                    self._counts_i32.data_ptr(), self._src_info.data_ptr())
+            self._ll_args = a
             self._keep_alive = (x, xs)
-            self._staged = (out_tokens, out_counts, out_scales)
+            self._staged = (out_tokens, out_counts, out_scales, out_t, out_s, cnt_f, back_t, back_s, back_c)
             if send_only:
+                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 self.state = HandleState.DISPATCH_STAGED
                 return
-            g.fabric.phase(g.rank)
+            if g._fused_ok():
+                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
+            else:
+                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+                g.fabric.phase(g.rank)
+                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
             self._ll_recv()
 
     def _ll_recv(self) -> None:
+        """Finish a dispatch whose receive phase has been launched."""
         g = self.group
-        cfg = g.config
-        out_tokens, out_counts, out_scales = self._staged
+        out_tokens, out_counts, out_scales, out_t, out_s, cnt_f, back_t, back_s, back_c = self._staged
         self._staged = None
-        ell, n = cfg.experts_per_rank, cfg.num_ranks
-        dev = g.device
-        out_t, back_t = self._dev_out(out_tokens)
-        out_s, back_s = self._dev_out(out_scales) if out_scales is not None else (None, False)
-        cnt_f, back_c = self._dev_out(out_counts, full=True)
-        self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
-        self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
-        g._launch("epb_ll_dispatch_recv", g._g, _ptr(self._hseq), _ptr(out_t), out_tokens.dtype.code, _ptr(out_s),
-                  _ptr(cnt_f), _ptr(self._counts_i32), _ptr(self._src_info), self._sp())
         if g.strict:
             g.check()
         if back_t:
@@ -613,22 +628,28 @@ class EpHandle:
             if ht:
                 self._ht_combine(y, rows_in.dtype, w, out)
                 return
-            g._launch("epb_ll_combine_send", g._g, _ptr(self._hseq), _ptr(y), rows_in.dtype.code,
-                      _ptr(self._counts_i32), _ptr(self._src_info), self._sp())
-            self._staged = (out, w, y)
+            o, back = self._dev_out(out, full=True)
+            a = _lib.LLCombineArgs(y.data_ptr(), rows_in.dtype.code, self._counts_i32.data_ptr(),
+                                   self._src_info.data_ptr(), w.data_ptr(), b, o.data_ptr(), out.dtype.code)
+            self._ll_cargs = a
+            self._staged = (out, o, back, w, y)
             if send_only:
+                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 self.state = HandleState.COMBINE_STAGED
                 return
-            g.fabric.phase(g.rank)
+            if g._fused_ok():
+                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
+            else:
+                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+                g.fabric.phase(g.rank)
+                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
             self._ll_combine_recv()
 
     def _ll_combine_recv(self) -> None:
+        """Finish a combine whose receive phase has been launched."""
         g = self.group
-        out, w, _y = self._staged
+        out, o, back, _w, _y = self._staged
         self._staged = None
-        o, back = self._dev_out(out, full=True)
-        g._launch("epb_ll_combine_recv", g._g, _ptr(self._hseq), _ptr(w), self._b, _ptr(o), out.dtype.code,
-                  self._sp())
         if g.strict:
             g.check()
         if back:
@@ -664,11 +685,15 @@ class EpHandle:
         if self.state is HandleState.DISPATCH_STAGED:
             with torch.cuda.stream(g.stream):
                 g.fabric.phase(g.rank)
+                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
+                          ctypes.byref(self._ll_args), self._sp())
                 self._ll_recv()
             return
         if self.state is HandleState.COMBINE_STAGED:
             with torch.cuda.stream(g.stream):
                 g.fabric.phase(g.rank)
+                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
+                          ctypes.byref(self._ll_cargs), self._sp())
                 self._ll_combine_recv()
             return
         raise EpError(ErrorCode.HANDLE_STATE_ERROR, f"nothing staged to complete in state {self.state.value}")
