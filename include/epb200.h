@@ -129,6 +129,9 @@ int epb_group_open_peers(epb_group* g, const epb_ipc_desc* descs);
 /* single-process emulation: peer windows are plain device pointers */
 int epb_group_set_peers(epb_group* g, const uint64_t* peer_windows);
 int epb_group_set_timeout(epb_group* g, uint64_t timeout_ns);
+/* diagnostics: with a device buffer of >= grid*16 u64, LL kernels stamp
+ * %globaltimer at phase checkpoints (thread 0 of each CTA); NULL disables */
+int epb_group_set_trace(epb_group* g, uint64_t* trace);
 /* reads (and with clear!=0 resets) the device error word; synchronises */
 int epb_group_poll_error(epb_group* g, int clear, int32_t* code);
 int epb_group_destroy(epb_group* g);

@@ -13,13 +13,16 @@
 namespace epb {
 
 constexpr int kMaxRanksHost = 64;
+// LL kernels run a fixed, rank-independent grid (2 CTAs per B200 SM) so every
+// rank knows how many per-CTA flags each peer publishes
+constexpr int kLLGrid = 296;
 
 inline size_t a16(size_t x) { return (x + 15) / 16 * 16; }
 inline size_t a256(size_t x) { return (x + 255) / 256 * 256; }
 inline int width_of(int dt) { return dt == EPB_F32 ? 4 : (dt == EPB_FP8 ? 1 : 2); }
 
 // LL, per parity:
-//   [disp counters: L*N u64][comb counters: E u64]         (256-aligned)
+//   [count words: L*N u64][dispatch flags: N*grid u64][combine flags: N*grid u64]
 //   [disp slots: n_disp x slot_stride]                      (256-aligned)
 //   [comb slots: n_comb x comb_stride]
 // slot = [row RBp][scales SBp][hdr: t, kcount, K ids, K ranks (HBp)]
@@ -28,7 +31,8 @@ struct LLGeom {
   int RB, RBp, SB, SBp, HB, HBp, CB;
   int slot_stride, comb_stride;
   int64_t n_disp, n_comb;
-  uint64_t disp_ctr, comb_ctr, disp_slot, comb_slot;  // offsets within a parity
+  uint64_t disp_ctr, disp_flag, comb_flag, disp_slot, comb_slot;  // offsets within a parity
+  int grid;  // CTAs of every LL launch (kLLGrid)
   uint64_t parity_bytes, window_bytes, logical_bytes;
 };
 
@@ -68,9 +72,13 @@ inline void make_ll_geom(const epb_config& c, LLGeom& g) {
     g.n_disp = (int64_t)g.N * g.B;
     g.n_comb = (int64_t)g.B * g.K;
   }
+  // per parity: count words [L*N] (m, q of each (local expert, src) pair),
+  // dispatch flags [N src][grid CTA], combine flags [N src][grid CTA]
+  g.grid = kLLGrid;
   g.disp_ctr = 0;
-  g.comb_ctr = pairs * 8;
-  g.disp_slot = a256(g.comb_ctr + (uint64_t)g.E * 8);
+  g.disp_flag = pairs * 8;
+  g.comb_flag = g.disp_flag + (uint64_t)g.N * g.grid * 8;
+  g.disp_slot = a256(g.comb_flag + (uint64_t)g.N * g.grid * 8);
   g.comb_slot = a256(g.disp_slot + (uint64_t)g.n_disp * g.slot_stride);
   g.parity_bytes = a256(g.comb_slot + (uint64_t)g.n_comb * g.comb_stride);
   g.window_bytes = 2 * g.parity_bytes;

@@ -197,6 +197,7 @@ int epb_group_open_peers(epb_group* g, const epb_ipc_desc* descs) {
   }
   EPB_CUDA(cudaMemcpy(g->d_peers, ptrs.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice));
   g->peers_ready = true;
+  g->sys_scope = true;
   return EPB_OK;
 }
 
@@ -205,6 +206,12 @@ int epb_group_set_peers(epb_group* g, const uint64_t* peer_windows) {
   EPB_CUDA(cudaMemcpy(g->d_peers, peer_windows, sizeof(uint64_t) * g->cfg.num_ranks,
                       cudaMemcpyHostToDevice));
   g->peers_ready = true;
+  return EPB_OK;
+}
+
+int epb_group_set_trace(epb_group* g, uint64_t* trace) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  g->trace = trace;
   return EPB_OK;
 }
 

@@ -24,7 +24,9 @@ struct epb_group {
   epb::LLGeom ll;
   epb::HTGeom ht;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  uint64_t* trace = nullptr;    // optional [grid][16] globaltimer stamps (diagnostics)
   bool peers_ready = false;
+  bool sys_scope = false;       // peers on other GPUs: system-scope fences/flags
 };
 
 namespace epb {

@@ -1,42 +1,77 @@
 // Low-Latency dispatch / combine: two kernels per round (K2+K3 fused, K4a+K4b
-// fused), each runnable as send-only, recv-only or both (cooperative launch).
+// fused), each runnable as send-only, recv-only or both (one cooperative
+// launch).  Every LL launch uses the same fixed grid (kLLGrid CTAs) on every
+// rank, so a receiver knows how many per-CTA flags each peer publishes.
 //
 // Reference semantics (epsim ll.py):
 //  * dispatch send (ll.py:255-308): per destination rank d, the tokens that
-//    touch d go, ascending t, into d's slots [src*B + j]; afterwards one
-//    counter per (local expert of d, src) carries m(e, src) + 1.  Here the
-//    counter word is (tag << 40) | (q << 20) | m, published with a release
-//    fence after this rank's last slot store to d.  The tag (from the round
+//    touch d go, ascending t, into d's slots [src*B + j]; the receiver learns
+//    m(e, src) per (local expert, src) pair (the reference's counter value
+//    m + 1).  Here CTA 0 of the source writes the tagged count words
+//    (tag << 40) | (q << 20) | m and every source CTA publishes one tagged
+//    flag per destination after a release fence; the tag (from the round
 //    sequence) replaces the reference's counter reset (ll.py:351-353).
-//  * dispatch recv (ll.py:310-400): wait for the counters, then place every
-//    slot row at recv[l, src*B + i] for each local expert; i (the filled[l]
-//    order) and j (the slot) are computed by the SENDER from its routing in
-//    shared memory (ballot-free prefix counts over earlier tokens) and i is
-//    carried in the slot header after the reference header fields.
+//  * dispatch recv (ll.py:310-400): after all flags of all sources, every
+//    slot row goes to recv[l, src*B + i] for each local expert; i (the
+//    filled[l] order) and j (the slot) are prefix counts the SENDER computes
+//    over its earlier tokens, i travels in the slot header after the
+//    reference header fields (layout.py:282-295).
 //  * combine send (ll.py:404-462): each valid expert row (l, src, i) goes,
-//    re-encoded in the combine wire dtype, to src's slot t*K + k; then one
-//    flag per (expert rank -> home rank).
+//    in the combine wire dtype, to src's slot t*K + k.
 //  * combine recv (ll.py:464-507): out[t] = sum_k w[t,k] * y_k in f32,
 //    ascending k from acc = 0, explicit __fmul_rn/__fadd_rn (no FMA).
 //
-// Latency design: routing layout, validation and the per-destination
-// counts are computed inside the dispatch kernel from a shared-memory copy of
-// topk_idx; copies keep 8 x 16 B loads in flight per lane before storing.
+// Latency design (B200): the token row is prefetched into registers at
+// kernel start so its DRAM latency hides behind the routing pass; routing
+// validation, counts and prefix ranks are one parallel shared-memory pass;
+// flags replace atomics; copies keep 8 x 16 B loads in flight per lane;
+// fences/flags use GPU scope when every rank lives on this GPU.
 #include "common.cuh"
 #include "internal.h"
-#include "layout.cuh"
 
 namespace epb {
 
 constexpr int kPhaseSend = 1, kPhaseRecv = 2;
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kUnroll = 8;
+constexpr int kParts = 4;  // combine send: warps per row
+
+// diagnostics: thread 0 of each CTA stamps the global timer at checkpoints
+#define LL_STAMP(P, I)                                                                    \
+  do {                                                                                   \
+    if ((P).trace && threadIdx.x == 0) (P).trace[blockIdx.x * 16 + (I)] = globaltimer(); \
+  } while (0)
 
 EPB_DEV uint32_t ll_tag_of(uint32_t seq) { return (seq % 0xFFFFFFu) + 1u; }
 EPB_DEV uint32_t ld_volatile_u32(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
 EPB_DEV uint8_t* peer_base(const uint64_t* peers, int r) { return reinterpret_cast<uint8_t*>(peers[r]); }
-EPB_DEV void st_relaxed_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+
+EPB_DEV void fence_scoped(bool sys) {
+  if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+EPB_DEV void st_flag(uint64_t* p, uint64_t v, bool sys) {
+  if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+EPB_DEV uint64_t ld_flag(const uint64_t* p, bool sys) {
+  uint64_t v;
+  if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin until the low 32 bits equal `tag` (bounded; records TransportClosed)
+EPB_DEV bool wait_flag(const uint64_t* f, uint32_t tag, bool sys, uint64_t timeout_ns, int* err) {
+  uint64_t start = 0;
+  for (int spins = 0;; ++spins) {
+    if ((uint32_t)ld_flag(f, sys) == tag) return true;
+    if (*(volatile int*)err != 0) return false;
+    if (spins == 64) start = globaltimer();
+    if (spins > 64 && (spins & 255) == 0 && globaltimer() - start > timeout_ns) {
+      atomicCAS(err, 0, EPB_TRANSPORT_CLOSED);
+      return false;
+    }
+  }
 }
 EPB_DEV int4 ld_weak_v4(const void* p) {
   int4 v;
@@ -47,19 +82,19 @@ EPB_DEV void st_weak_v4(void* p, int4 v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
 }
 
-// Warp-cooperative copy of nch 16-byte chunks, kUnroll loads in flight per lane.
-EPB_DEV void warp_copy16(const uint8_t* src, uint8_t* dst, int nch, int lane) {
-  for (int base = 0; base < nch; base += 32 * kUnroll) {
+// Warp-cooperative copy of chunks [c0, c1) (16 B each), kUnroll loads in flight per lane.
+EPB_DEV void warp_copy16(const uint8_t* src, uint8_t* dst, int c0, int c1, int lane) {
+  for (int base = c0; base < c1; base += 32 * kUnroll) {
     int4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int c = base + u * 32 + lane;
-      if (c < nch) v[u] = ld_weak_v4(src + (int64_t)c * 16);
+      if (c < c1) v[u] = ld_weak_v4(src + (int64_t)c * 16);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int c = base + u * 32 + lane;
-      if (c < nch) st_weak_v4(dst + (int64_t)c * 16, v[u]);
+      if (c < c1) st_weak_v4(dst + (int64_t)c * 16, v[u]);
     }
   }
 }
@@ -87,6 +122,19 @@ EPB_DEV uint32_t ll_round_seq(uint32_t* dseq, int* drd, uint32_t* hseq, bool all
   return s_seq;
 }
 
+template <int XT, int EPC>
+EPB_DEV void load_input_chunk(const uint8_t* xrow, const float* xsc, int64_t e0, float* f) {
+  load_elems_vec<XT, EPC>(xrow, e0, f);
+  if constexpr (XT == EPB_FP8) {
+    // fp8 input with block scales: dequantise (core.py:153-162); without
+    // scales the codes are plain E4M3 values (implicit scale 1)
+    if (xsc != nullptr) {
+#pragma unroll
+      for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[(e0 + i) >> 7]);
+    }
+  }
+}
+
 // ===========================================================================
 // dispatch
 // ===========================================================================
@@ -102,40 +150,15 @@ struct LLDisp {
   int32_t* src_info;
   const uint64_t* peers;
   const uint8_t* win;
-  int* done;
   int* err;
   uint32_t* dseq;
   int* drd;
+  uint64_t* trace;
   LLGeom g;
   uint64_t timeout_ns;
   int b, rank, phases;
+  bool sys;
 };
-
-// Convert elements [e0, e0 + EPC) of an input row (dtype XT) to f32.
-template <int XT, int EPC>
-EPB_DEV void load_input_chunk(const uint8_t* xrow, const float* xsc, int64_t e0, float* f) {
-  load_elems_vec<XT, EPC>(xrow, e0, f);
-  if constexpr (XT == EPB_FP8) {
-    // fp8 input with block scales: dequantise (core.py:153-162); without
-    // scales the codes are plain E4M3 values (implicit scale 1)
-    if (xsc != nullptr) {
-#pragma unroll
-      for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[(e0 + i) >> 7]);
-    }
-  }
-}
-
-// counters of pairs (l, src = rank) at destination d
-EPB_DEV void ll_publish_disp(const LLDisp& p, int d, const int* s_m, int qd, uint64_t parity_off,
-                             uint32_t tag) {
-  const LLGeom& g = p.g;
-  uint64_t* ctr = reinterpret_cast<uint64_t*>(peer_base(p.peers, d) + parity_off + g.disp_ctr);
-  for (int l = 0; l < g.L; ++l) {
-    const int e = d * g.L + l;
-    const uint64_t m = e < g.E ? (uint64_t)s_m[e] : 0ull;
-    st_relaxed_sys(&ctr[l * g.N + p.rank], ((uint64_t)tag << 40) | ((uint64_t)qd << 20) | m);
-  }
-}
 
 // copy one received slot row (WT, optional scales) to an output row (OT)
 template <int WT, bool SC, int OT>
@@ -145,7 +168,7 @@ EPB_DEV void ll_copy_row(const LLGeom& g, const uint8_t* slot, uint8_t* orow, fl
     constexpr int EPC = Elems<WT>::n;
     const int nch = H / EPC;
     if constexpr (OT == WT) {
-      warp_copy16(slot, orow, nch, lane);
+      warp_copy16(slot, orow, 0, nch, lane);
       if constexpr (SC) {
         const float* sc = reinterpret_cast<const float*>(slot + g.RBp);
         for (int i = lane; i < H / 128; i += 32) osc[i] = sc[i];
@@ -193,52 +216,124 @@ template <int XT, int WT, bool SC, int OT>
 __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   extern __shared__ int smem[];
   const LLGeom& g = p.g;
-  const int K = g.K, N = g.N, H = g.H, L = g.L, E = g.E, B = g.B;
+  const int K = g.K, N = g.N, H = g.H, L = g.L, E = g.E, B = g.B, G = g.grid;
   const int b = p.b;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool sys = p.sys;
+  constexpr int EPC = Elems<WT>::n;
+  constexpr int XW = XT == EPB_F32 ? 4 : (XT == EPB_FP8 ? 1 : 2);
+  constexpr int NV = (EPC * XW) >= 16 ? (EPC * XW) / 16 : 0;  // 16-B input loads per chunk
+  const bool vec = (H & 15) == 0;
+  const int nch = vec ? H / EPC : 0;
+
+  // prefetch this CTA's first token chunk: its DRAM latency overlaps the
+  // routing pass below
+  int4 xr[NV > 0 ? NV : 1];
+  const bool pre = (p.phases & kPhaseSend) && NV > 0 && vec && (int)blockIdx.x < b && (int)threadIdx.x < nch;
+  if (pre) {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.x) +
+                         ((int64_t)blockIdx.x * H + (int64_t)threadIdx.x * EPC) * XW;
+#pragma unroll
+    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) xr[v] = ld_nc_v4(src + 16 * v);
+  }
+  LL_STAMP(p, 0);
   const uint32_t seq = ll_round_seq(p.dseq, p.drd, p.hseq, p.phases & kPhaseSend);
   const uint32_t tag = ll_tag_of(seq);
   const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+  LL_STAMP(p, 1);
 
   if (p.phases & kPhaseSend) {
-    // shared: topk snapshot, layout outputs, per-warp histograms
-    const int nwarps = blockDim.x >> 5;
-    int* s_topk = smem;                              // [b*K]
-    int* s_rank = s_topk + b * K;                    // [b*K]
-    int* s_slot = s_rank + b * K;                    // [b*N]
-    int* s_m = s_slot + b * N;                       // [E]
-    int* s_q = s_m + E;                              // [N]
-    BlockLayoutSmem lsm;
-    lsm.hist = s_q + N;                              // [nwarps][E+N]
-    lsm.ballot = reinterpret_cast<uint32_t*>(lsm.hist + nwarps * (E + N));
-    __shared__ int s_bad;
-    __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks], s_nd;
+    int* s_topk = smem;                                                            // [b*K]
+    uint64_t* s_mask = reinterpret_cast<uint64_t*>(s_topk + ((b * K + 1) & ~1));  // [b]
+    int* s_m = reinterpret_cast<int*>(s_mask + b);                                 // [E]
+    int* s_q = s_m + E;                                                            // [N]
+    __shared__ int s_bad, s_nd;
+    __shared__ int s_cnt[2 * kMaxTopK];
+    __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks];
     __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
-    for (int i = threadIdx.x; i < b * K; i += blockDim.x) s_topk[i] = (int)p.topk[i];
+    for (int i = threadIdx.x; i < E + N; i += blockDim.x) s_m[i] = 0;
+    if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
-    // validation before any traffic (api.py:150-170): every CTA reaches the
-    // same verdict on the same routing, so no CTA sends anything on error
-    if (!block_validate(p.topk, b, K, E, &s_bad)) {
+    // routing rows: snapshot, validation (api.py:150-170), per-expert and
+    // per-destination counts, destination masks
+    for (int t = threadIdx.x; t < b; t += blockDim.x) {
+      int ids[kMaxTopK];
+      bool ok = true;
+      uint64_t mask = 0;
+      for (int k = 0; k < K; ++k) {
+        const int64_t e = p.topk[(int64_t)t * K + k];
+        ok &= (e >= 0 && e < E);
+        ids[k] = (int)e;
+      }
+      for (int k = 0; ok && k < K; ++k)
+        for (int j = 0; j < k; ++j) ok &= ids[j] != ids[k];
+      if (!ok) { s_bad = 1; continue; }
+      for (int k = 0; k < K; ++k) {
+        s_topk[t * K + k] = ids[k];
+        atomicAdd(&s_m[ids[k]], 1);
+        mask |= 1ull << (ids[k] / L);
+      }
+      s_mask[t] = mask;
+      for (uint64_t mm = mask; mm; mm &= mm - 1) atomicAdd(&s_q[__ffsll(mm) - 1], 1);
+    }
+    __syncthreads();
+    if (s_bad) {
+      // validation before any traffic: every CTA reaches the same verdict
       if (threadIdx.x == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
       return;
     }
-    block_layout(s_topk, b, K, E, N, L, lsm, s_m, s_q, s_rank, s_slot, nullptr);
+    LL_STAMP(p, 2);
     const uint64_t slot_off = parity_off + g.disp_slot;
     const int64_t slot_base = (int64_t)p.rank * B;
-    for (int t = blockIdx.x; t < b; t += gridDim.x) {
+    for (int t = blockIdx.x; t < b; t += G) {
+      // prefix counts over earlier tokens: i(t,k) = #{t' < t : e_tk in row t'}
+      // and, for the owner d_k of e_tk, j = #{t' < t : d_k in mask t'}
+      if ((int)threadIdx.x < 2 * K) s_cnt[threadIdx.x] = 0;
+      __syncthreads();
+      for (int kg = 0; kg < K; kg += 8) {
+        int ek[8], dk[8], ce[8], cd[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          ek[u] = kg + u < K ? s_topk[t * K + kg + u] : -1;
+          dk[u] = ek[u] >= 0 ? ek[u] / L : 0;
+          ce[u] = 0;
+          cd[u] = 0;
+        }
+        for (int tp = threadIdx.x; tp < t; tp += blockDim.x) {
+          const uint64_t m = s_mask[tp];
+          for (int j = 0; j < K; ++j) {
+            const int e2 = s_topk[tp * K + j];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ce[u] += (e2 == ek[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cd[u] += (int)((m >> dk[u]) & 1);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int a = __reduce_add_sync(0xffffffffu, ce[u]);
+          const int c = __reduce_add_sync(0xffffffffu, cd[u]);
+          if (lane == 0 && kg + u < K) {
+            if (a) atomicAdd(&s_cnt[kg + u], a);
+            if (c) atomicAdd(&s_cnt[K + kg + u], c);
+          }
+        }
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
         int nd = 0;
-        for (int d = 0; d < N; ++d) {
-          const int j = s_slot[t * N + d];
-          if (j >= 0) { s_dst[nd] = d; s_j[nd] = j; ++nd; }
+        for (int k = 0; k < K; ++k) {
+          const int e = s_topk[t * K + k];
+          const int d = e / L;
+          bool seen = false;
+          for (int i = 0; i < nd; ++i) seen |= s_dst[i] == d;
+          if (!seen) { s_dst[nd] = d; s_j[nd] = s_cnt[K + k]; ++nd; }
+          s_hdr[2 + k] = (uint32_t)e;
+          s_hdr[2 + K + k] = (uint32_t)s_cnt[k];
         }
         s_nd = nd;
         s_hdr[0] = (uint32_t)t;
         s_hdr[1] = (uint32_t)K;
-      }
-      if (threadIdx.x < K) {
-        s_hdr[2 + threadIdx.x] = (uint32_t)s_topk[t * K + threadIdx.x];
-        s_hdr[2 + K + threadIdx.x] = (uint32_t)s_rank[t * K + threadIdx.x];
       }
       __syncthreads();
       const int nd = s_nd;
@@ -247,14 +342,26 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
           reinterpret_cast<uint32_t*>(slot + g.RBp + g.SBp)[w] = s_hdr[w];
         }
-      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * dtype_width(XT);
+      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
       const float* xsc = p.x_scales ? p.x_scales + (int64_t)t * (H / 128) : nullptr;
-      if ((H & 15) == 0) {
-        constexpr int EPC = Elems<WT>::n;
-        const int nch = H / EPC;
+      if (vec) {
         for (int c = threadIdx.x; c < nch; c += blockDim.x) {
           float f[EPC];
-          load_input_chunk<XT, EPC>(xrow, xsc, (int64_t)c * EPC, f);
+          if (pre && t == (int)blockIdx.x && c == (int)threadIdx.x) {
+            if constexpr (NV > 0) {
+              constexpr int PER = 16 / XW;  // input elements per 16-B load
+#pragma unroll
+              for (int v = 0; v < NV; ++v) unpack16<XT>(xr[v], f + v * PER);
+              if constexpr (XT == EPB_FP8) {
+                if (xsc != nullptr) {
+#pragma unroll
+                  for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[((int64_t)c * EPC + i) >> 7]);
+                }
+              }
+            }
+          } else {
+            load_input_chunk<XT, EPC>(xrow, xsc, (int64_t)c * EPC, f);
+          }
           float scale = 0.0f;
           if constexpr (SC) {
             // block-128 = 8 consecutive 16-element chunks = 8 aligned lanes
@@ -293,53 +400,54 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         }
       }
       __syncthreads();
-      // completion: the last token to land at d publishes d's counters
-      if (threadIdx.x < nd) {
-        const int d = s_dst[threadIdx.x];
-        fence_sys();
-        const int old = atomicAdd(&p.done[d], 1);
-        if (old == s_q[d] - 1) {
-          p.done[d] = 0;
-          fence_sys();
-          ll_publish_disp(p, d, s_m, s_q[d], parity_off, tag);
-        }
-      }
-      __syncthreads();
     }
-    // destinations that receive nothing still get their (m = 0) counters
-    if (blockIdx.x == 0)
-      for (int d = threadIdx.x; d < N; d += blockDim.x)
-        if (s_q[d] == 0) ll_publish_disp(p, d, s_m, 0, parity_off, tag);
+    LL_STAMP(p, 3);
+    // publish: CTA 0 writes the count words of every (local expert, src)
+    // pair at every destination; then every CTA fences and flags each
+    // destination (a receiver waits for all grid CTAs of all sources)
+    if (blockIdx.x == 0) {
+      for (int i = threadIdx.x; i < N * L; i += blockDim.x) {
+        const int d = i / L, l = i - d * L, e = d * L + l;
+        uint64_t* ctr = reinterpret_cast<uint64_t*>(peer_base(p.peers, d) + parity_off + g.disp_ctr);
+        const uint64_t m = e < E ? (uint64_t)s_m[e] : 0ull;
+        ctr[l * N + p.rank] = ((uint64_t)tag << 40) | ((uint64_t)s_q[d] << 20) | m;
+      }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < N) {
+      fence_scoped(sys);
+      uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.disp_flag) +
+                       (int64_t)p.rank * G + blockIdx.x;
+      st_flag(flag, (uint64_t)tag, sys);
+    }
+    LL_STAMP(p, 4);
   }
 
   if (p.phases & kPhaseRecv) {
     __shared__ int s_rq[kMaxRanks], s_pre[kMaxRanks + 1];
     __shared__ int s_fail;
+    LL_STAMP(p, 5);
     const int lo = p.rank * L;
     const int nloc = max(0, min(L, E - lo));
     if (threadIdx.x == 0) s_fail = 0;
     __syncthreads();
-    const uint64_t* ctr = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.disp_ctr);
+    const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.disp_flag);
+    for (int i = threadIdx.x; i < N * G; i += blockDim.x)
+      if (!wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
+    __syncthreads();
+    if (s_fail) return;
+    LL_STAMP(p, 6);
+    const volatile uint64_t* ctr = reinterpret_cast<const volatile uint64_t*>(p.win + parity_off + g.disp_ctr);
     if (blockIdx.x == 0) {
       for (int i = threadIdx.x; i < L * N; i += blockDim.x) {
-        int m = 0;
-        if (i < nloc * N) {
-          uint64_t v = 0;
-          if (!wait_tag(&ctr[i], tag, 40, 0xFFFFFFu, p.timeout_ns, p.err, &v)) { s_fail = 1; continue; }
-          m = (int)(v & 0xFFFFF);
-        }
+        const int m = i < nloc * N ? (int)(ctr[i] & 0xFFFFF) : 0;
         p.counts_i32[i] = m;
         p.counts_f32[i] = (float)m;
       }
     }
     if (nloc == 0) return;
-    if (threadIdx.x < N) {
-      uint64_t v = 0;
-      if (!wait_tag(&ctr[threadIdx.x], tag, 40, 0xFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
-      s_rq[threadIdx.x] = (int)((v >> 20) & 0xFFFFF);
-    }
+    if ((int)threadIdx.x < N) s_rq[threadIdx.x] = (int)((ctr[threadIdx.x] >> 20) & 0xFFFFF);
     __syncthreads();
-    if (s_fail) return;
     if (threadIdx.x == 0) {
       int run = 0;
       for (int s = 0; s < N; ++s) { s_pre[s] = run; run += s_rq[s]; }
@@ -364,6 +472,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + row * orow_bytes,
                               SC ? p.out_scales + row * (H / 128) : nullptr, lane);
     }
+    LL_STAMP(p, 7);
   }
 }
 
@@ -379,19 +488,22 @@ struct LLComb {
   const uint32_t* hseq;
   const uint64_t* peers;
   const uint8_t* win;
-  int* done;
   int* err;
+  uint64_t* trace;
   LLGeom g;
   uint64_t timeout_ns;
   int b, rank, phases;
+  bool sys;
 };
 
 template <int IT, int WT, int OT>
 __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
   extern __shared__ int s_pre[];  // [L*N + 1]
   const LLGeom& g = p.g;
-  const int N = g.N, L = g.L, B = g.B, H = g.H, K = g.K;
+  const int N = g.N, L = g.L, B = g.B, H = g.H, K = g.K, G = g.grid;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool sys = p.sys;
+  LL_STAMP(p, 0);
   __shared__ uint32_t s_seq;
   if (threadIdx.x == 0) s_seq = ld_volatile_u32(p.hseq);
   __syncthreads();
@@ -399,21 +511,17 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
   const uint32_t tag = ll_tag_of(seq);
   const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
   constexpr int EPC = Elems<WT>::n;
+  const bool vec = (H & 15) == 0;
+  const int nch = vec ? H / EPC : 0;
 
   if (p.phases & kPhaseSend) {
-    __shared__ int s_rows_to[kMaxRanks], s_cnt[kMaxRanks], s_wsum[kThreads / 32];
+    __shared__ int s_wsum[kThreads / 32];
     const int P = L * N;
-    if (threadIdx.x < N) { s_rows_to[threadIdx.x] = 0; s_cnt[threadIdx.x] = 0; }
-    __syncthreads();
     // block-wide exclusive scan of the (l, src) counts
     const int per = (P + blockDim.x - 1) / blockDim.x;
     const int i0 = threadIdx.x * per;
     int local = 0;
-    for (int i = i0; i < min(P, i0 + per); ++i) {
-      const int c = p.counts[i];
-      local += c;
-      if (c) atomicAdd(&s_rows_to[i % N], c);
-    }
+    for (int i = i0; i < min(P, i0 + per); ++i) local += p.counts[i];
     int incl = local;
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -430,9 +538,13 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     }
     if (threadIdx.x == blockDim.x - 1) s_pre[P] = run;
     __syncthreads();
+    LL_STAMP(p, 1);
     const int total = s_pre[P];
-    const int gw = blockIdx.x * nw + warp, tw = gridDim.x * nw;
-    for (int r = gw; r < total; r += tw) {
+    const int part = (nch + kParts - 1) / kParts;
+    const int tasks = vec ? total * kParts : total;
+    for (int task = blockIdx.x * nw + warp; task < tasks; task += gridDim.x * nw) {
+      const int r = vec ? task / kParts : task;
+      const int q = vec ? task - r * kParts : 0;
       int lo_i = 0, hi_i = P;  // largest pair with s_pre[pair] <= r
       while (hi_i - lo_i > 1) {
         const int mid = (lo_i + hi_i) >> 1;
@@ -444,24 +556,24 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
       const int info = p.src_info[row];
       uint8_t* dst = peer_base(p.peers, s) + parity_off + g.comb_slot + (int64_t)info * g.comb_stride;
       const uint8_t* yrow = reinterpret_cast<const uint8_t*>(p.y) + row * H * dtype_width(IT);
-      if ((H & 15) == 0) {
-        const int nch = H / EPC;
+      if (vec) {
+        const int c0 = q * part, c1 = min(nch, c0 + part);
         if constexpr (IT == WT) {
-          for (int base = 0; base < nch; base += 32 * kUnroll) {
+          for (int base = c0; base < c1; base += 32 * kUnroll) {
             int4 v[kUnroll];
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
               const int c = base + u * 32 + lane;
-              if (c < nch) v[u] = ld_nc_v4(yrow + (int64_t)c * 16);
+              if (c < c1) v[u] = ld_nc_v4(yrow + (int64_t)c * 16);
             }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
               const int c = base + u * 32 + lane;
-              if (c < nch) st_na_v4(dst + (int64_t)c * 16, v[u]);
+              if (c < c1) st_na_v4(dst + (int64_t)c * 16, v[u]);
             }
           }
         } else {
-          for (int c = lane; c < nch; c += 32) {
+          for (int c = c0 + lane; c < c1; c += 32) {
             float f[EPC];
             load_elems_vec<IT, EPC>(yrow, (int64_t)c * EPC, f);
             st_na_v4(dst + (int64_t)c * 16, pack16<WT>(f));
@@ -470,47 +582,44 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
       } else {
         for (int el = lane; el < H; el += 32) store_elem(dst, WT, el, load_elem(yrow, IT, el));
       }
-      if (lane == 0) atomicAdd(&s_cnt[s], 1);
     }
     __syncthreads();
-    if (threadIdx.x < N) {
-      const int s = threadIdx.x;
-      const int c = s_cnt[s];
-      uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, s) + parity_off + g.comb_ctr) + p.rank;
-      if (c > 0) {
-        fence_sys();
-        const int old = atomicAdd(&p.done[s], c);
-        if (old + c == s_rows_to[s]) {
-          p.done[s] = 0;
-          fence_sys();
-          st_relaxed_sys(flag, (uint64_t)tag);
-        }
-      } else if (blockIdx.x == 0 && s_rows_to[s] == 0) {
-        st_relaxed_sys(flag, (uint64_t)tag);
-      }
+    LL_STAMP(p, 2);
+    if ((int)threadIdx.x < N) {
+      fence_scoped(sys);
+      uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.comb_flag) +
+                       (int64_t)p.rank * G + blockIdx.x;
+      st_flag(flag, (uint64_t)tag, sys);
     }
+    LL_STAMP(p, 3);
   }
 
   if (p.phases & kPhaseRecv) {
     __shared__ float s_w[kMaxTopK];
     __shared__ int s_fail;
+    LL_STAMP(p, 4);
     if (threadIdx.x == 0) s_fail = 0;
     __syncthreads();
-    const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.comb_ctr);
-    if (threadIdx.x < N) {
-      uint64_t v;
-      if (!wait_tag(&flags[threadIdx.x], tag, 0, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
-    }
+    const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.comb_flag);
+    for (int i = threadIdx.x; i < N * G; i += blockDim.x)
+      if (!wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
     __syncthreads();
     if (s_fail) return;
+    LL_STAMP(p, 5);
     const uint8_t* slots = p.win + parity_off + g.comb_slot;
-    for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
-      if (threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
+    // tasks: (token, part of the row), blockDim chunks per task
+    const int parts = vec ? (nch + blockDim.x - 1) / blockDim.x : 1;
+    const int tasks = p.b * parts;
+    for (int task = blockIdx.x; task < tasks; task += gridDim.x) {
+      const int t = task / parts, pt = task - t * parts;
+      __syncthreads();
+      if ((int)threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
       __syncthreads();
       uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
       const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
-      if ((H & 15) == 0) {
-        for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
+      if (vec) {
+        const int c = pt * blockDim.x + threadIdx.x;
+        if (c < nch) {
           float acc[EPC];
 #pragma unroll
           for (int i = 0; i < EPC; ++i) acc[i] = 0.0f;
@@ -540,8 +649,8 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
           store_elem(orow, OT, el, acc);
         }
       }
-      __syncthreads();
     }
+    LL_STAMP(p, 6);
   }
 }
 
@@ -564,17 +673,16 @@ int sm_count() {
 
 template <typename Params>
 cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const Params& p, cudaStream_t s) {
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(smem, 48 * 1024));
+  if (e != cudaSuccess) return e;
   if (coop) {
     // both phases in one launch: CTAs in the receive phase wait on flags the
     // send phase of other CTAs writes, so all CTAs must be co-resident
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     if (e != cudaSuccess) return e;
-    grid = std::max(1, std::min(grid, per_sm * sm_count()));
+    if (per_sm * sm_count() < grid) return cudaErrorCooperativeLaunchTooLarge;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -592,46 +700,45 @@ cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const
 }
 
 template <int XT, int WT, bool SC, int OT>
-cudaError_t run_disp(const LLDisp& p, int grid, size_t smem, cudaStream_t s) {
-  return launch(ll_dispatch_kernel<XT, WT, SC, OT>, grid, smem, p.phases == 3, p, s);
+cudaError_t run_disp(const LLDisp& p, size_t smem, cudaStream_t s) {
+  return launch(ll_dispatch_kernel<XT, WT, SC, OT>, p.g.grid, smem, p.phases == 3, p, s);
 }
 
 template <int XT, int WT, bool SC>
-cudaError_t run_disp_o(const LLDisp& p, int out_dtype, int grid, size_t smem, cudaStream_t s) {
-  if (out_dtype == EPB_F32 || WT == EPB_F32) return run_disp<XT, WT, SC, EPB_F32>(p, grid, smem, s);
-  return run_disp<XT, WT, SC, WT>(p, grid, smem, s);
+cudaError_t run_disp_o(const LLDisp& p, int out_dtype, size_t smem, cudaStream_t s) {
+  if (out_dtype == EPB_F32 || WT == EPB_F32) return run_disp<XT, WT, SC, EPB_F32>(p, smem, s);
+  return run_disp<XT, WT, SC, WT>(p, smem, s);
 }
 
 template <int XT>
-cudaError_t run_disp_x(const LLDisp& p, int out_dtype, int grid, size_t smem, cudaStream_t s) {
+cudaError_t run_disp_x(const LLDisp& p, int out_dtype, size_t smem, cudaStream_t s) {
   switch (p.g.wire) {
-    case EPB_F32: return run_disp_o<XT, EPB_F32, false>(p, out_dtype, grid, smem, s);
-    case EPB_BF16: return run_disp_o<XT, EPB_BF16, false>(p, out_dtype, grid, smem, s);
-    case EPB_F16: return run_disp_o<XT, EPB_F16, false>(p, out_dtype, grid, smem, s);
+    case EPB_F32: return run_disp_o<XT, EPB_F32, false>(p, out_dtype, smem, s);
+    case EPB_BF16: return run_disp_o<XT, EPB_BF16, false>(p, out_dtype, smem, s);
+    case EPB_F16: return run_disp_o<XT, EPB_F16, false>(p, out_dtype, smem, s);
     default:
-      return p.g.scales ? run_disp_o<XT, EPB_FP8, true>(p, out_dtype, grid, smem, s)
-                        : run_disp_o<XT, EPB_FP8, false>(p, out_dtype, grid, smem, s);
+      return p.g.scales ? run_disp_o<XT, EPB_FP8, true>(p, out_dtype, smem, s)
+                        : run_disp_o<XT, EPB_FP8, false>(p, out_dtype, smem, s);
   }
 }
 
 template <int IT, int WT, int OT>
-cudaError_t run_comb(const LLComb& p, int grid, size_t smem, cudaStream_t s) {
-  return launch(ll_combine_kernel<IT, WT, OT>, grid, smem, p.phases == 3, p, s);
+cudaError_t run_comb(const LLComb& p, size_t smem, cudaStream_t s) {
+  return launch(ll_combine_kernel<IT, WT, OT>, p.g.grid, smem, p.phases == 3, p, s);
 }
 
 template <int IT, int WT>
-cudaError_t run_comb_o(const LLComb& p, int out_dtype, int grid, size_t smem, cudaStream_t s) {
-  return out_dtype == EPB_F32 ? run_comb<IT, WT, EPB_F32>(p, grid, smem, s)
-                              : run_comb<IT, WT, EPB_BF16>(p, grid, smem, s);
+cudaError_t run_comb_o(const LLComb& p, int out_dtype, size_t smem, cudaStream_t s) {
+  return out_dtype == EPB_F32 ? run_comb<IT, WT, EPB_F32>(p, smem, s) : run_comb<IT, WT, EPB_BF16>(p, smem, s);
 }
 
 template <int IT>
-cudaError_t run_comb_w(const LLComb& p, int out_dtype, int grid, size_t smem, cudaStream_t s) {
+cudaError_t run_comb_w(const LLComb& p, int out_dtype, size_t smem, cudaStream_t s) {
   switch (p.g.cwire) {
-    case EPB_F32: return run_comb_o<IT, EPB_F32>(p, out_dtype, grid, smem, s);
-    case EPB_BF16: return run_comb_o<IT, EPB_BF16>(p, out_dtype, grid, smem, s);
-    case EPB_F16: return run_comb_o<IT, EPB_F16>(p, out_dtype, grid, smem, s);
-    default: return run_comb_o<IT, EPB_FP8>(p, out_dtype, grid, smem, s);
+    case EPB_F32: return run_comb_o<IT, EPB_F32>(p, out_dtype, smem, s);
+    case EPB_BF16: return run_comb_o<IT, EPB_BF16>(p, out_dtype, smem, s);
+    case EPB_F16: return run_comb_o<IT, EPB_F16>(p, out_dtype, smem, s);
+    default: return run_comb_o<IT, EPB_FP8>(p, out_dtype, smem, s);
   }
 }
 
@@ -672,25 +779,23 @@ int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases, const epb_ll_d
   LLDisp p;
   p.x = a->x; p.x_scales = a->x_scales; p.topk = a->topk_idx; p.hseq = hseq;
   p.out = a->out; p.out_scales = a->out_scales; p.counts_f32 = a->counts_f32; p.counts_i32 = a->counts_i32;
-  p.src_info = a->src_info; p.peers = g->d_peers; p.win = g->window; p.done = g->d_done; p.err = g->d_err;
-  p.dseq = reinterpret_cast<uint32_t*>(g->d_scratch); p.drd = g->d_scratch + 1;
+  p.src_info = a->src_info; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err;
+  p.dseq = reinterpret_cast<uint32_t*>(g->d_scratch); p.drd = g->d_scratch + 1; p.trace = g->trace;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
-  const int recv_warps = (int)std::min<int64_t>(g->ll.n_disp * g->ll.K, 1 << 20);
-  int grid = std::max(b, (recv_warps + 7) / 8);
-  grid = std::max(1, std::min(grid, 2 * sm_count()));
+  p.sys = g->sys_scope;
   const int E = g->ll.E, N = g->ll.N, K = g->ll.K;
   const size_t smem = (phases & kPhaseSend)
-      ? sizeof(int) * ((size_t)2 * b * K + (size_t)b * N + E + N) + BlockLayoutSmem::bytes(kThreads / 32, E, N)
+      ? sizeof(int) * ((size_t)((b * K + 1) & ~1) + (size_t)2 * b + E + N)
       : 0;
   if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "LL batch too large for the fused dispatch kernel");
   cudaStream_t s = as_stream(stream);
   cudaError_t e;
   const int od = a->out_dtype;
   switch ((phases & kPhaseSend) ? a->x_dtype : wire) {
-    case EPB_F32: e = run_disp_x<EPB_F32>(p, od, grid, smem, s); break;
-    case EPB_BF16: e = run_disp_x<EPB_BF16>(p, od, grid, smem, s); break;
-    case EPB_F16: e = run_disp_x<EPB_F16>(p, od, grid, smem, s); break;
-    case EPB_FP8: e = run_disp_x<EPB_FP8>(p, od, grid, smem, s); break;
+    case EPB_F32: e = run_disp_x<EPB_F32>(p, od, smem, s); break;
+    case EPB_BF16: e = run_disp_x<EPB_BF16>(p, od, smem, s); break;
+    case EPB_F16: e = run_disp_x<EPB_F16>(p, od, smem, s); break;
+    case EPB_FP8: e = run_disp_x<EPB_FP8>(p, od, smem, s); break;
     default: return fail(EPB_INVALID_ARGUMENT, "x dtype");
   }
   if (e != cudaSuccess) return cuda_check(e, "ll_dispatch");
@@ -711,16 +816,14 @@ int epb_ll_combine(epb_group* g, const uint32_t* hseq, int32_t phases, const epb
   if (a->in_dtype != EPB_F32 && a->in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
   LLComb p;
   p.y = a->expert_out; p.counts = a->counts_i32; p.src_info = a->src_info; p.w = a->weights; p.out = a->out;
-  p.hseq = hseq; p.peers = g->d_peers; p.win = g->window; p.done = g->d_done + g->cfg.num_ranks;
-  p.err = g->d_err; p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
+  p.hseq = hseq; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err; p.trace = g->trace;
+  p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
+  p.sys = g->sys_scope;
   const size_t smem = sizeof(int) * ((size_t)g->ll.L * g->ll.N + 1);
   if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "too many (expert, rank) pairs for combine");
-  const int rows = g->ll.B * g->ll.K;  // upper bound of rows a rank returns (balanced)
-  int grid = std::max(b, (rows + 7) / 8);
-  grid = std::max(1, std::min(grid, 2 * sm_count()));
   cudaStream_t s = as_stream(stream);
-  cudaError_t e = a->in_dtype == EPB_F32 ? run_comb_w<EPB_F32>(p, a->out_dtype, grid, smem, s)
-                                         : run_comb_w<EPB_BF16>(p, a->out_dtype, grid, smem, s);
+  cudaError_t e = a->in_dtype == EPB_F32 ? run_comb_w<EPB_F32>(p, a->out_dtype, smem, s)
+                                         : run_comb_w<EPB_BF16>(p, a->out_dtype, smem, s);
   if (e != cudaSuccess) return cuda_check(e, "ll_combine");
   return EPB_OK;
 }

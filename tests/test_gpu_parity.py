@@ -339,5 +339,11 @@ def test_host_buffers_round_trip():
     d, comb = _ll_oracle(cfg, wl, owl.expert_identity)
     np.testing.assert_array_equal(cnt.read_f32(), d[0]["counts"])
     np.testing.assert_array_equal(out.read_f32(), d[0]["recv"])
+    w_host = ep.tensor_create((4, 2), ep.Dtype.F32, ep.TensorTag.TOPK_WEIGHTS, buffer=wl.weights[0].copy())
+    comb = ep.tensor_create((4, 32), ep.Dtype.F32, ep.TensorTag.TOKENS, buffer=np.zeros(4 * 32, np.float32))
+    h.combine([out, w_host], [comb])
+    np.testing.assert_array_equal(comb.read_f32(), comb_ref := comb.read_f32())
+    np.testing.assert_array_equal(comb_ref, comb.data.numpy().reshape(4, 32))
+    np.testing.assert_array_equal(comb_ref, _ll_oracle(cfg, wl, owl.expert_identity)[1][0])
     h.destroy()
     g.destroy()
