@@ -226,7 +226,9 @@ class LLStep:
             "combine_remote": int((owner != self.rank).sum()) * H * 2}
 
 
-def capture(step_obj, group, warmup_eager=3):
+def capture(step_obj, group, phases: bool, warmup_eager=3):
+    """One CUDA graph of a whole step between two timing events; with
+    `phases`, every kernel launch inside is also preceded by an event."""
     import torch
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -240,40 +242,55 @@ def capture(step_obj, group, warmup_eager=3):
     group.trace_phases(marks)
     with torch.cuda.graph(graph):
         group.mark("step:start")
+        if not phases:
+            group.trace_phases(None)
         step_obj.step()
+        group.trace_phases(marks)
         group.mark("step:end")
     group.trace_phases(None)
     torch.cuda.synchronize()
     return graph, marks
 
 
+def replay_timed(graph, marks, steps, flush):
+    """Replay `steps` times, L2 flushed before each (outside the events);
+    returns (total ms, {phase: ms})."""
+    import torch
+    names = [m[0] for m in marks]
+    phase = {n: 0.0 for n in names[:-1]}
+    total = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        evs = [m[1] for m in marks]
+        total += evs[0].elapsed_time(evs[-1])
+        for i in range(len(evs) - 1):
+            phase[names[i]] += evs[i].elapsed_time(evs[i + 1])
+    return total, phase
+
+
 def run_ll(args, world, rank):
     import torch
     st = LLStep(world, rank, args.tokens)
-    graph, marks = capture(st, st.g)
+    graph, marks = capture(st, st.g, phases=False)
+    graph_b, marks_b = capture(st, st.g, phases=True)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
         flush.zero_()
         graph.replay()
     barrier(world)
-    names = [m[0] for m in marks]
-    phase = {n: 0.0 for n in names[:-1]}
-    total = 0.0
     with ClockSampler(torch.cuda.current_device()) as clk:
         barrier(world)
-        for _ in range(args.steps):
-            flush.zero_()
-            graph.replay()
-            torch.cuda.synchronize()
-            evs = [m[1] for m in marks]
-            total += evs[0].elapsed_time(evs[-1])
-            for i in range(len(evs) - 1):
-                phase[names[i]] += evs[i].elapsed_time(evs[i + 1])
+        total, _ = replay_timed(graph, marks, args.steps, flush)
         barrier(world)
+    # per-kernel breakdown from the instrumented graph (events between launches)
+    nb = max(10, min(args.steps, 100))
+    _, phase = replay_timed(graph_b, marks_b, nb, flush)
     st.g.check()
     total_max = allreduce_max(total, world)
-    per_phase = {n: v / args.steps * 1000.0 for n, v in phase.items()}  # us
-    launches = sum(1 for n in names if n.startswith("epb_"))
+    per_phase = {n: v / nb * 1000.0 for n, v in phase.items()}  # us
+    launches = sum(1 for n, _ in marks_b if n.startswith("epb_"))
     return st, total_max / args.steps, per_phase, launches * args.steps, clk.report()
 
 

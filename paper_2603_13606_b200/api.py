@@ -216,7 +216,7 @@ class EpGroup:
         """Snapshot a routing decision (api.py:218-239).  LL: local; HT:
         collective (metadata exchange), receive count known on return."""
         self._check_alive()
-        routing = _validated_routing(topk_idx, self.config, self.device)
+        routing = _validated_routing(topk_idx, self.config, self.device, snapshot=self.strict)
         handle = EpHandle(self, routing)
         with torch.cuda.stream(self.stream):
             if self.config.algorithm is Algorithm.HT:
@@ -253,7 +253,7 @@ class EpGroup:
             self._hooks.release(self._buffer)
 
 
-def _validated_routing(topk_idx, cfg: EpConfig, device) -> torch.Tensor:
+def _validated_routing(topk_idx, cfg: EpConfig, device, snapshot: bool = True) -> torch.Tensor:
     """Host-side shape/dtype/capacity checks (api.py:150-170); range and
     distinctness are checked by the routing-layout kernel."""
     if isinstance(topk_idx, torch.Tensor):
@@ -274,7 +274,10 @@ def _validated_routing(topk_idx, cfg: EpConfig, device) -> torch.Tensor:
                       f"{b} routed tokens exceed max_tokens_per_rank {cfg.max_tokens_per_rank}")
     if isinstance(r, np.ndarray):
         r = torch.from_numpy(np.ascontiguousarray(r.astype(np.int64, copy=False)))
-    return r.to(device=device, dtype=torch.int64).contiguous().clone()
+    if not snapshot and r.device == device and r.dtype == torch.int64 and r.is_contiguous():
+        return r  # perf mode: the caller keeps topk_idx unchanged until dispatch
+    out = r.to(device=device, dtype=torch.int64, non_blocking=True).contiguous()
+    return out.clone() if out is r else out
 
 
 def create_group(fabric, rank: int, config: EpConfig, hooks: Optional[AllocationHooks] = None,

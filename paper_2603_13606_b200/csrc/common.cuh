@@ -94,18 +94,34 @@ EPB_DEV float e4m3_value(uint32_t c) {
 // magnitude (searchsorted side="left" over midpoints, core.py:109-120), sign
 // from signbit.  Hardware cvt.rn.satfinite is RNE, so a tie that RNE sent to
 // the larger neighbour is stepped down one code.
-EPB_DEV uint32_t e4m3_encode(float x) {
+//
+// An exact midpoint is recognised from the bits: in the normal range
+// [2^-6, 448] it has fraction bit 19 set and bits 18..0 clear; in the
+// subnormal range it is an odd multiple of 2^-10.  Clearing that half-step
+// (bit 19, or subtracting 2^-10) gives the lower neighbour exactly, which
+// the hardware RNE conversion then encodes without rounding.
+EPB_DEV float e4m3_tie_down(float x) {
   const float a = fminf(fabsf(x), 448.0f);
-  __nv_fp8_storage_t c = __nv_cvt_float_to_fp8(a, __NV_SATFINITE, __NV_E4M3);
-  uint32_t code = (uint32_t)c & 0x7F;
-  if (code > 0) {
-    const float v = e4m3_value(code);
-    if (v > a) {
-      const float lo = e4m3_value(code - 1);
-      if (__fsub_rn(a, lo) == __fsub_rn(v, a)) code -= 1;
-    }
+  const uint32_t u = __float_as_uint(a);
+  if (a >= 0x1p-6f) {
+    if ((u & 0xFFFFFu) == 0x80000u) return __uint_as_float(u & ~0x80000u);
+  } else {
+    const float s = a * 1024.0f;  // exact (power of two)
+    if (s == truncf(s) && (((int)s) & 1)) return __fsub_rn(a, 0x1p-10f);
   }
-  return code | (signbit(x) ? 0x80u : 0u);
+  return a;
+}
+
+EPB_DEV uint32_t e4m3_encode(float x) {
+  const __nv_fp8_storage_t c = __nv_cvt_float_to_fp8(e4m3_tie_down(x), __NV_SATFINITE, __NV_E4M3);
+  return ((uint32_t)c & 0x7F) | (signbit(x) ? 0x80u : 0u);
+}
+
+// two codes at once (one cvt.rn.satfinite.e4m3x2.f32): lo = x0, hi = x1
+EPB_DEV uint32_t e4m3_encode2(float x0, float x1) {
+  const __nv_fp8x2_storage_t c =
+      __nv_cvt_float2_to_fp8x2(make_float2(e4m3_tie_down(x0), e4m3_tie_down(x1)), __NV_SATFINITE, __NV_E4M3);
+  return ((uint32_t)c & 0x7F7Fu) | (signbit(x0) ? 0x80u : 0u) | (signbit(x1) ? 0x8000u : 0u);
 }
 
 EPB_DEV uint16_t bf16_bits_rne(float x) {
@@ -187,8 +203,7 @@ EPB_DEV int4 pack16(const float* f) {
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      w[i] = e4m3_encode(f[4 * i]) | (e4m3_encode(f[4 * i + 1]) << 8) |
-             (e4m3_encode(f[4 * i + 2]) << 16) | (e4m3_encode(f[4 * i + 3]) << 24);
+      w[i] = e4m3_encode2(f[4 * i], f[4 * i + 1]) | (e4m3_encode2(f[4 * i + 2], f[4 * i + 3]) << 16);
   }
   return make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
 }

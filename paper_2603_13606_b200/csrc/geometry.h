@@ -13,9 +13,10 @@
 namespace epb {
 
 constexpr int kMaxRanksHost = 64;
-// LL kernels run a fixed, rank-independent grid (2 CTAs per B200 SM) so every
-// rank knows how many per-CTA flags each peer publishes
-constexpr int kLLGrid = 296;
+// LL kernels run a fixed, rank-independent grid (one 512-thread CTA per B200
+// SM, co-resident for the cooperative fused launch) so every rank knows how
+// many per-CTA flags each peer publishes
+constexpr int kLLGrid = 148;
 
 inline size_t a16(size_t x) { return (x + 15) / 16 * 16; }
 inline size_t a256(size_t x) { return (x + 255) / 256 * 256; }

@@ -65,9 +65,10 @@ EPB_DEV bool wait_flag(const uint64_t* f, uint32_t tag, bool sys, uint64_t timeo
   uint64_t start = 0;
   for (int spins = 0;; ++spins) {
     if ((uint32_t)ld_flag(f, sys) == tag) return true;
+    if ((spins & 31) != 31) continue;
     if (*(volatile int*)err != 0) return false;
-    if (spins == 64) start = globaltimer();
-    if (spins > 64 && (spins & 255) == 0 && globaltimer() - start > timeout_ns) {
+    if (spins == 63) start = globaltimer();
+    if (spins > 64 && (spins & 255) == 255 && globaltimer() - start > timeout_ns) {
       atomicCAS(err, 0, EPB_TRANSPORT_CLOSED);
       return false;
     }
@@ -102,24 +103,24 @@ EPB_DEV void warp_copy16(const uint8_t* src, uint8_t* dst, int c0, int c1, int l
 // The round sequence lives on the device (graph-replayable): the send phase
 // reads the group counter; the last CTA to read it stores it into the
 // handle word and advances the counter.  Recv-only launches read the handle.
-EPB_DEV uint32_t ll_round_seq(uint32_t* dseq, int* drd, uint32_t* hseq, bool alloc) {
+EPB_DEV uint32_t ll_round_seq(uint32_t* dseq, uint32_t* hseq, bool alloc) {
   __shared__ uint32_t s_seq;
-  if (threadIdx.x == 0) {
-    if (alloc) {
-      const uint32_t seq = ld_volatile_u32(dseq);
-      s_seq = seq;
-      __threadfence();
-      if (atomicAdd(drd, 1) == (int)gridDim.x - 1) {
-        *drd = 0;
-        *hseq = seq;
-        *dseq = seq + 1;
-      }
-    } else {
-      s_seq = ld_volatile_u32(hseq);
-    }
-  }
+  if (threadIdx.x == 0) s_seq = ld_volatile_u32(alloc ? dseq : hseq);
   __syncthreads();
   return s_seq;
+}
+
+// end of a send phase: the last CTA (all have read the counter by now)
+// records the round in the handle word and advances the group counter
+EPB_DEV void ll_round_commit(uint32_t* dseq, int* drd, uint32_t* hseq, uint32_t seq) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(drd, 1) == (int)gridDim.x - 1) {
+      *drd = 0;
+      *hseq = seq;
+      *dseq = seq + 1;
+    }
+  }
 }
 
 template <int XT, int EPC>
@@ -161,32 +162,37 @@ struct LLDisp {
 };
 
 // copy one received slot row (WT, optional scales) to an output row (OT)
+// (part `part` of `parts` equal chunk ranges; the scales go with part 0)
 template <int WT, bool SC, int OT>
-EPB_DEV void ll_copy_row(const LLGeom& g, const uint8_t* slot, uint8_t* orow, float* osc, int lane) {
+EPB_DEV void ll_copy_row(const LLGeom& g, const uint8_t* slot, uint8_t* orow, float* osc, int lane, int part,
+                         int parts) {
   const int H = g.H;
   if ((H & 15) == 0) {
     constexpr int EPC = Elems<WT>::n;
     const int nch = H / EPC;
+    const int per = (nch + parts - 1) / parts;
+    const int c0 = part * per, c1 = min(nch, c0 + per);
     if constexpr (OT == WT) {
-      warp_copy16(slot, orow, 0, nch, lane);
+      warp_copy16(slot, orow, c0, c1, lane);
       if constexpr (SC) {
         const float* sc = reinterpret_cast<const float*>(slot + g.RBp);
-        for (int i = lane; i < H / 128; i += 32) osc[i] = sc[i];
+        if (part == 0)
+          for (int i = lane; i < H / 128; i += 32) osc[i] = sc[i];
       }
     } else {
       static_assert(OT == EPB_F32, "recv output is f32 or the wire dtype");
       const float* sc = reinterpret_cast<const float*>(slot + g.RBp);
-      for (int base = 0; base < nch; base += 32 * 4) {
+      for (int base = c0; base < c1; base += 32 * 4) {
         int4 v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = base + u * 32 + lane;
-          if (c < nch) v[u] = ld_weak_v4(slot + (int64_t)c * 16);
+          if (c < c1) v[u] = ld_weak_v4(slot + (int64_t)c * 16);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = base + u * 32 + lane;
-          if (c < nch) {
+          if (c < c1) {
             float f[EPC];
             unpack16<WT>(v[u], f);
             if constexpr (SC) {
@@ -200,6 +206,7 @@ EPB_DEV void ll_copy_row(const LLGeom& g, const uint8_t* slot, uint8_t* orow, fl
       }
     }
   } else {
+    if (part != 0) return;
     for (int el = lane; el < H; el += 32) {
       if constexpr (OT == WT) {
         if constexpr (OT == EPB_F32) reinterpret_cast<float*>(orow)[el] = reinterpret_cast<const float*>(slot)[el];
@@ -237,44 +244,77 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) xr[v] = ld_nc_v4(src + 16 * v);
   }
   LL_STAMP(p, 0);
-  const uint32_t seq = ll_round_seq(p.dseq, p.drd, p.hseq, p.phases & kPhaseSend);
+  const uint32_t seq = ll_round_seq(p.dseq, p.hseq, p.phases & kPhaseSend);
   const uint32_t tag = ll_tag_of(seq);
   const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
   LL_STAMP(p, 1);
 
   if (p.phases & kPhaseSend) {
-    int* s_topk = smem;                                                            // [b*K]
-    uint64_t* s_mask = reinterpret_cast<uint64_t*>(s_topk + ((b * K + 1) & ~1));  // [b]
-    int* s_m = reinterpret_cast<int*>(s_mask + b);                                 // [E]
-    int* s_q = s_m + E;                                                            // [N]
+    // shared: routing snapshot, per-expert and per-destination token bitmaps
+    // (bit t' of word t'/32), per-expert / per-destination counts
+    const int W = (b + 31) >> 5;
+    int* s_topk = smem;                                                        // [b*K]
+    uint32_t* s_ebits = reinterpret_cast<uint32_t*>(s_topk + b * K);           // [E][W]
+    uint32_t* s_dbits = s_ebits + E * W;                                       // [N][W]
+    int* s_m = reinterpret_cast<int*>(s_dbits + N * W);                        // [E]
+    int* s_q = s_m + E;                                                        // [N]
     __shared__ int s_bad, s_nd;
-    __shared__ int s_cnt[2 * kMaxTopK];
     __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks];
     __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
-    for (int i = threadIdx.x; i < E + N; i += blockDim.x) s_m[i] = 0;
+    for (int i = threadIdx.x; i < (E + N) * W + E + N; i += blockDim.x) reinterpret_cast<int*>(s_ebits)[i] = 0;
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
-    // routing rows: snapshot, validation (api.py:150-170), per-expert and
-    // per-destination counts, destination masks
+    // routing rows: snapshot, validation (api.py:150-170), counts, bitmaps
     for (int t = threadIdx.x; t < b; t += blockDim.x) {
-      int ids[kMaxTopK];
       bool ok = true;
       uint64_t mask = 0;
-      for (int k = 0; k < K; ++k) {
-        const int64_t e = p.topk[(int64_t)t * K + k];
-        ok &= (e >= 0 && e < E);
-        ids[k] = (int)e;
+      const uint32_t bit = 1u << (t & 31);
+      const int wi = t >> 5;
+      if (K <= 8) {
+        // register path (top-k <= 8): no local-memory row copy
+        int ids[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t e = k < K ? p.topk[(int64_t)t * K + k] : -1 - k;
+          ok &= (k >= K) || (e >= 0 && e < E);
+          ids[k] = (int)e;
+        }
+#pragma unroll
+        for (int k = 1; k < 8; ++k)
+#pragma unroll
+          for (int j = 0; j < k; ++j) ok &= (k >= K) || ids[j] != ids[k];
+        if (!ok) { s_bad = 1; continue; }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k < K) {
+            s_topk[t * K + k] = ids[k];
+            atomicAdd(&s_m[ids[k]], 1);
+            atomicOr(&s_ebits[ids[k] * W + wi], bit);
+            mask |= 1ull << (ids[k] / L);
+          }
+        }
+      } else {
+        int ids[kMaxTopK];
+        for (int k = 0; k < K; ++k) {
+          const int64_t e = p.topk[(int64_t)t * K + k];
+          ok &= (e >= 0 && e < E);
+          ids[k] = (int)e;
+        }
+        for (int k = 0; ok && k < K; ++k)
+          for (int j = 0; j < k; ++j) ok &= ids[j] != ids[k];
+        if (!ok) { s_bad = 1; continue; }
+        for (int k = 0; k < K; ++k) {
+          s_topk[t * K + k] = ids[k];
+          atomicAdd(&s_m[ids[k]], 1);
+          atomicOr(&s_ebits[ids[k] * W + wi], bit);
+          mask |= 1ull << (ids[k] / L);
+        }
       }
-      for (int k = 0; ok && k < K; ++k)
-        for (int j = 0; j < k; ++j) ok &= ids[j] != ids[k];
-      if (!ok) { s_bad = 1; continue; }
-      for (int k = 0; k < K; ++k) {
-        s_topk[t * K + k] = ids[k];
-        atomicAdd(&s_m[ids[k]], 1);
-        mask |= 1ull << (ids[k] / L);
+      for (uint64_t mm = mask; mm; mm &= mm - 1) {
+        const int d = __ffsll(mm) - 1;
+        atomicAdd(&s_q[d], 1);
+        atomicOr(&s_dbits[d * W + wi], bit);
       }
-      s_mask[t] = mask;
-      for (uint64_t mm = mask; mm; mm &= mm - 1) atomicAdd(&s_q[__ffsll(mm) - 1], 1);
     }
     __syncthreads();
     if (s_bad) {
@@ -286,56 +326,46 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     const uint64_t slot_off = parity_off + g.disp_slot;
     const int64_t slot_base = (int64_t)p.rank * B;
     for (int t = blockIdx.x; t < b; t += G) {
-      // prefix counts over earlier tokens: i(t,k) = #{t' < t : e_tk in row t'}
-      // and, for the owner d_k of e_tk, j = #{t' < t : d_k in mask t'}
-      if ((int)threadIdx.x < 2 * K) s_cnt[threadIdx.x] = 0;
-      __syncthreads();
-      for (int kg = 0; kg < K; kg += 8) {
-        int ek[8], dk[8], ce[8], cd[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          ek[u] = kg + u < K ? s_topk[t * K + kg + u] : -1;
-          dk[u] = ek[u] >= 0 ? ek[u] / L : 0;
-          ce[u] = 0;
-          cd[u] = 0;
-        }
-        for (int tp = threadIdx.x; tp < t; tp += blockDim.x) {
-          const uint64_t m = s_mask[tp];
-          for (int j = 0; j < K; ++j) {
-            const int e2 = s_topk[tp * K + j];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) ce[u] += (e2 == ek[u]);
+      if (warp == 0) {
+        // lane k: i = #{t' < t routed to e_tk} (popc of e's bitmap below t)
+        // and, for its owner d_k, j = #{t' < t touching d_k}; lanes keep the
+        // first occurrence of each destination
+        const uint32_t below = (1u << (t & 31)) - 1u;
+        const int wt = t >> 5;
+        int e = -1, d = -1, ci = 0, cj = 0;
+        if (lane < K) {
+          e = s_topk[t * K + lane];
+          d = e / L;
+          for (int w = 0; w < wt; ++w) {
+            ci += __popc(s_ebits[e * W + w]);
+            cj += __popc(s_dbits[d * W + w]);
           }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) cd[u] += (int)((m >> dk[u]) & 1);
+          ci += __popc(s_ebits[e * W + wt] & below);
+          cj += __popc(s_dbits[d * W + wt] & below);
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int a = __reduce_add_sync(0xffffffffu, ce[u]);
-          const int c = __reduce_add_sync(0xffffffffu, cd[u]);
-          if (lane == 0 && kg + u < K) {
-            if (a) atomicAdd(&s_cnt[kg + u], a);
-            if (c) atomicAdd(&s_cnt[K + kg + u], c);
+        bool first = lane < K;
+        for (int j = 0; j < K; ++j) {
+          const int dj = __shfl_sync(0xffffffffu, d, j);
+          first &= !(j < lane && dj == d);
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, first);
+        if (lane < K) {
+          s_hdr[2 + lane] = (uint32_t)e;
+          s_hdr[2 + K + lane] = (uint32_t)ci;
+          if (first) {
+            const int pos = __popc(fm & ((1u << lane) - 1u));
+            s_dst[pos] = d;
+            s_j[pos] = cj;
           }
+        }
+        if (lane == 0) {
+          s_nd = __popc(fm);
+          s_hdr[0] = (uint32_t)t;
+          s_hdr[1] = (uint32_t)K;
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int nd = 0;
-        for (int k = 0; k < K; ++k) {
-          const int e = s_topk[t * K + k];
-          const int d = e / L;
-          bool seen = false;
-          for (int i = 0; i < nd; ++i) seen |= s_dst[i] == d;
-          if (!seen) { s_dst[nd] = d; s_j[nd] = s_cnt[K + k]; ++nd; }
-          s_hdr[2 + k] = (uint32_t)e;
-          s_hdr[2 + K + k] = (uint32_t)s_cnt[k];
-        }
-        s_nd = nd;
-        s_hdr[0] = (uint32_t)t;
-        s_hdr[1] = (uint32_t)K;
-      }
-      __syncthreads();
+      LL_STAMP(p, 9);
       const int nd = s_nd;
       for (int w = threadIdx.x; w < 2 + 2 * K; w += blockDim.x)
         for (int i = 0; i < nd; ++i) {
@@ -420,6 +450,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
                        (int64_t)p.rank * G + blockIdx.x;
       st_flag(flag, (uint64_t)tag, sys);
     }
+    ll_round_commit(p.dseq, p.drd, p.hseq, seq);
     LL_STAMP(p, 4);
   }
 
@@ -458,7 +489,9 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     const int nw = blockDim.x >> 5;
     const int ob = (OT == EPB_F32 ? 4 : dtype_width(OT));
     const int64_t orow_bytes = (int64_t)H * ob;
-    for (int f = blockIdx.x * nw + warp; f < items; f += gridDim.x * nw) {
+    // items = (slot, k, half row); CTA-major order spreads them over every SM
+    for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * items; f2 += gridDim.x * nw) {
+      const int f = f2 >> 1, half = f2 & 1;
       const int sl = f / K, k = f - sl * K;
       int s = 0;
       while (s_pre[s + 1] <= sl) ++s;
@@ -468,9 +501,9 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const int e = (int)hdr[2 + k];
       if (e < lo || e >= lo + nloc) continue;
       const int64_t row = (int64_t)(e - lo) * N * B + (int64_t)s * B + hdr[2 + K + k];
-      if (lane == 0) p.src_info[row] = (int32_t)(hdr[0] * K + k);
+      if (lane == 0 && half == 0) p.src_info[row] = (int32_t)(hdr[0] * K + k);
       ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + row * orow_bytes,
-                              SC ? p.out_scales + row * (H / 128) : nullptr, lane);
+                              SC ? p.out_scales + row * (H / 128) : nullptr, lane, half, 2);
     }
     LL_STAMP(p, 7);
   }
@@ -607,19 +640,21 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     if (s_fail) return;
     LL_STAMP(p, 5);
     const uint8_t* slots = p.win + parity_off + g.comb_slot;
-    // tasks: (token, part of the row), blockDim chunks per task
-    const int parts = vec ? (nch + blockDim.x - 1) / blockDim.x : 1;
-    const int tasks = p.b * parts;
-    for (int task = blockIdx.x; task < tasks; task += gridDim.x) {
-      const int t = task / parts, pt = task - t * parts;
-      __syncthreads();
-      if ((int)threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
-      __syncthreads();
-      uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
-      const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
-      if (vec) {
-        const int c = pt * blockDim.x + threadIdx.x;
-        if (c < nch) {
+    if (vec) {
+      // warp tasks: (token, 64-chunk segment); each lane reduces 2 chunks
+      // with all K slot loads of a chunk in flight
+      constexpr int kSeg = 64;
+      const int segs = (nch + kSeg - 1) / kSeg;
+      const int tasks = p.b * segs;
+      for (int task = warp * gridDim.x + blockIdx.x; task < tasks; task += gridDim.x * nw) {
+        const int t = task / segs, sg = task - t * segs;
+        uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
+        const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
+        const float* wt = p.w + (int64_t)t * K;
+#pragma unroll
+        for (int h = 0; h < kSeg / 32; ++h) {
+          const int c = sg * kSeg + h * 32 + lane;
+          if (c >= nch) break;
           float acc[EPC];
 #pragma unroll
           for (int i = 0; i < EPC; ++i) acc[i] = 0.0f;
@@ -633,7 +668,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
               if (k0 + u < K) {
                 float y[EPC];
                 unpack16<WT>(v[u], y);
-                const float wk = s_w[k0 + u];
+                const float wk = wt[k0 + u];
 #pragma unroll
                 for (int i = 0; i < EPC; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(wk, y[i]));
               }
@@ -641,7 +676,14 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
           }
           store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, acc);
         }
-      } else {
+      }
+    } else {
+      for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
+        __syncthreads();
+        if ((int)threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
+        __syncthreads();
+        uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
+        const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
         for (int el = threadIdx.x; el < H; el += blockDim.x) {
           float acc = 0.0f;
           for (int k = 0; k < K; ++k)
@@ -784,9 +826,8 @@ int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases, const epb_ll_d
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;
   const int E = g->ll.E, N = g->ll.N, K = g->ll.K;
-  const size_t smem = (phases & kPhaseSend)
-      ? sizeof(int) * ((size_t)((b * K + 1) & ~1) + (size_t)2 * b + E + N)
-      : 0;
+  const size_t W = (size_t)(b + 31) / 32;
+  const size_t smem = (phases & kPhaseSend) ? sizeof(int) * ((size_t)b * K + (E + N) * W + E + N) : 0;
   if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "LL batch too large for the fused dispatch kernel");
   cudaStream_t s = as_stream(stream);
   cudaError_t e;

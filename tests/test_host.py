@@ -61,7 +61,7 @@ def test_window_logical_bytes_match_reference(layout):
         _lib.call("epb_window_geometry", ctypes.byref(c), ctypes.byref(info))
         assert info.logical_bytes == (w_opt if layout == "optimized" else w_leg)
         assert info.physical_bytes >= info.logical_bytes
-        assert info.physical_bytes <= info.logical_bytes * 1.05 + 8192
+        assert info.physical_bytes <= info.logical_bytes * 1.05 + 64 * 1024  # + per-CTA flag words
         geom = SlotGeometry.for_config(int(h), names[dt], int(k), bool(sc))
         rep = footprint(MoeShape(int(e), int(n), int(b), int(k), int(h)), geom, layout)
         # ll_regions window == footprint incl. coordination when L*N == E

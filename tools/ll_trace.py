@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2603_13606_b200 import _lib  # noqa: E402
 
-DISP = ["start", "seq", "routed", "stored", "published", "recv", "waited", "copied"]
+DISP = ["start", "seq", "routed", "stored", "published", "recv", "waited", "copied", "prefixed", "hdr"]
 COMB = ["start", "prefix", "sent", "published", "recv", "waited", "reduced"]
 
 
