@@ -1,0 +1,183 @@
+"""Multi-GPU parity worker: one process per GPU (torchrun), ProcessFabric
+over NCCL for the bootstrap, CUDA-IPC peer windows for all token traffic.
+Every rank runs LL and HT rounds through the public API and checks its own
+outputs bit-for-bit against the CPU oracle (which computes every rank's
+expected values from the same seeded workload).
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port 29511 tests/mp_worker.py
+"""
+
+import os
+import sys
+import traceback
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_13606_b200 as ep  # noqa: E402
+from oracle import codecs as oc  # noqa: E402
+from oracle import ht as oht  # noqa: E402
+from oracle import ll as oll  # noqa: E402
+from oracle import workload as owl  # noqa: E402
+
+T = ep.TensorTag
+
+
+def bf16r(x):
+    return oc.bf16_to_f32(oc.f32_to_bf16(x))
+
+
+def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, staged, mode, rounds=1):
+    cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, bmax, dtype, scales, combine_dtype=combine_dtype)
+    fab = ep.ProcessFabric(ep.NodeTopology(world, world))
+    g = ep.create_group(fab, rank, cfg)
+    ell = cfg.experts_per_rank
+    for rnd in range(rounds):
+        wl = owl.make_workload(e, world, bmax, k, h, seed + rnd)
+        if mode == "bf16":
+            wl.tokens = [bf16r(t) for t in wl.tokens]
+        d = oll.dispatch(wl.tokens, wl.routing, e, world, bmax, h, dtype.value, scales)
+        ys = [bf16r(oll.apply_experts(d[r]["recv"], d[r]["counts"], r, e, world, bmax, owl.expert_scale))
+              for r in range(world)]
+        want = oll.combine(ys, wl.routing, wl.weights, e, world, bmax, h, cfg.combine_wire.value)[rank]
+        hd = g.create_handle(wl.routing[rank])
+        if mode == "bf16":
+            inputs = [ep.tensor_from_f32(wl.tokens[rank], ep.Dtype.BF16, T.TOKENS)]
+        elif scales:
+            c, s = oc.quantize_block(wl.tokens[rank])
+            tok = ep.tensor_create(c.shape, ep.Dtype.FP8, T.TOKENS)
+            tok.write_raw(c)
+            sc = ep.tensor_create(s.shape, ep.Dtype.F32, T.SCALES)
+            sc.write_raw(s)
+            inputs = [tok, sc]
+        else:
+            inputs = [ep.tensor_from_f32(wl.tokens[rank], dtype, T.TOKENS)]
+        out = ep.tensor_create((ell, world * bmax, h), ep.Dtype.F32, T.TOKENS)
+        cnt = ep.tensor_create((ell, world), ep.Dtype.F32, T.RECV_EXPERT_COUNTER_HOST)
+        hd.dispatch(inputs, [out, cnt], send_only=staged)
+        if staged:
+            hd.complete()
+        counts = cnt.read_f32()
+        np.testing.assert_array_equal(counts, d[rank]["counts"])
+        recv = out.read_f32()
+        plan = d[rank]["plan"]
+        if len(plan):
+            idx = (plan[:, 0], plan[:, 1] * bmax + plan[:, 2])
+            np.testing.assert_array_equal(recv[idx], d[rank]["recv"][idx])
+        y = ys[rank]
+        comb_in = [ep.tensor_from_f32(y, ep.Dtype.BF16, T.TOKENS),
+                   ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)]
+        comb_out = ep.tensor_create((bmax, h), ep.Dtype.F32, T.TOKENS)
+        hd.combine(comb_in, [comb_out], send_only=staged)
+        if staged:
+            hd.complete()
+        np.testing.assert_array_equal(comb_out.read_f32(), want)
+        hd.destroy()
+    g.destroy()
+
+
+def ll_pipelined(world, rank):
+    """Two handles in flight (parities 0 and 1), ll.py:171-218."""
+    e, k, h, b = 32, 4, 512, 16
+    cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, b, ep.Dtype.BF16)
+    fab = ep.ProcessFabric(ep.NodeTopology(world, world))
+    g = ep.create_group(fab, rank, cfg)
+    ell = cfg.experts_per_rank
+    wls = [owl.make_workload(e, world, b, k, h, s) for s in (20, 21)]
+    hds, outs = [], []
+    for wl in wls:
+        hd = g.create_handle(wl.routing[rank])
+        out = ep.tensor_create((ell, world * b, h), ep.Dtype.F32, T.TOKENS)
+        cnt = ep.tensor_create((ell, world), ep.Dtype.F32, T.RECV_EXPERT_COUNTER_HOST)
+        hd.dispatch([ep.tensor_from_f32(wl.tokens[rank], ep.Dtype.BF16, T.TOKENS)], [out, cnt], send_only=True)
+        hds.append(hd)
+        outs.append((out, cnt))
+    for hd in hds:
+        hd.complete()
+    combs = []
+    for wl, hd, (out, cnt) in zip(wls, hds, outs):
+        y = oll.apply_experts(out.read_f32(), cnt.read_f32().astype(np.int64), rank, e, world, b, owl.expert_identity)
+        co = ep.tensor_create((b, h), ep.Dtype.F32, T.TOKENS)
+        hd.combine([ep.tensor_from_f32(y, ep.Dtype.F32, T.TOKENS),
+                    ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)], [co], send_only=True)
+        combs.append(co)
+    for hd in hds:
+        hd.complete()
+    for wl, co in zip(wls, combs):
+        d = oll.dispatch(wl.tokens, wl.routing, e, world, b, h, "bf16", False)
+        ys = [oll.apply_experts(d[r]["recv"], d[r]["counts"], r, e, world, b, owl.expert_identity)
+              for r in range(world)]
+        want = oll.combine(ys, wl.routing, wl.weights, e, world, b, h, "bf16")[rank]
+        np.testing.assert_array_equal(co.read_f32(), want)
+    for hd in hds:
+        hd.destroy()
+    g.destroy()
+
+
+def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert):
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, rpn, e, k, h, b, ep.Dtype.BF16)
+    fab = ep.ProcessFabric(ep.NodeTopology(world, rpn))
+    g = ep.create_group(fab, rank, cfg)
+    wl = owl.make_workload(e, world, b, k, h, seed)
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, e, world, h, "bf16")
+    ys = [oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_affine) for r in range(world)]
+    if bf16_expert:
+        ys = [bf16r(y) for y in ys]
+    want = oht.combine(ys, wl.routing, wl.weights, e, world, rpn)[rank]
+    hd = g.create_handle(wl.routing[rank])
+    tot = hd.get_num_recv_tokens()
+    assert tot == dd[rank]["recv_total"], (tot, dd[rank]["recv_total"])
+    out = ep.tensor_create((tot, h), ep.Dtype.F32, T.TOKENS)
+    cnt = ep.tensor_create((cfg.experts_per_rank, world), ep.Dtype.F32, T.TOKENS_PER_EXPERTS)
+    w = ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)
+    hd.dispatch([ep.tensor_from_f32(wl.tokens[rank], ep.Dtype.BF16, T.TOKENS), w], [out, cnt])
+    np.testing.assert_array_equal(out.read_f32(), dd[rank]["rows"])
+    np.testing.assert_array_equal(hd.dispatch_result.origin.cpu().numpy(), dd[rank]["origin"])
+    ydt = ep.Dtype.BF16 if bf16_expert else ep.Dtype.F32
+    co = ep.tensor_create((b, h), ep.Dtype.F32, T.TOKENS)
+    hd.combine([ep.tensor_from_f32(ys[rank], ydt, T.TOKENS), w], [co])
+    np.testing.assert_array_equal(co.read_f32(), want)
+    hd.destroy()
+    g.destroy()
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    os.environ.setdefault("EPB_TIMEOUT_MS", "20000")
+    cases = [
+        ("ll fp8+scales dsv3 b=64", lambda: ll_case(world, rank, 256, 8, 7168, 64, ep.Dtype.FP8, True, None, 1, False, "ref")),
+        ("ll c2 hot path bf16->fp8 / bf16 comb", lambda: ll_case(world, rank, 256, 8, 7168, 128, ep.Dtype.FP8, True,
+                                                                  ep.Dtype.BF16, 2, False, "bf16")),
+        ("ll staged bf16 uneven", lambda: ll_case(world, rank, 3 * world + 1, 3, 256, 12, ep.Dtype.BF16, False, None,
+                                                  3, True, "ref", rounds=3)),
+        ("ll pipelined parities", lambda: ll_pipelined(world, rank)),
+        ("ht bf16 single node", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 4, False)),
+        ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
+    ]
+    failures = []
+    for name, fn in cases:
+        try:
+            fn()
+            ok = 1
+        except Exception:  # noqa: BLE001 - reported below
+            ok = 0
+            failures.append(name + "\n" + traceback.format_exc())
+        t = torch.tensor([ok], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(f"[{'PASS' if t.item() else 'FAIL'}] N={world} {name}", flush=True)
+    for f in failures:
+        print(f"rank {rank} FAILURE: {f}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(1 if failures else 0)
+
+
+if __name__ == "__main__":
+    main()
