@@ -252,12 +252,25 @@ def capture(step_obj, group, phases: bool, warmup_eager=3):
     return graph, marks
 
 
-def replay_timed(graph, marks, steps, flush):
-    """Replay `steps` times, L2 flushed before each (outside the events);
-    returns (total ms, {phase: ms})."""
+def replay_timed(graph, marks, steps, flush, sync_each=False):
+    """Replay `steps` times back to back, the L2 flushed before each step
+    outside the timed events.  Without `sync_each` the host never waits
+    between steps (per-step events are recorded around each replay on the
+    stream), so ranks stay aligned by the exchange itself instead of by host
+    jitter.  With `sync_each` the in-graph phase events are read after every
+    replay.  Returns (total ms, {phase: ms})."""
     import torch
     names = [m[0] for m in marks]
     phase = {n: 0.0 for n in names[:-1]}
+    if not sync_each:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in evs:
+            flush.zero_()
+            a.record()
+            graph.replay()
+            b.record()
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs), phase
     total = 0.0
     for _ in range(steps):
         flush.zero_()
@@ -286,7 +299,8 @@ def run_ll(args, world, rank):
         barrier(world)
     # per-kernel breakdown from the instrumented graph (events between launches)
     nb = max(10, min(args.steps, 100))
-    _, phase = replay_timed(graph_b, marks_b, nb, flush)
+    barrier(world)
+    _, phase = replay_timed(graph_b, marks_b, nb, flush, sync_each=True)
     st.g.check()
     total_max = allreduce_max(total, world)
     per_phase = {n: v / nb * 1000.0 for n, v in phase.items()}  # us
