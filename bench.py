@@ -215,13 +215,15 @@ class LLStep:
             arrive = sent
         else:
             arrive = sent  # symmetric workload: what a rank receives ~ what it sends
-        # fused kernels: dispatch = read x + write slots + read arrived slots +
-        # write expert-major rows; combine = read expert rows + write slots +
-        # read K slots per token + write the bf16 output
+        # compulsory HBM bytes per launch: dispatch = read the
+        # bf16 tokens + routing, write the FP8 expert-major rows + scales;
+        # combine = read the bf16 expert rows + weights, write the bf16 output.
+        # Slot traffic in the window is an intermediate (L2-resident at N=1).
+        del sent, arrive
         return {
             "epb_routing_layout": self.b * K * 8 + self.b * (K + self.world) * 4 + (E + self.world) * 4,
-            "epb_ll_dispatch": self.b * H * 2 + sent * row8 + arrive * row8 + recv_rows * row8,
-            "epb_ll_combine": recv_rows * H * 2 * 2 + self.b * K * H * 2 + self.b * H * 2,
+            "epb_ll_dispatch": self.b * H * 2 + self.b * K * 8 + recv_rows * row8,
+            "epb_ll_combine": recv_rows * H * 2 + self.b * K * 4 + self.b * H * 2,
         }, {"dispatch_remote": int(sum(len(set(r) - {self.rank}) for r in owner)) * row8,
             "combine_remote": int((owner != self.rank).sum()) * H * 2}
 
