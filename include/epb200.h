@@ -18,8 +18,8 @@
  *   LLRank.combine (ll.py:404-462)               | epb_ll_combine phase SEND     (K4a)
  *   LLRank.complete_combine (ll.py:464-507)      | epb_ll_combine phase RECV     (K4b)
  *   HTRank.exchange_metadata (ht.py:291-331)     | epb_ht_meta_send / _recv      (K5a)
- *   HTRank.dispatch + _assemble (ht.py:381-583)  | epb_ht_dispatch_send / _recv  (K5b)
- *   HTRank.combine (ht.py:587-735)               | epb_ht_combine_send / _recv   (K6)
+ *   HTRank.dispatch + _assemble (ht.py:381-583)  | epb_ht_dispatch               (K5b)
+ *   HTRank.combine (ht.py:587-735)               | epb_ht_combine                (K6)
  *   quantize_block / dequantize_block            | epb_fp8_quantize / _dequantize (K7)
  *     (core.py:127-162)                          |
  *   fabric.shutdown / wait timeout               | epb_group_poll_error (device error word)
@@ -189,23 +189,47 @@ int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay,
  * offset of group (e, src) on owner(e); recv_total: [1] i32 */
 int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out,
                      int32_t* offsets, int32_t* recv_total, void* stream);
-/* K5b: HT dispatch.  x [b, H] x_dtype, weights [b, K] f32 */
-int epb_ht_dispatch_send(epb_group* g, uint32_t round, const void* x,
-                         int32_t x_dtype, const float* weights,
-                         const int64_t* topk_idx, const epb_layout* lay,
-                         const int32_t* offsets, void* stream);
-/* out [recv_total, H] out_dtype; origin [recv_total, 4] = (e, src, t, k);
- * origin_w [recv_total] f32 */
-int epb_ht_dispatch_recv(epb_group* g, uint32_t round, void* out,
-                         int32_t out_dtype, int32_t* origin, float* origin_w,
-                         void* stream);
-/* K6: HT combine.  expert_rows [recv_total, H] f32|bf16 */
-int epb_ht_combine_send(epb_group* g, uint32_t round, const void* expert_rows,
-                        int32_t in_dtype, const int32_t* origin,
-                        int32_t recv_total, void* stream);
-int epb_ht_combine_recv(epb_group* g, uint32_t round, const int64_t* topk_idx,
-                        const float* weights, int32_t b, void* out,
-                        int32_t out_dtype, void* stream);
+/* K5b: HT dispatch (ht.py:381-583).  phases: SEND writes one record per
+ * (token, remote destination) and places rows for this rank's own experts
+ * directly in `out`; RECV waits for every source and scatters record rows to
+ * their sorted (expert, src, token) positions.  BOTH = the two launches back
+ * to back (peers on other GPUs). */
+typedef struct epb_ht_dispatch_args {
+  const void* x;             /* [b, H] f32|bf16|f16 */
+  int32_t x_dtype;
+  const float* weights;      /* [b, K] f32 (travel with the records) */
+  const int64_t* topk_idx;   /* [b, K] */
+  int32_t num_tokens;
+  const int32_t* rank_count; /* K1 layout: q [N]        */
+  const int32_t* tok_rank;   /*            [b*K]        */
+  const int32_t* tok_slot;   /*            [b*N]        */
+  const int32_t* offsets;    /* epb_ht_meta_recv [E, N] */
+  void* out;                 /* [recv_total, H] f32 or the wire dtype */
+  int32_t out_dtype;
+  int32_t* origin;           /* [recv_total, 4] = (e, src, t, k) */
+  float* origin_w;           /* [recv_total] */
+} epb_ht_dispatch_args;
+int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases,
+                    const epb_ht_dispatch_args* args, void* stream);
+
+/* K6: HT combine (ht.py:587-735).  SEND moves expert rows of remote tokens
+ * to their home's combine slots; RECV reduces in the reference's
+ * (node, k) order, reading rows of its own tokens in place. */
+typedef struct epb_ht_combine_args {
+  const void* expert_rows;   /* [recv_total, H] f32|bf16, dispatch order */
+  int32_t in_dtype;
+  const int32_t* origin;     /* from the dispatch */
+  int32_t recv_total;
+  const int64_t* topk_idx;   /* [b, K] */
+  const float* weights;      /* [b, K] f32 */
+  int32_t num_tokens;
+  const int32_t* tok_rank;   /* K1 layout [b*K] */
+  const int32_t* offsets;    /* [E, N] */
+  void* out;                 /* [b, H] f32|bf16 */
+  int32_t out_dtype;
+} epb_ht_combine_args;
+int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases,
+                   const epb_ht_combine_args* args, void* stream);
 /* device-side check that combine weights equal the dispatched ones
  * (ht.py:605-609); sets EPB_INVALID_ARGUMENT in the error word */
 int epb_weights_equal(epb_group* g, const float* a, const float* b, int64_t n,

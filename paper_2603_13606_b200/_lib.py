@@ -53,6 +53,21 @@ class LLCombineArgs(ctypes.Structure):
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32)]
 
 
+class HTDispatchArgs(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("x_dtype", ctypes.c_int32), ("weights", ctypes.c_void_p),
+                ("topk_idx", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
+                ("rank_count", ctypes.c_void_p), ("tok_rank", ctypes.c_void_p), ("tok_slot", ctypes.c_void_p),
+                ("offsets", ctypes.c_void_p), ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
+                ("origin", ctypes.c_void_p), ("origin_w", ctypes.c_void_p)]
+
+
+class HTCombineArgs(ctypes.Structure):
+    _fields_ = [("expert_rows", ctypes.c_void_p), ("in_dtype", ctypes.c_int32), ("origin", ctypes.c_void_p),
+                ("recv_total", ctypes.c_int32), ("topk_idx", ctypes.c_void_p), ("weights", ctypes.c_void_p),
+                ("num_tokens", ctypes.c_int32), ("tok_rank", ctypes.c_void_p), ("offsets", ctypes.c_void_p),
+                ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32)]
+
+
 PHASE_SEND, PHASE_RECV, PHASE_BOTH = 1, 2, 3
 
 
@@ -85,10 +100,8 @@ SIGNATURES = {
     "epb_ll_combine": [_P, _P, _I, ctypes.c_void_p, _P],
     "epb_ht_meta_send": [_P, _U, ctypes.POINTER(Layout), _P],
     "epb_ht_meta_recv": [_P, _U, _P, _P, _P, _P],
-    "epb_ht_dispatch_send": [_P, _U, _P, _I, _P, _P, ctypes.POINTER(Layout), _P, _P],
-    "epb_ht_dispatch_recv": [_P, _U, _P, _I, _P, _P, _P],
-    "epb_ht_combine_send": [_P, _U, _P, _I, _P, _I, _P],
-    "epb_ht_combine_recv": [_P, _U, _P, _P, _I, _P, _I, _P],
+    "epb_ht_dispatch": [_P, _U, _I, ctypes.c_void_p, _P],
+    "epb_ht_combine": [_P, _U, _I, ctypes.c_void_p, _P],
     "epb_weights_equal": [_P, _P, _P, _L, _P],
     "epb_fp8_quantize": [_P, _I, _L, _I, _P, _P, _P],
     "epb_fp8_dequantize": [_P, _P, _L, _I, _P, _P],

@@ -574,15 +574,20 @@ class EpHandle:
         w = self._dev_in(weights)
         self._weights = w.clone()
         rnd = self._round
-        g._launch("epb_ht_dispatch_send", g._g, rnd, _ptr(x), tokens.dtype.code, _ptr(w), _ptr(self.routing),
-                  ctypes.byref(self._lay), _ptr(meta["offsets"]), self._sp())
-        g.fabric.phase(g.rank)
         total = meta["recv_total"]
         out_t, back_t = self._dev_out(out_tokens, full=True)
         origin = torch.empty((max(total, 1), 4), dtype=torch.int32, device=g.device)
         origin_w = torch.empty(max(total, 1), dtype=torch.float32, device=g.device)
-        g._launch("epb_ht_dispatch_recv", g._g, rnd, _ptr(out_t), out_tokens.dtype.code, _ptr(origin),
-                  _ptr(origin_w), self._sp())
+        a = _lib.HTDispatchArgs(x.data_ptr(), tokens.dtype.code, w.data_ptr(), self.routing.data_ptr(), self._b,
+                                self._q.data_ptr(), self._tok_rank.data_ptr(), self._tok_slot.data_ptr(),
+                                meta["offsets"].data_ptr(), out_t.data_ptr(), out_tokens.dtype.code,
+                                origin.data_ptr(), origin_w.data_ptr())
+        if g._fused_ok():
+            g._launch("epb_ht_dispatch", g._g, rnd, _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
+        else:
+            g._launch("epb_ht_dispatch", g._g, rnd, _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+            g.fabric.phase(g.rank)
+            g._launch("epb_ht_dispatch", g._g, rnd, _lib.PHASE_RECV, ctypes.byref(a), self._sp())
         if g.strict:
             g.check()
         if back_t:
@@ -668,12 +673,16 @@ class EpHandle:
         g._launch("epb_weights_equal", g._g, _ptr(w), _ptr(self._weights), w.numel(), self._sp())
         if g.strict:
             g.check()
-        g._launch("epb_ht_combine_send", g._g, self._round, _ptr(y), y_dtype.code, _ptr(res.origin),
-                  res.recv_total, self._sp())
-        g.fabric.phase(g.rank)
         o, back = self._dev_out(out, full=True)
-        g._launch("epb_ht_combine_recv", g._g, self._round, _ptr(self.routing), _ptr(w), self._b, _ptr(o),
-                  out.dtype.code, self._sp())
+        a = _lib.HTCombineArgs(y.data_ptr(), y_dtype.code, res.origin.data_ptr(), res.recv_total,
+                               self.routing.data_ptr(), w.data_ptr(), self._b, self._tok_rank.data_ptr(),
+                               self._meta["offsets"].data_ptr(), o.data_ptr(), out.dtype.code)
+        if g._fused_ok():
+            g._launch("epb_ht_combine", g._g, self._round, _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
+        else:
+            g._launch("epb_ht_combine", g._g, self._round, _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+            g.fabric.phase(g.rank)
+            g._launch("epb_ht_combine", g._g, self._round, _lib.PHASE_RECV, ctypes.byref(a), self._sp())
         if g.strict:
             g.check()
         if back:

@@ -8,14 +8,17 @@
 //  * dispatch (ht.py:381-468, 553-583): one record per (token, destination
 //    rank) = header + K f32 weights + row; the receiver places a copy of the
 //    row for every local expert it names, sorted by (local expert, src, t).
-//    Here the sender also writes, per k, the final output row on the owner
-//    (offset(e, src) + rank of t within (e, src)), so the receiver's
-//    placement is a parallel scatter that never depends on arrival order.
+//    The sender also writes, per k, the final output row on the owner
+//    (offset(e, src) + rank of t within (e, src)), so placement is a parallel
+//    scatter that never depends on arrival order.  Rows a rank routes to its
+//    OWN experts skip the window: the sender writes them straight to their
+//    sorted output position.
 //  * combine (ht.py:587-735): p = f32(w * y) from the f32 expert row; per
 //    token, per node holding its experts (ascending), a partial = first p
 //    then f32 adds in ascending k; out = f32(0 + partial_0) + partial_1 ...
 //    Expert rows travel in their own dtype (f32, or bf16 which widens
 //    exactly) and the home rank forms p, so the product is bit-identical.
+//    Rows of the home's own experts are read in place, not copied.
 //  * single-node transport only: the reference's rail FIFOs / forwarders
 //    (ht.py:479-551) are out of scope on one NVSwitch domain, but the
 //    hierarchical SUM ORDER is reproduced for any ranks_per_node.
@@ -24,10 +27,21 @@
 
 namespace epb {
 
+constexpr int kHTThreads = 512;
+constexpr int kHU = 8;  // 16-B loads in flight per lane in copies
+
 EPB_DEV uint8_t* hpeer(const uint64_t* peers, int r) { return reinterpret_cast<uint8_t*>(peers[r]); }
 
 EPB_DEV void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+EPB_DEV int4 ld_plain_v4(const void* p) {
+  int4 v;
+  asm volatile("ld.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+EPB_DEV void st_plain_v4(void* p, int4 v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
 }
 
 // ---------------------------------------------------------------------------
@@ -52,7 +66,7 @@ __global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
     reinterpret_cast<int32_t*>(hpeer(p.peers, d) + row_off)[c] = v;
   }
   __syncthreads();
-  if (threadIdx.x < g.N) {
+  if ((int)threadIdx.x < g.N) {
     fence_sys();
     uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, threadIdx.x) + g.meta_flag) +
                      p.parity * g.N + p.rank;
@@ -126,6 +140,9 @@ struct HTSend {
   const int32_t* tok_slot;
   const int32_t* offsets;  // [E, N]
   const uint64_t* peers;
+  void* out;               // own sorted output (self rows land here directly)
+  int32_t* origin;
+  float* origin_w;
   int* done;
   HTGeom g;
   int b, rank;
@@ -137,38 +154,60 @@ EPB_DEV void ht_publish_records(const HTSend& p, int d) {
   st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | (uint32_t)p.q[d]);
 }
 
-template <int XT, int WT>
-__global__ void __launch_bounds__(512) ht_dispatch_send_kernel(HTSend p) {
+template <int XT, int WT, int OT>
+__global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) {
   __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks], s_nd;
+  __shared__ int s_pos[kMaxTopK], s_ns;      // self rows: output positions
   __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
   __shared__ float s_w[kMaxTopK];
   __shared__ int s_cnt[kMaxRanks];
   const HTGeom& g = p.g;
   const int K = g.K, N = g.N, H = g.H, L = g.L;
-  if (threadIdx.x < N) s_cnt[threadIdx.x] = 0;
+  const int me = p.rank;
+  constexpr int EPC = Elems<WT>::n;
+  constexpr int XW = XT == EPB_F32 ? 4 : 2;
+  constexpr int OW = OT == EPB_F32 ? 4 : 2;
+  if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
   for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
     __syncthreads();
     if (threadIdx.x == 0) {
       int nd = 0;
       for (int d = 0; d < N; ++d) {
         const int j = p.tok_slot[(int64_t)t * N + d];
-        if (j >= 0) { s_dst[nd] = d; s_j[nd] = j; ++nd; s_cnt[d] += 1; }
+        if (j >= 0 && d != me) { s_dst[nd] = d; s_j[nd] = j; ++nd; s_cnt[d] += 1; }
       }
       s_nd = nd;
       s_hdr[0] = (uint32_t)t;
       s_hdr[1] = (uint32_t)K;
     }
-    if (threadIdx.x < K) {
-      const int e = (int)p.topk[(int64_t)t * K + threadIdx.x];
-      s_hdr[2 + threadIdx.x] = (uint32_t)e;
-      s_hdr[2 + K + threadIdx.x] =
-          (uint32_t)(p.offsets[e * N + p.rank] + p.tok_rank[(int64_t)t * K + threadIdx.x]);
-      s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
+    if (threadIdx.x == 32) {
+      int ns = 0;
+      for (int k = 0; k < K; ++k) {
+        const int e = (int)p.topk[(int64_t)t * K + k];
+        if (e / L == me) s_pos[ns++] = p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k];
+      }
+      s_ns = ns;
+    }
+    if ((int)threadIdx.x < K) {
+      const int k = threadIdx.x;
+      const int e = (int)p.topk[(int64_t)t * K + k];
+      const int pos = p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k];
+      const float wk = p.w[(int64_t)t * K + k];
+      s_hdr[2 + k] = (uint32_t)e;
+      s_w[k] = wk;
+      if (e / L == me) {
+        p.origin[(int64_t)pos * 4 + 0] = e;
+        p.origin[(int64_t)pos * 4 + 1] = me;
+        p.origin[(int64_t)pos * 4 + 2] = t;
+        p.origin[(int64_t)pos * 4 + 3] = k;
+        p.origin_w[pos] = wk;
+      }
+      // position on the owner; only meaningful to the owner's receiver
+      s_hdr[2 + K + k] = (uint32_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]);
     }
     __syncthreads();
-    const int nd = s_nd;
-    const int64_t rec0 = (int64_t)p.rank * g.B;
-    // weights + header + positions
+    const int nd = s_nd, ns = s_ns;
+    const int64_t rec0 = (int64_t)me * g.B;
     for (int wd = threadIdx.x; wd < K + 2 + 2 * K; wd += blockDim.x) {
       for (int i = 0; i < nd; ++i) {
         uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
@@ -176,9 +215,8 @@ __global__ void __launch_bounds__(512) ht_dispatch_send_kernel(HTSend p) {
         else reinterpret_cast<uint32_t*>(rec + g.RBp + g.WBp)[wd - K] = s_hdr[wd - K];
       }
     }
-    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * dtype_width(XT);
+    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
     if ((H & 15) == 0) {
-      constexpr int EPC = Elems<WT>::n;
       for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
         float f[EPC];
         load_elems_vec<XT, EPC>(xrow, (int64_t)c * EPC, f);
@@ -186,6 +224,13 @@ __global__ void __launch_bounds__(512) ht_dispatch_send_kernel(HTSend p) {
         for (int i = 0; i < nd; ++i) {
           uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
           st_na_v4(rec + (int64_t)c * 16, v);
+        }
+        if (ns) {
+          float fw[EPC];
+          unpack16<WT>(v, fw);  // the wire image, exactly what a record would carry
+          for (int i = 0; i < ns; ++i)
+            store_f32_chunk<OT, EPC>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i] * H * OW,
+                                     (int64_t)c * EPC, fw);
         }
       }
     } else {
@@ -195,12 +240,16 @@ __global__ void __launch_bounds__(512) ht_dispatch_send_kernel(HTSend p) {
           uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
           store_elem(rec, WT, el, f);
         }
+        if (ns) {
+          const float fw = WT == EPB_F32 ? f : (WT == EPB_BF16 ? bf16_widen(bf16_bits_rne(f)) : f16_widen(f16_bits_rne(f)));
+          for (int i = 0; i < ns; ++i)
+            store_elem(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i] * H * OW, OT, el, fw);
+        }
       }
     }
-    (void)L;
   }
   __syncthreads();
-  if (threadIdx.x < N) {
+  if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
     const int d = threadIdx.x;
     const int c = s_cnt[d];
     if (c > 0) {
@@ -230,18 +279,19 @@ struct HTRecv {
 };
 
 template <int WT, int OT>
-__global__ void __launch_bounds__(256) ht_dispatch_recv_kernel(HTRecv p) {
+__global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) {
   __shared__ int s_pre[kMaxRanks + 1], s_q[kMaxRanks];
   __shared__ int s_fail;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H, L = g.L;
+  const int me = p.rank;
   if (threadIdx.x == 0) s_fail = 0;
   __syncthreads();
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
-    if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
-    s_q[s] = (int)(v & 0xFFFFFFFFu);
+    if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    s_q[s] = s == me ? 0 : (int)(v & 0xFFFFFFFFu);  // own rows were placed by the sender
   }
   __syncthreads();
   if (s_fail) return;
@@ -251,44 +301,54 @@ __global__ void __launch_bounds__(256) ht_dispatch_recv_kernel(HTRecv p) {
     s_pre[N] = run;
   }
   __syncthreads();
-  const int total = s_pre[N];
-  const int lo = p.rank * L, hi = min(lo + L, g.E);
+  const int items = s_pre[N] * K;  // (record, k); non-local k exit at once
+  const int lo = me * L, hi = min(lo + L, g.E);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int ob = dtype_width(OT);
-  for (int f = blockIdx.x * nw + warp; f < total; f += gridDim.x * nw) {
+  constexpr int OW = OT == EPB_F32 ? 4 : 2;
+  constexpr int EPC = Elems<WT>::n;
+  for (int f = warp * gridDim.x + blockIdx.x; f < items; f += gridDim.x * nw) {
+    const int rj = f / K, k = f - rj * K;
     int s = 0;
-    while (s_pre[s + 1] <= f) ++s;
-    const int j = f - s_pre[s];
+    while (s_pre[s + 1] <= rj) ++s;
+    const int j = rj - s_pre[s];
     const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
-    const float* wts = reinterpret_cast<const float*>(rec + g.RBp);
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
-    const uint32_t t = hdr[0];
-    for (int k = 0; k < K; ++k) {
-      const int e = (int)hdr[2 + k];
-      if (e < lo || e >= hi) continue;
-      const int64_t pos = hdr[2 + K + k];
-      if (lane == 0) {
-        p.origin[pos * 4 + 0] = e;
-        p.origin[pos * 4 + 1] = s;
-        p.origin[pos * 4 + 2] = (int32_t)t;
-        p.origin[pos * 4 + 3] = k;
-        p.origin_w[pos] = wts[k];
-      }
-      uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + pos * H * ob;
-      if ((H & 15) == 0) {
-        constexpr int EPC = Elems<WT>::n;
-        if constexpr (OT == WT) {
-          for (int c = lane; c < H / EPC; c += 32) st_v4(orow + (int64_t)c * 16, ld_v4(rec + (int64_t)c * 16));
-        } else {
-          for (int c = lane; c < H / EPC; c += 32) {
-            float fv[EPC];
-            unpack16<WT>(ld_v4(rec + (int64_t)c * 16), fv);
-            store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, fv);
+    const int e = (int)hdr[2 + k];
+    if (e < lo || e >= hi) continue;
+    const int64_t pos = hdr[2 + K + k];
+    if (lane == 0) {
+      p.origin[pos * 4 + 0] = e;
+      p.origin[pos * 4 + 1] = s;
+      p.origin[pos * 4 + 2] = (int32_t)hdr[0];
+      p.origin[pos * 4 + 3] = k;
+      p.origin_w[pos] = reinterpret_cast<const float*>(rec + g.RBp)[k];
+    }
+    uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + pos * H * OW;
+    if ((H & 15) == 0) {
+      const int nch = H / EPC;
+      for (int base = 0; base < nch; base += 32 * kHU) {
+        int4 v[kHU];
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+          const int c = base + u * 32 + lane;
+          if (c < nch) v[u] = ld_plain_v4(rec + (int64_t)c * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+          const int c = base + u * 32 + lane;
+          if (c < nch) {
+            if constexpr (OT == WT) {
+              st_plain_v4(orow + (int64_t)c * 16, v[u]);
+            } else {
+              float fv[EPC];
+              unpack16<WT>(v[u], fv);
+              store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, fv);
+            }
           }
         }
-      } else {
-        for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
       }
+    } else {
+      for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
     }
   }
 }
@@ -321,35 +381,50 @@ EPB_DEV void ht_publish_comb(const HTCombSend& p, int s, int count) {
 }
 
 template <int IT>
-__global__ void __launch_bounds__(256) ht_combine_send_kernel(HTCombSend p) {
+__global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend p) {
   __shared__ int s_cnt[kMaxRanks];
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H;
-  if (threadIdx.x < N) s_cnt[threadIdx.x] = 0;
+  const int me = p.rank;
+  if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
   __syncthreads();
-  const int per = (p.rows + gridDim.x - 1) / gridDim.x;
-  const int r0 = blockIdx.x * per, r1 = min(p.rows, r0 + per);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   constexpr int ib = IT == EPB_F32 ? 4 : 2;
-  for (int r = r0 + warp; r < r1; r += nw) {
+  const int bytes = H * ib;
+  const int nch = (bytes & 15) == 0 ? bytes / 16 : 0;
+  // warp tasks: (row, half); rows of my own tokens stay (the home reads them in place)
+  for (int task = warp * gridDim.x + blockIdx.x; task < 2 * p.rows; task += gridDim.x * nw) {
+    const int r = task >> 1, half = task & 1;
     const int s = p.origin[(int64_t)r * 4 + 1];
+    if (s == me) continue;
     const int t = p.origin[(int64_t)r * 4 + 2];
     const int k = p.origin[(int64_t)r * 4 + 3];
     uint8_t* dst = hpeer(p.peers, s) + g.crow + ((int64_t)t * K + k) * g.crow_stride;
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.y) + (int64_t)r * H * ib;
-    const int bytes = H * ib;
-    if ((bytes & 15) == 0) {
-      for (int c = lane; c < bytes / 16; c += 32) st_na_v4(dst + (int64_t)c * 16, ld_nc_v4(src + (int64_t)c * 16));
-    } else {
-      for (int c = lane; c < bytes / 4; c += 32)
-        reinterpret_cast<uint32_t*>(dst)[c] = reinterpret_cast<const uint32_t*>(src)[c];
-      if (lane == 0 && (bytes & 3))
-        reinterpret_cast<uint16_t*>(dst)[bytes / 2 - 1] = reinterpret_cast<const uint16_t*>(src)[bytes / 2 - 1];
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.y) + (int64_t)r * bytes;
+    if (nch) {
+      const int per = (nch + 1) / 2;
+      const int c0 = half * per, c1 = min(nch, c0 + per);
+      for (int base = c0; base < c1; base += 32 * kHU) {
+        int4 v[kHU];
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+          const int c = base + u * 32 + lane;
+          if (c < c1) v[u] = ld_nc_v4(src + (int64_t)c * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+          const int c = base + u * 32 + lane;
+          if (c < c1) st_na_v4(dst + (int64_t)c * 16, v[u]);
+        }
+      }
+    } else if (half == 0) {
+      for (int c = lane; c < bytes / 2; c += 32)
+        reinterpret_cast<uint16_t*>(dst)[c] = reinterpret_cast<const uint16_t*>(src)[c];
     }
-    if (lane == 0) atomicAdd(&s_cnt[s], 1);
+    if (lane == 0 && half == 0) atomicAdd(&s_cnt[s], 1);
   }
   __syncthreads();
-  if (threadIdx.x < N) {
+  if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
     const int s = threadIdx.x;
     const int c = s_cnt[s];
     const int want = ht_rows_to(p, s);
@@ -370,81 +445,117 @@ __global__ void __launch_bounds__(256) ht_combine_send_kernel(HTCombSend p) {
 struct HTCombRecv {
   const int64_t* topk;
   const float* w;
+  const void* y_local;       // this rank's expert rows [recv_total, H] (own tokens read in place)
+  const int32_t* tok_rank;   // [b, K]
+  const int32_t* offsets;    // [E, N]
   void* out;
   const uint8_t* win;
   int* err;
   HTGeom g;
   uint64_t timeout_ns;
-  int b;
+  int b, rank, y_dtype;
   uint32_t tag;
 };
 
+// 8 consecutive elements (one "chunk") of expert row k of token t, as f32
+EPB_DEV void ht_load8(const uint8_t* row, int dt, int c, float* y) {
+  if (dt == EPB_F32) {
+    unpack16<EPB_F32>(ld_plain_v4(row + (int64_t)c * 32), y);
+    unpack16<EPB_F32>(ld_plain_v4(row + (int64_t)c * 32 + 16), y + 4);
+  } else {
+    unpack16<EPB_BF16>(ld_plain_v4(row + (int64_t)c * 16), y);
+  }
+}
+
 template <int OT>
-__global__ void __launch_bounds__(256) ht_combine_recv_kernel(HTCombRecv p) {
+__global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv p) {
   __shared__ int s_dt[kMaxRanks];
   __shared__ int s_fail;
-  __shared__ float s_w[kMaxTopK];
-  __shared__ int s_node[kMaxTopK], s_kdt[kMaxTopK], s_nodes[kMaxTopK], s_nn;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H, L = g.L;
+  const int me = p.rank;
   if (threadIdx.x == 0) s_fail = 0;
   __syncthreads();
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.cflag);
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
-    if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
-    s_dt[s] = (int)((v >> 28) & 0xF);
+    if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    s_dt[s] = s == me ? p.y_dtype : (int)((v >> 28) & 0xF);
   }
   __syncthreads();
   if (s_fail) return;
   const uint8_t* crow = p.win + g.crow;
-  for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
-    if (threadIdx.x < K) {
-      const int e = (int)p.topk[(int64_t)t * K + threadIdx.x];
-      const int owner = e / L;
-      s_node[threadIdx.x] = owner / g.rpn;
-      s_kdt[threadIdx.x] = s_dt[owner];
-      s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // distinct nodes of this token, ascending (ht.py:718-719)
-      int nn = 0;
-      for (int k = 0; k < K; ++k) {
-        const int nd = s_node[k];
-        int pos = 0;
-        while (pos < nn && s_nodes[pos] < nd) ++pos;
-        if (pos < nn && s_nodes[pos] == nd) continue;
-        for (int j = nn; j > pos; --j) s_nodes[j] = s_nodes[j - 1];
-        s_nodes[pos] = nd;
-        ++nn;
-      }
-      s_nn = nn;
-    }
-    __syncthreads();
-    const int nn = s_nn;
-    uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
-    const uint8_t* tslots = crow + (int64_t)t * K * g.crow_stride;
-    if ((H & 7) == 0) {
-      for (int c = threadIdx.x; c < H / 8; c += blockDim.x) {
-        float acc[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int yb = p.y_dtype == EPB_F32 ? 4 : 2;
+  constexpr int OW = OT == EPB_F32 ? 4 : 2;
+  const bool one_node = g.rpn == N;
+  if ((H & 7) == 0) {
+    // warp tasks: (token, 32-chunk segment of 8 elements); lane = one chunk
+    const int nch = H / 8;
+    const int segs = (nch + 31) / 32;
+    for (int task = warp * gridDim.x + blockIdx.x; task < p.b * segs; task += gridDim.x * nw) {
+      const int t = task / segs, c = (task - t * segs) * 32 + lane;
+      if (c >= nch) continue;
+      float acc[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-        for (int ni = 0; ni < nn; ++ni) {
-          const int nd = s_nodes[ni];
+      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      if (one_node) {
+        // single node: part = p_0 + p_1 + ... (first present as init), out = 0 + part
+        float part[8];
+        for (int k0 = 0; k0 < K; k0 += 4) {
+          float y[4][8];
+          float wk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u;
+            if (k < K) {
+              const int e = (int)p.topk[(int64_t)t * K + k];
+              const int owner = e / L;
+              const uint8_t* row = owner == me
+                  ? reinterpret_cast<const uint8_t*>(p.y_local) +
+                        (int64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]) * H * yb
+                  : crow + ((int64_t)t * K + k) * g.crow_stride;
+              ht_load8(row, s_dt[owner], c, y[u]);
+              wk[u] = p.w[(int64_t)t * K + k];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u;
+            if (k < K) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float pk = __fmul_rn(wk[u], y[u][i]);
+                part[i] = k == 0 ? pk : __fadd_rn(part[i], pk);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(0.0f, part[i]);
+      } else {
+        // several nodes: ascending node, per node first-present then ascending k
+        int prev = -1;
+        for (;;) {
+          int nd = 0x7fffffff;
+          for (int k = 0; k < K; ++k) {
+            const int n2 = ((int)p.topk[(int64_t)t * K + k] / L) / g.rpn;
+            if (n2 > prev && n2 < nd) nd = n2;
+          }
+          if (nd == 0x7fffffff) break;
           float part[8];
           bool started = false;
           for (int k = 0; k < K; ++k) {
-            if (s_node[k] != nd) continue;
+            const int e = (int)p.topk[(int64_t)t * K + k];
+            const int owner = e / L;
+            if (owner / g.rpn != nd) continue;
+            const uint8_t* row = owner == me
+                ? reinterpret_cast<const uint8_t*>(p.y_local) +
+                      (int64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]) * H * yb
+                : crow + ((int64_t)t * K + k) * g.crow_stride;
             float y[8];
-            const uint8_t* sl = tslots + (int64_t)k * g.crow_stride;
-            if (s_kdt[k] == EPB_F32) {
-              unpack16<EPB_F32>(ld_v4(sl + (int64_t)c * 32), y);
-              unpack16<EPB_F32>(ld_v4(sl + (int64_t)c * 32 + 16), y + 4);
-            } else {
-              unpack16<EPB_BF16>(ld_v4(sl + (int64_t)c * 16), y);
-            }
-            const float wk = s_w[k];
+            ht_load8(row, s_dt[owner], c, y);
+            const float wk = p.w[(int64_t)t * K + k];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float pk = __fmul_rn(wk, y[i]);
@@ -454,29 +565,44 @@ __global__ void __launch_bounds__(256) ht_combine_recv_kernel(HTCombRecv p) {
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], part[i]);
+          prev = nd;
         }
-        store_f32_chunk<OT, 8>(orow, (int64_t)c * 8, acc);
       }
-    } else {
+      store_f32_chunk<OT, 8>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * OW, (int64_t)c * 8, acc);
+    }
+  } else {
+    // hidden not a multiple of 8: element path, one CTA per token
+    for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
       for (int el = threadIdx.x; el < H; el += blockDim.x) {
         float acc = 0.0f;
-        for (int ni = 0; ni < nn; ++ni) {
-          const int nd = s_nodes[ni];
+        int prev = -1;
+        for (;;) {
+          int nd = 0x7fffffff;
+          for (int k = 0; k < K; ++k) {
+            const int n2 = ((int)p.topk[(int64_t)t * K + k] / L) / g.rpn;
+            if (n2 > prev && n2 < nd) nd = n2;
+          }
+          if (nd == 0x7fffffff) break;
           float part = 0.0f;
           bool started = false;
           for (int k = 0; k < K; ++k) {
-            if (s_node[k] != nd) continue;
-            const float y = load_elem(tslots + (int64_t)k * g.crow_stride, s_kdt[k], el);
-            const float pk = __fmul_rn(s_w[k], y);
+            const int e = (int)p.topk[(int64_t)t * K + k];
+            const int owner = e / L;
+            if (owner / g.rpn != nd) continue;
+            const uint8_t* row = owner == me
+                ? reinterpret_cast<const uint8_t*>(p.y_local) +
+                      (int64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]) * H * yb
+                : crow + ((int64_t)t * K + k) * g.crow_stride;
+            const float pk = __fmul_rn(p.w[(int64_t)t * K + k], load_elem(row, s_dt[owner], el));
             part = started ? __fadd_rn(part, pk) : pk;
             started = true;
           }
           acc = __fadd_rn(acc, part);
+          prev = nd;
         }
-        store_elem(orow, OT, el, acc);
+        store_elem(reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * OW, OT, el, acc);
       }
     }
-    __syncthreads();
   }
 }
 
@@ -504,41 +630,49 @@ int hsm_count() {
   return n;
 }
 
-int check_ht(epb_group* g) {
+int check_ht(epb_group* g, int phases) {
   if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
   if (g->cfg.algorithm != EPB_HT) return fail(EPB_HANDLE_STATE_ERROR, "group is not HT");
   if (!g->peers_ready) return fail(EPB_HANDLE_STATE_ERROR, "peer windows not mapped");
+  if (phases < 1 || phases > 3) return fail(EPB_INVALID_ARGUMENT, "phases must be 1 (send), 2 (recv) or 3");
   return EPB_OK;
 }
 
-template <int XT, int WT>
+template <int XT, int WT, int OT>
 cudaError_t launch_hsend(const HTSend& p, cudaStream_t s) {
-  const int grid = max(1, min(p.b, 2 * hsm_count()));
-  ht_dispatch_send_kernel<XT, WT><<<grid, 512, 0, s>>>(p);
+  const int grid = std::max(1, std::min(p.b, 2 * hsm_count()));
+  ht_dispatch_send_kernel<XT, WT, OT><<<grid, kHTThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
+template <int XT, int WT>
+cudaError_t launch_hsend_o(const HTSend& p, int out_dtype, cudaStream_t s) {
+  return out_dtype == EPB_F32 ? launch_hsend<XT, WT, EPB_F32>(p, s) : launch_hsend<XT, WT, WT>(p, s);
+}
+
 template <int XT>
-cudaError_t launch_hsend_x(const HTSend& p, cudaStream_t s) {
+cudaError_t launch_hsend_x(const HTSend& p, int out_dtype, cudaStream_t s) {
   switch (p.g.wire) {
-    case EPB_F32: return launch_hsend<XT, EPB_F32>(p, s);
-    case EPB_BF16: return launch_hsend<XT, EPB_BF16>(p, s);
-    default: return launch_hsend<XT, EPB_F16>(p, s);
+    case EPB_F32: return launch_hsend<XT, EPB_F32, EPB_F32>(p, s);
+    case EPB_BF16: return launch_hsend_o<XT, EPB_BF16>(p, out_dtype, s);
+    default: return launch_hsend_o<XT, EPB_F16>(p, out_dtype, s);
   }
 }
 
 template <int WT, int OT>
 cudaError_t launch_hrecv(const HTRecv& p, cudaStream_t s) {
-  ht_dispatch_recv_kernel<WT, OT><<<2 * hsm_count(), 256, 0, s>>>(p);
+  ht_dispatch_recv_kernel<WT, OT><<<2 * hsm_count(), kHTThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
+
+bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
 
 extern "C" {
 
 int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay, void* stream) {
-  if (int rc = check_ht(g)) return rc;
+  if (int rc = check_ht(g, 1)) return rc;
   HTMetaSend p;
   p.m = lay->expert_count; p.q = lay->rank_count; p.peers = g->d_peers; p.g = g->ht;
   p.rank = g->rank; p.parity = round & 1; p.tag = ht_tag(round);
@@ -549,7 +683,7 @@ int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay, void* 
 
 int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out, int32_t* offsets,
                      int32_t* recv_total, void* stream) {
-  if (int rc = check_ht(g)) return rc;
+  if (int rc = check_ht(g, 2)) return rc;
   HTMetaRecv p;
   p.win = g->window; p.meta_out = meta_out; p.offsets = offsets; p.recv_total = recv_total;
   p.err = g->d_err; p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank;
@@ -562,86 +696,78 @@ int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out, int32_t* o
   return EPB_OK;
 }
 
-int epb_ht_dispatch_send(epb_group* g, uint32_t round, const void* x, int32_t x_dtype,
-                         const float* weights, const int64_t* topk_idx, const epb_layout* lay,
-                         const int32_t* offsets, void* stream) {
-  if (int rc = check_ht(g)) return rc;
-  if (lay->num_tokens > 0 && (reinterpret_cast<uintptr_t>(x) & 15))
-    return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
-  HTSend p;
-  p.x = x; p.w = weights; p.topk = topk_idx; p.q = lay->rank_count; p.tok_rank = lay->tok_rank;
-  p.tok_slot = lay->tok_slot; p.offsets = offsets; p.peers = g->d_peers; p.done = g->d_done;
-  p.g = g->ht; p.b = lay->num_tokens; p.rank = g->rank; p.tag = ht_tag(round);
-  cudaStream_t s = as_stream(stream);
-  cudaError_t e;
-  switch (x_dtype) {
-    case EPB_F32: e = launch_hsend_x<EPB_F32>(p, s); break;
-    case EPB_BF16: e = launch_hsend_x<EPB_BF16>(p, s); break;
-    case EPB_F16: e = launch_hsend_x<EPB_F16>(p, s); break;
-    default: return fail(EPB_TAG_MISMATCH, "HT dispatch input must be f32/bf16/f16");
-  }
-  if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_send");
-  return EPB_OK;
-}
-
-int epb_ht_dispatch_recv(epb_group* g, uint32_t round, void* out, int32_t out_dtype, int32_t* origin,
-                         float* origin_w, void* stream) {
-  if (int rc = check_ht(g)) return rc;
+int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases, const epb_ht_dispatch_args* a, void* stream) {
+  if (int rc = check_ht(g, phases)) return rc;
   const int wire = g->cfg.token_dtype;
-  if (out_dtype != EPB_F32 && out_dtype != wire)
+  if (a->out_dtype != EPB_F32 && a->out_dtype != wire)
     return fail(EPB_TAG_MISMATCH, "dispatch output must be f32 or the wire dtype");
-  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
-  HTRecv p;
-  p.out = out; p.origin = origin; p.origin_w = origin_w; p.win = g->window; p.err = g->d_err;
-  p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank; p.tag = ht_tag(round);
+  if (!a16(a->out)) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
   cudaStream_t s = as_stream(stream);
-  cudaError_t e;
-  switch (wire) {
-    case EPB_F32: e = launch_hrecv<EPB_F32, EPB_F32>(p, s); break;
-    case EPB_BF16:
-      e = out_dtype == EPB_F32 ? launch_hrecv<EPB_BF16, EPB_F32>(p, s) : launch_hrecv<EPB_BF16, EPB_BF16>(p, s);
-      break;
-    default:
-      e = out_dtype == EPB_F32 ? launch_hrecv<EPB_F16, EPB_F32>(p, s) : launch_hrecv<EPB_F16, EPB_F16>(p, s);
+  if (phases & 1) {
+    if (a->num_tokens > 0 && !a16(a->x)) return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
+    HTSend p;
+    p.x = a->x; p.w = a->weights; p.topk = a->topk_idx; p.q = a->rank_count; p.tok_rank = a->tok_rank;
+    p.tok_slot = a->tok_slot; p.offsets = a->offsets; p.peers = g->d_peers; p.out = a->out;
+    p.origin = a->origin; p.origin_w = a->origin_w; p.done = g->d_done; p.g = g->ht;
+    p.b = a->num_tokens; p.rank = g->rank; p.tag = ht_tag(round);
+    cudaError_t e;
+    switch (a->x_dtype) {
+      case EPB_F32: e = launch_hsend_x<EPB_F32>(p, a->out_dtype, s); break;
+      case EPB_BF16: e = launch_hsend_x<EPB_BF16>(p, a->out_dtype, s); break;
+      case EPB_F16: e = launch_hsend_x<EPB_F16>(p, a->out_dtype, s); break;
+      default: return fail(EPB_TAG_MISMATCH, "HT dispatch input must be f32/bf16/f16");
+    }
+    if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_send");
   }
-  if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_recv");
+  if (phases & 2) {
+    HTRecv p;
+    p.out = a->out; p.origin = a->origin; p.origin_w = a->origin_w; p.win = g->window; p.err = g->d_err;
+    p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank; p.tag = ht_tag(round);
+    cudaError_t e;
+    switch (wire) {
+      case EPB_F32: e = launch_hrecv<EPB_F32, EPB_F32>(p, s); break;
+      case EPB_BF16:
+        e = a->out_dtype == EPB_F32 ? launch_hrecv<EPB_BF16, EPB_F32>(p, s) : launch_hrecv<EPB_BF16, EPB_BF16>(p, s);
+        break;
+      default:
+        e = a->out_dtype == EPB_F32 ? launch_hrecv<EPB_F16, EPB_F32>(p, s) : launch_hrecv<EPB_F16, EPB_F16>(p, s);
+    }
+    if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_recv");
+  }
   return EPB_OK;
 }
 
-int epb_ht_combine_send(epb_group* g, uint32_t round, const void* expert_rows, int32_t in_dtype,
-                        const int32_t* origin, int32_t recv_total, void* stream) {
-  if (int rc = check_ht(g)) return rc;
-  if (in_dtype != EPB_F32 && in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
-  if (recv_total > 0 && (reinterpret_cast<uintptr_t>(expert_rows) & 15))
-    return fail(EPB_INVALID_ARGUMENT, "expert rows must be 16-byte aligned");
-  // the metadata rows of this round live in the window (parity = round & 1)
-  HTCombSend p;
-  p.y = expert_rows; p.origin = origin;
-  p.meta = reinterpret_cast<const int32_t*>(g->window + g->ht.meta +
-                                            (uint64_t)(round & 1) * g->ht.N * (g->ht.E + g->ht.N) * 4);
-  p.peers = g->d_peers; p.done = g->d_done + g->cfg.num_ranks; p.g = g->ht; p.rows = recv_total;
-  p.rank = g->rank; p.in_dtype = in_dtype; p.tag = ht_tag(round);
-  const int grid = max(1, min(2 * hsm_count(), (recv_total + 7) / 8));
+int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_combine_args* a, void* stream) {
+  if (int rc = check_ht(g, phases)) return rc;
+  if (a->in_dtype != EPB_F32 && a->in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
+  if (a->recv_total > 0 && !a16(a->expert_rows)) return fail(EPB_INVALID_ARGUMENT, "expert rows must be 16-byte aligned");
   cudaStream_t s = as_stream(stream);
-  if (in_dtype == EPB_F32) ht_combine_send_kernel<EPB_F32><<<grid, 256, 0, s>>>(p);
-  else ht_combine_send_kernel<EPB_BF16><<<grid, 256, 0, s>>>(p);
-  EPB_LAUNCH_CHECK();
-  return EPB_OK;
-}
-
-int epb_ht_combine_recv(epb_group* g, uint32_t round, const int64_t* topk_idx, const float* weights,
-                        int32_t b, void* out, int32_t out_dtype, void* stream) {
-  if (int rc = check_ht(g)) return rc;
-  if (out_dtype != EPB_F32 && out_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine output f32|bf16");
-  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
-  HTCombRecv p;
-  p.topk = topk_idx; p.w = weights; p.out = out; p.win = g->window; p.err = g->d_err; p.g = g->ht;
-  p.timeout_ns = g->timeout_ns; p.b = b; p.tag = ht_tag(round);
-  const int grid = max(1, min(b, 4 * hsm_count()));
-  cudaStream_t s = as_stream(stream);
-  if (out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_F32><<<grid, 256, 0, s>>>(p);
-  else ht_combine_recv_kernel<EPB_BF16><<<grid, 256, 0, s>>>(p);
-  EPB_LAUNCH_CHECK();
+  if (phases & 1) {
+    // the metadata rows of this round live in the window (parity = round & 1)
+    HTCombSend p;
+    p.y = a->expert_rows; p.origin = a->origin;
+    p.meta = reinterpret_cast<const int32_t*>(g->window + g->ht.meta +
+                                              (uint64_t)(round & 1) * g->ht.N * (g->ht.E + g->ht.N) * 4);
+    p.peers = g->d_peers; p.done = g->d_done + g->cfg.num_ranks; p.g = g->ht; p.rows = a->recv_total;
+    p.rank = g->rank; p.in_dtype = a->in_dtype; p.tag = ht_tag(round);
+    const int grid = 2 * hsm_count();
+    if (a->in_dtype == EPB_F32) ht_combine_send_kernel<EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
+    else ht_combine_send_kernel<EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
+    EPB_LAUNCH_CHECK();
+  }
+  if (phases & 2) {
+    if (a->out_dtype != EPB_F32 && a->out_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine output f32|bf16");
+    if (!a16(a->out)) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
+    HTCombRecv p;
+    p.topk = a->topk_idx; p.w = a->weights; p.y_local = a->expert_rows; p.tok_rank = a->tok_rank;
+    p.offsets = a->offsets; p.out = a->out; p.win = g->window; p.err = g->d_err; p.g = g->ht;
+    p.timeout_ns = g->timeout_ns; p.b = a->num_tokens; p.rank = g->rank; p.y_dtype = a->in_dtype;
+    p.tag = ht_tag(round);
+    const int grid = 2 * hsm_count();
+    if (a->out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
+    else ht_combine_recv_kernel<EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
+    EPB_LAUNCH_CHECK();
+  }
   return EPB_OK;
 }
 
