@@ -156,45 +156,33 @@ EPB_DEV void ht_publish_records(const HTSend& p, int d) {
 
 template <int XT, int WT, int OT>
 __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) {
-  __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks], s_nd;
-  __shared__ int s_pos[kMaxTopK], s_ns;      // self rows: output positions
-  __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
-  __shared__ float s_w[kMaxTopK];
+  // a CTA owns tokens blockIdx.x + i*gridDim.x; their routing metadata is
+  // gathered for kTB tokens at once (one latency for the batch), then rows
+  // move token by token
+  constexpr int kTB = 16;
+  __shared__ int s_e[kTB][kMaxTopK], s_pos[kTB][kMaxTopK];
+  __shared__ float s_w[kTB][kMaxTopK];
+  __shared__ int s_j[kTB][kMaxRanks];
   __shared__ int s_cnt[kMaxRanks];
   const HTGeom& g = p.g;
-  const int K = g.K, N = g.N, H = g.H, L = g.L;
+  const int K = g.K, N = g.N, H = g.H, L = g.L, G = gridDim.x;
   const int me = p.rank;
   constexpr int EPC = Elems<WT>::n;
   constexpr int XW = XT == EPB_F32 ? 4 : 2;
   constexpr int OW = OT == EPB_F32 ? 4 : 2;
+  const int64_t rec0 = (int64_t)me * g.B;
   if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
-  for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
+  for (int base = blockIdx.x; base < p.b; base += G * kTB) {
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int nd = 0;
-      for (int d = 0; d < N; ++d) {
-        const int j = p.tok_slot[(int64_t)t * N + d];
-        if (j >= 0 && d != me) { s_dst[nd] = d; s_j[nd] = j; ++nd; s_cnt[d] += 1; }
-      }
-      s_nd = nd;
-      s_hdr[0] = (uint32_t)t;
-      s_hdr[1] = (uint32_t)K;
-    }
-    if (threadIdx.x == 32) {
-      int ns = 0;
-      for (int k = 0; k < K; ++k) {
-        const int e = (int)p.topk[(int64_t)t * K + k];
-        if (e / L == me) s_pos[ns++] = p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k];
-      }
-      s_ns = ns;
-    }
-    if ((int)threadIdx.x < K) {
-      const int k = threadIdx.x;
+    for (int idx = threadIdx.x; idx < kTB * K; idx += blockDim.x) {
+      const int i = idx / K, k = idx - i * K, t = base + i * G;
+      if (t >= p.b) continue;
       const int e = (int)p.topk[(int64_t)t * K + k];
       const int pos = p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k];
       const float wk = p.w[(int64_t)t * K + k];
-      s_hdr[2 + k] = (uint32_t)e;
-      s_w[k] = wk;
+      s_e[i][k] = e;
+      s_pos[i][k] = pos;
+      s_w[i][k] = wk;
       if (e / L == me) {
         p.origin[(int64_t)pos * 4 + 0] = e;
         p.origin[(int64_t)pos * 4 + 1] = me;
@@ -202,48 +190,62 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) 
         p.origin[(int64_t)pos * 4 + 3] = k;
         p.origin_w[pos] = wk;
       }
-      // position on the owner; only meaningful to the owner's receiver
-      s_hdr[2 + K + k] = (uint32_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]);
+    }
+    for (int idx = threadIdx.x; idx < kTB * N; idx += blockDim.x) {
+      const int i = idx / N, d = idx - i * N, t = base + i * G;
+      int j = -1;
+      if (t < p.b && d != me) j = p.tok_slot[(int64_t)t * N + d];
+      s_j[i][d] = j;
     }
     __syncthreads();
-    const int nd = s_nd, ns = s_ns;
-    const int64_t rec0 = (int64_t)me * g.B;
-    for (int wd = threadIdx.x; wd < K + 2 + 2 * K; wd += blockDim.x) {
-      for (int i = 0; i < nd; ++i) {
-        uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
-        if (wd < K) reinterpret_cast<float*>(rec + g.RBp)[wd] = s_w[wd];
-        else reinterpret_cast<uint32_t*>(rec + g.RBp + g.WBp)[wd - K] = s_hdr[wd - K];
-      }
-    }
-    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
-    if ((H & 15) == 0) {
-      for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
-        float f[EPC];
-        load_elems_vec<XT, EPC>(xrow, (int64_t)c * EPC, f);
-        const int4 v = pack16<WT>(f);
-        for (int i = 0; i < nd; ++i) {
-          uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
-          st_na_v4(rec + (int64_t)c * 16, v);
+    if ((int)threadIdx.x < N)
+      for (int i = 0; i < kTB; ++i) s_cnt[threadIdx.x] += s_j[i][threadIdx.x] >= 0;
+    for (int i = 0; i < kTB; ++i) {
+      const int t = base + i * G;
+      if (t >= p.b) break;
+      // record header (reference fields + output positions) and weights
+      const int words = K + 2 + 2 * K;
+      for (int idx = threadIdx.x; idx < N * words; idx += blockDim.x) {
+        const int d = idx / words, wd = idx - d * words;
+        if (s_j[i][d] < 0) continue;
+        uint8_t* rec = hpeer(p.peers, d) + g.rec + (rec0 + s_j[i][d]) * g.rec_stride;
+        if (wd < K) {
+          reinterpret_cast<float*>(rec + g.RBp)[wd] = s_w[i][wd];
+        } else {
+          const int h = wd - K;
+          const uint32_t v = h == 0 ? (uint32_t)t : h == 1 ? (uint32_t)K
+                             : h < 2 + K ? (uint32_t)s_e[i][h - 2] : (uint32_t)s_pos[i][h - 2 - K];
+          reinterpret_cast<uint32_t*>(rec + g.RBp + g.WBp)[h] = v;
         }
-        if (ns) {
+      }
+      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
+      if ((H & 15) == 0) {
+        for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
+          float f[EPC];
+          load_elems_vec<XT, EPC>(xrow, (int64_t)c * EPC, f);
+          const int4 v = pack16<WT>(f);
+          for (int d = 0; d < N; ++d) {
+            const int j = s_j[i][d];
+            if (j >= 0) st_na_v4(hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride + (int64_t)c * 16, v);
+          }
           float fw[EPC];
-          unpack16<WT>(v, fw);  // the wire image, exactly what a record would carry
-          for (int i = 0; i < ns; ++i)
-            store_f32_chunk<OT, EPC>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i] * H * OW,
-                                     (int64_t)c * EPC, fw);
+          unpack16<WT>(v, fw);  // the wire image, exactly what a record carries
+          for (int k = 0; k < K; ++k)
+            if (s_e[i][k] / L == me)
+              store_f32_chunk<OT, EPC>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW,
+                                       (int64_t)c * EPC, fw);
         }
-      }
-    } else {
-      for (int el = threadIdx.x; el < H; el += blockDim.x) {
-        const float f = load_elem(xrow, XT, el);
-        for (int i = 0; i < nd; ++i) {
-          uint8_t* rec = hpeer(p.peers, s_dst[i]) + g.rec + (rec0 + s_j[i]) * g.rec_stride;
-          store_elem(rec, WT, el, f);
-        }
-        if (ns) {
+      } else {
+        for (int el = threadIdx.x; el < H; el += blockDim.x) {
+          const float f = load_elem(xrow, XT, el);
+          for (int d = 0; d < N; ++d) {
+            const int j = s_j[i][d];
+            if (j >= 0) store_elem(hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride, WT, el, f);
+          }
           const float fw = WT == EPB_F32 ? f : (WT == EPB_BF16 ? bf16_widen(bf16_bits_rne(f)) : f16_widen(f16_bits_rne(f)));
-          for (int i = 0; i < ns; ++i)
-            store_elem(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i] * H * OW, OT, el, fw);
+          for (int k = 0; k < K; ++k)
+            if (s_e[i][k] / L == me)
+              store_elem(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW, OT, el, fw);
         }
       }
     }
@@ -457,9 +459,10 @@ struct HTCombRecv {
   uint32_t tag;
 };
 
-// 8 consecutive elements (one "chunk") of expert row k of token t, as f32
-EPB_DEV void ht_load8(const uint8_t* row, int dt, int c, float* y) {
-  if (dt == EPB_F32) {
+// 8 consecutive elements (chunk c) of a row in dtype IT, as f32
+template <int IT>
+EPB_DEV void ht_load8(const uint8_t* row, int c, float* y) {
+  if constexpr (IT == EPB_F32) {
     unpack16<EPB_F32>(ld_plain_v4(row + (int64_t)c * 32), y);
     unpack16<EPB_F32>(ld_plain_v4(row + (int64_t)c * 32 + 16), y + 4);
   } else {
@@ -467,35 +470,50 @@ EPB_DEV void ht_load8(const uint8_t* row, int dt, int c, float* y) {
   }
 }
 
-template <int OT>
+template <int IT, int OT>
 __global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv p) {
-  __shared__ int s_dt[kMaxRanks];
   __shared__ int s_fail;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H, L = g.L;
   const int me = p.rank;
+  constexpr int YB = IT == EPB_F32 ? 4 : 2;
+  constexpr int OW = OT == EPB_F32 ? 4 : 2;
   if (threadIdx.x == 0) s_fail = 0;
   __syncthreads();
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.cflag);
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
-    if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
-    s_dt[s] = s == me ? p.y_dtype : (int)((v >> 28) & 0xF);
+    if (s == me) continue;
+    if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) { s_fail = 1; continue; }
+    // every rank must combine in the same dtype (the rows are raw bytes)
+    if ((int)((v >> 28) & 0xF) != IT) { atomicCAS(p.err, 0, EPB_TAG_MISMATCH); s_fail = 1; }
   }
   __syncthreads();
   if (s_fail) return;
   const uint8_t* crow = p.win + g.crow;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int yb = p.y_dtype == EPB_F32 ? 4 : 2;
-  constexpr int OW = OT == EPB_F32 ? 4 : 2;
   const bool one_node = g.rpn == N;
-  if ((H & 7) == 0) {
-    // warp tasks: (token, 32-chunk segment of 8 elements); lane = one chunk
+  if ((H & 7) == 0 && K <= 32) {
+    // warp tasks: (token, 32-chunk segment of 8 elements); lane = one chunk.
+    // Lane k first resolves row k of the token (own expert rows are read in
+    // place from the local expert output, others from the combine slots).
     const int nch = H / 8;
     const int segs = (nch + 31) / 32;
     for (int task = warp * gridDim.x + blockIdx.x; task < p.b * segs; task += gridDim.x * nw) {
       const int t = task / segs, c = (task - t * segs) * 32 + lane;
-      if (c >= nch) continue;
+      uint64_t my_row = 0;
+      float my_w = 0.0f;
+      int my_node = 0;
+      if (lane < K) {
+        const int e = (int)p.topk[(int64_t)t * K + lane];
+        const int owner = e / L;
+        my_node = owner / g.rpn;
+        my_w = p.w[(int64_t)t * K + lane];
+        my_row = owner == me
+            ? reinterpret_cast<uint64_t>(p.y_local) +
+                  (uint64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + lane]) * H * YB
+            : reinterpret_cast<uint64_t>(crow + ((int64_t)t * K + lane) * g.crow_stride);
+      }
       float acc[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
@@ -507,17 +525,9 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv 
           float wk[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int k = k0 + u;
-            if (k < K) {
-              const int e = (int)p.topk[(int64_t)t * K + k];
-              const int owner = e / L;
-              const uint8_t* row = owner == me
-                  ? reinterpret_cast<const uint8_t*>(p.y_local) +
-                        (int64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]) * H * yb
-                  : crow + ((int64_t)t * K + k) * g.crow_stride;
-              ht_load8(row, s_dt[owner], c, y[u]);
-              wk[u] = p.w[(int64_t)t * K + k];
-            }
+            const uint64_t row = __shfl_sync(0xffffffffu, my_row, (k0 + u) & 31);
+            wk[u] = __shfl_sync(0xffffffffu, my_w, (k0 + u) & 31);
+            if (k0 + u < K && c < nch) ht_load8<IT>(reinterpret_cast<const uint8_t*>(row), c, y[u]);
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -539,23 +549,19 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv 
         for (;;) {
           int nd = 0x7fffffff;
           for (int k = 0; k < K; ++k) {
-            const int n2 = ((int)p.topk[(int64_t)t * K + k] / L) / g.rpn;
+            const int n2 = __shfl_sync(0xffffffffu, my_node, k);
             if (n2 > prev && n2 < nd) nd = n2;
           }
           if (nd == 0x7fffffff) break;
           float part[8];
           bool started = false;
           for (int k = 0; k < K; ++k) {
-            const int e = (int)p.topk[(int64_t)t * K + k];
-            const int owner = e / L;
-            if (owner / g.rpn != nd) continue;
-            const uint8_t* row = owner == me
-                ? reinterpret_cast<const uint8_t*>(p.y_local) +
-                      (int64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]) * H * yb
-                : crow + ((int64_t)t * K + k) * g.crow_stride;
+            const int n2 = __shfl_sync(0xffffffffu, my_node, k);
+            const uint64_t row = __shfl_sync(0xffffffffu, my_row, k);
+            const float wk = __shfl_sync(0xffffffffu, my_w, k);
+            if (n2 != nd) continue;
             float y[8];
-            ht_load8(row, s_dt[owner], c, y);
-            const float wk = p.w[(int64_t)t * K + k];
+            if (c < nch) ht_load8<IT>(reinterpret_cast<const uint8_t*>(row), c, y);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float pk = __fmul_rn(wk, y[i]);
@@ -568,7 +574,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv 
           prev = nd;
         }
       }
-      store_f32_chunk<OT, 8>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * OW, (int64_t)c * 8, acc);
+      if (c < nch) store_f32_chunk<OT, 8>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * OW, (int64_t)c * 8, acc);
     }
   } else {
     // hidden not a multiple of 8: element path, one CTA per token
@@ -591,9 +597,9 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv 
             if (owner / g.rpn != nd) continue;
             const uint8_t* row = owner == me
                 ? reinterpret_cast<const uint8_t*>(p.y_local) +
-                      (int64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]) * H * yb
+                      (int64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k]) * H * YB
                 : crow + ((int64_t)t * K + k) * g.crow_stride;
-            const float pk = __fmul_rn(p.w[(int64_t)t * K + k], load_elem(row, s_dt[owner], el));
+            const float pk = __fmul_rn(p.w[(int64_t)t * K + k], load_elem(row, IT, el));
             part = started ? __fadd_rn(part, pk) : pk;
             started = true;
           }
@@ -764,8 +770,13 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
     p.timeout_ns = g->timeout_ns; p.b = a->num_tokens; p.rank = g->rank; p.y_dtype = a->in_dtype;
     p.tag = ht_tag(round);
     const int grid = 2 * hsm_count();
-    if (a->out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
-    else ht_combine_recv_kernel<EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
+    if (a->in_dtype == EPB_F32) {
+      if (a->out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_F32, EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
+      else ht_combine_recv_kernel<EPB_F32, EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
+    } else {
+      if (a->out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_BF16, EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
+      else ht_combine_recv_kernel<EPB_BF16, EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
+    }
     EPB_LAUNCH_CHECK();
   }
   return EPB_OK;
