@@ -409,7 +409,7 @@ def run_ht(args, world, rank):
         for i in range(len(marks) - 1):
             tphase[names[i]] = tphase.get(names[i], 0.0) + marks[i][1].elapsed_time(marks[i + 1][1])
         td.append(ev["epb_ht_dispatch"].elapsed_time(ev["dispatch:end"]))
-        tc.append(ev["epb_weights_equal"].elapsed_time(ev["combine:end"]))
+        tc.append(ev["epb_ht_combine"].elapsed_time(ev["combine:end"]))
     g.check()
     barrier(world)
     t_d = allreduce_max(statistics.median(td), world) / 1e3

@@ -227,6 +227,9 @@ typedef struct epb_ht_combine_args {
   const int32_t* offsets;    /* [E, N] */
   void* out;                 /* [b, H] f32|bf16 */
   int32_t out_dtype;
+  const float* dispatch_weights; /* [b, K] weights given at dispatch, checked
+                                    against `weights` before any traffic
+                                    (ht.py:605-609); NULL skips the check */
 } epb_ht_combine_args;
 int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases,
                    const epb_ht_combine_args* args, void* stream);

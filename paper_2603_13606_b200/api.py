@@ -425,8 +425,14 @@ class EpHandle:
         g._launch("epb_ht_meta_recv", g._g, rnd, _ptr(meta), _ptr(offsets), _ptr(total), self._sp())
         g.check()  # synchronises: receive shapes are host-known on return (api.py:235-237)
         meta_h = meta.cpu().numpy()
+        ell = cfg.experts_per_rank
+        lo = g.rank * ell
+        hi = min(lo + ell, e)
+        counts = np.zeros((ell, n), dtype=np.float32)  # TOKENS_PER_EXPERTS (api.py:437-441)
+        counts[:hi - lo] = meta_h[:, lo:hi].T
         self._meta = dict(m=meta_h[:, :e].astype(np.int64), q=meta_h[:, e:].astype(np.int64),
-                          recv_total=int(total.item()), offsets=offsets)
+                          recv_total=int(total.item()), offsets=offsets,
+                          counts_dev=torch.from_numpy(counts).to(dev))
         self._round_open = True
 
     # -- staging helpers ----------------------------------------------------------
@@ -595,9 +601,7 @@ class EpHandle:
         ell, n = cfg.experts_per_rank, cfg.num_ranks
         lo = g.rank * ell
         hi = min(lo + ell, cfg.num_experts)
-        counts = np.zeros((ell, n), dtype=np.float32)
-        counts[:hi - lo] = meta["m"][:, lo:hi].T
-        out_counts.view().copy_(torch.from_numpy(counts))
+        out_counts.view().copy_(meta["counts_dev"])
         self._round_open = False
         self._dispatch_result = HTDispatchResult(out_t, origin[:total], origin_w[:total], meta["m"],
                                                  meta["q"], total)
@@ -670,13 +674,13 @@ class EpHandle:
         res = self._dispatch_result
         # combine weights must equal the dispatched ones (ht.py:605-609),
         # checked on the device before any combine traffic
-        g._launch("epb_weights_equal", g._g, _ptr(w), _ptr(self._weights), w.numel(), self._sp())
-        if g.strict:
-            g.check()
+        # (the weights-equal check runs first inside epb_ht_combine; a
+        # mismatch aborts the combine kernels before any traffic)
         o, back = self._dev_out(out, full=True)
         a = _lib.HTCombineArgs(y.data_ptr(), y_dtype.code, res.origin.data_ptr(), res.recv_total,
                                self.routing.data_ptr(), w.data_ptr(), self._b, self._tok_rank.data_ptr(),
-                               self._meta["offsets"].data_ptr(), o.data_ptr(), out.dtype.code)
+                               self._meta["offsets"].data_ptr(), o.data_ptr(), out.dtype.code,
+                               self._weights.data_ptr())
         if g._fused_ok():
             g._launch("epb_ht_combine", g._g, self._round, _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
         else:

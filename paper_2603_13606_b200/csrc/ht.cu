@@ -109,22 +109,37 @@ __global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
   __syncthreads();
   // offsets[e, s]: row of group (e, s) inside owner(e)'s sorted output
   // = (rows of earlier local experts of owner(e)) + (rows of e from src < s)
+  int* s_col = s_meta + N * C;  // [E]: per-expert totals, then their per-owner exclusive scan
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int lo = (e / L) * L;
-    int base = 0;
-    for (int e2 = lo; e2 < e; ++e2)
-      for (int s = 0; s < N; ++s) base += s_meta[s * C + e2];
+    int tot = 0;
+    for (int s = 0; s < N; ++s) tot += s_meta[s * C + e];
+    s_col[e] = tot;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int d = warp; d < N; d += blockDim.x >> 5) {  // one warp per owner: shuffle scan
+    const int lo = d * L, hi = min(lo + L, E);
+    int carry = 0;
+    for (int b0 = lo; b0 < hi; b0 += 32) {
+      const int e = b0 + lane;
+      const int v = e < hi ? s_col[e] : 0;
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (e < hi) s_col[e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (d == p.rank && lane == 0) *p.recv_total = carry;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int base = s_col[e];
     for (int s = 0; s < N; ++s) {
       p.offsets[e * N + s] = base;
       base += s_meta[s * C + e];
     }
-  }
-  if (threadIdx.x == 0) {
-    const int lo = p.rank * L, hi = min(lo + L, E);
-    int tot = 0;
-    for (int e = lo; e < hi; ++e)
-      for (int s = 0; s < N; ++s) tot += s_meta[s * C + e];
-    *p.recv_total = tot;
   }
 }
 
@@ -360,6 +375,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
 // ---------------------------------------------------------------------------
 struct HTCombSend {
   const void* y;
+  const int* err;        // a failed validation (weights) aborts before any traffic
   const int32_t* origin;
   const int32_t* meta;  // [N][E+N] (m rows)
   const uint64_t* peers;
@@ -388,6 +404,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H;
   const int me = p.rank;
+  if (*reinterpret_cast<const volatile int*>(p.err) != 0) return;
   if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -471,15 +488,16 @@ EPB_DEV void ht_load8(const uint8_t* row, int c, float* y) {
 }
 
 template <int IT, int OT>
-__global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv p) {
+__global__ void __launch_bounds__(kHTThreads, 2) ht_combine_recv_kernel(HTCombRecv p) {
   __shared__ int s_fail;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H, L = g.L;
   const int me = p.rank;
   constexpr int YB = IT == EPB_F32 ? 4 : 2;
   constexpr int OW = OT == EPB_F32 ? 4 : 2;
-  if (threadIdx.x == 0) s_fail = 0;
+  if (threadIdx.x == 0) s_fail = *reinterpret_cast<const volatile int*>(p.err) != 0;
   __syncthreads();
+  if (s_fail) return;
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.cflag);
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
@@ -518,31 +536,44 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_recv_kernel(HTCombRecv 
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
       if (one_node) {
-        // single node: part = p_0 + p_1 + ... (first present as init), out = 0 + part
-        float part[8];
-        for (int k0 = 0; k0 < K; k0 += 4) {
-          float y[4][8];
-          float wk[4];
+        // single node: acc = p_0 + p_1 + ... (first present as init), then
+        // out = 0 + acc; all KB rows of a batch are in flight at once
+        constexpr int KB = IT == EPB_F32 ? 2 : 4;
+        constexpr int NV = IT == EPB_F32 ? 2 : 1;  // 16-B loads per 8-element chunk
+        for (int k0 = 0; k0 < K; k0 += KB) {
+          int4 v[KB][NV];
+          float wk[KB];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < KB; ++u) {
             const uint64_t row = __shfl_sync(0xffffffffu, my_row, (k0 + u) & 31);
             wk[u] = __shfl_sync(0xffffffffu, my_w, (k0 + u) & 31);
-            if (k0 + u < K && c < nch) ht_load8<IT>(reinterpret_cast<const uint8_t*>(row), c, y[u]);
+            if (k0 + u < K && c < nch) {
+#pragma unroll
+              for (int q = 0; q < NV; ++q)
+                v[u][q] = ld_plain_v4(reinterpret_cast<const uint8_t*>(row) + (int64_t)c * 16 * NV + 16 * q);
+            }
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < KB; ++u) {
             const int k = k0 + u;
             if (k < K) {
+              float y[8];
+              if constexpr (IT == EPB_F32) {
+                unpack16<EPB_F32>(v[u][0], y);
+                unpack16<EPB_F32>(v[u][1], y + 4);
+              } else {
+                unpack16<EPB_BF16>(v[u][0], y);
+              }
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const float pk = __fmul_rn(wk[u], y[u][i]);
-                part[i] = k == 0 ? pk : __fadd_rn(part[i], pk);
+                const float pk = __fmul_rn(wk[u], y[i]);
+                acc[i] = k == 0 ? pk : __fadd_rn(acc[i], pk);
               }
             }
           }
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(0.0f, part[i]);
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(0.0f, acc[i]);
       } else {
         // several nodes: ascending node, per node first-present then ascending k
         int prev = -1;
@@ -694,7 +725,7 @@ int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out, int32_t* o
   p.win = g->window; p.meta_out = meta_out; p.offsets = offsets; p.recv_total = recv_total;
   p.err = g->d_err; p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank;
   p.parity = round & 1; p.tag = ht_tag(round);
-  const size_t smem = sizeof(int32_t) * g->ht.N * (g->ht.E + g->ht.N);
+  const size_t smem = sizeof(int32_t) * (g->ht.N * (g->ht.E + g->ht.N) + g->ht.E);
   if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "metadata too large");
   EPB_CUDA(cudaFuncSetAttribute(ht_meta_recv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ht_meta_recv_kernel<<<1, 1024, smem, as_stream(stream)>>>(p);
@@ -748,9 +779,17 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
   if (a->in_dtype != EPB_F32 && a->in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
   if (a->recv_total > 0 && !a16(a->expert_rows)) return fail(EPB_INVALID_ARGUMENT, "expert rows must be 16-byte aligned");
   cudaStream_t s = as_stream(stream);
+  if ((phases & 1) && a->dispatch_weights && a->num_tokens > 0) {
+    // combine weights must equal the dispatched ones (ht.py:605-609)
+    const int64_t n = (int64_t)a->num_tokens * g->cfg.top_k;
+    weights_equal_kernel<<<(int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, s>>>(
+        a->weights, a->dispatch_weights, n, g->d_err);
+    EPB_LAUNCH_CHECK();
+  }
   if (phases & 1) {
     // the metadata rows of this round live in the window (parity = round & 1)
     HTCombSend p;
+    p.err = g->d_err;
     p.y = a->expert_rows; p.origin = a->origin;
     p.meta = reinterpret_cast<const int32_t*>(g->window + g->ht.meta +
                                               (uint64_t)(round & 1) * g->ht.N * (g->ht.E + g->ht.N) * 4);
