@@ -40,8 +40,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=128)
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
-    torch.cuda.set_device(0)
-    st = bench.LLStep(1, 0, a.tokens)
+    world, rank = bench.init_dist()
+    st = bench.LLStep(world, rank, a.tokens)
     g = st.g
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     tr_d = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
@@ -52,7 +52,7 @@ def main():
         tr_d.zero_()
         tr_c.zero_()
         flush.zero_()
-        torch.cuda.synchronize()
+        bench.barrier(world)
         h = g.create_handle(st.topk)
         _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(tr_d.data_ptr()))
         h.dispatch([st.X], [st.RECV, st.RECV_SC, st.CNT])
@@ -61,9 +61,11 @@ def main():
         _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(0))
         h.destroy()
         torch.cuda.synchronize()
-        print(f"== rep {rep}")
-        show("dispatch", tr_d, DISP)
-        show("combine", tr_c, COMB)
+        if rank == 0:
+            print(f"== rep {rep} (rank 0 of {world})")
+            show("dispatch", tr_d, DISP)
+            show("combine", tr_c, COMB)
+        bench.barrier(world)
 
 
 if __name__ == "__main__":
