@@ -254,7 +254,7 @@ def capture(step_obj, group, phases: bool, warmup_eager=3):
     return graph, marks
 
 
-def replay_timed(graph, marks, steps, flush, sync_each=False):
+def replay_timed(graph, marks, steps, flush, sync_each=False, align=None):
     """Replay `steps` times back to back, the L2 flushed before each step
     outside the timed events.  Without `sync_each` the host never waits
     between steps (per-step events are recorded around each replay on the
@@ -268,6 +268,8 @@ def replay_timed(graph, marks, steps, flush, sync_each=False):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         for a, b in evs:
             flush.zero_()
+            if align is not None:
+                align()  # device barrier of all ranks, outside the timed events
             a.record()
             graph.replay()
             b.record()
@@ -276,6 +278,8 @@ def replay_timed(graph, marks, steps, flush, sync_each=False):
     total = 0.0
     for _ in range(steps):
         flush.zero_()
+        if align is not None:
+            align()
         graph.replay()
         torch.cuda.synchronize()
         evs = [m[1] for m in marks]
@@ -293,16 +297,17 @@ def run_ll(args, world, rank):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
         flush.zero_()
+        st.g.device_barrier()
         graph.replay()
     barrier(world)
     with ClockSampler(torch.cuda.current_device()) as clk:
         barrier(world)
-        total, _ = replay_timed(graph, marks, args.steps, flush)
+        total, _ = replay_timed(graph, marks, args.steps, flush, align=st.g.device_barrier)
         barrier(world)
     # per-kernel breakdown from the instrumented graph (events between launches)
     nb = max(10, min(args.steps, 100))
     barrier(world)
-    _, phase = replay_timed(graph_b, marks_b, nb, flush, sync_each=True)
+    _, phase = replay_timed(graph_b, marks_b, nb, flush, sync_each=True, align=st.g.device_barrier)
     st.g.check()
     total_max = allreduce_max(total, world)
     per_phase = {n: v / nb * 1000.0 for n, v in phase.items()}  # us
@@ -385,6 +390,7 @@ def run_ht(args, world, rank):
                          torch.randn((tot, H), device=dev).to(torch.bfloat16))
         rt, yt = bufs[tot]
         flush.zero_()
+        g.device_barrier()
         g.trace_phases(marks)
         h.dispatch([X, Wt], [ep.tensor_from_torch(rt, T.TOKENS), CNT])
         g.mark("dispatch:end")
@@ -500,6 +506,7 @@ def main():
         "config": {"workload": "configs[1] LL decode, DeepSeek-V3 shapes", "experts": E, "top_k": K,
                    "hidden": H, "tokens_per_rank": args.tokens, "ranks": world,
                    "parallelism": f"ep{world}", "l2": "flushed (256 MB memset) before every step",
+                   "align": "device barrier of all ranks before each step (untimed)",
                    "graph": "one CUDA graph per step (create_handle+dispatch+combine)"},
         "phase_us": {k: round(v, 2) for k, v in phases.items()},
         "gpu_launches": launches,

@@ -132,6 +132,9 @@ int epb_group_set_timeout(epb_group* g, uint64_t timeout_ns);
 /* diagnostics: with a device buffer of >= grid*16 u64, LL kernels stamp
  * %globaltimer at phase checkpoints (thread 0 of each CTA); NULL disables */
 int epb_group_set_trace(epb_group* g, uint64_t* trace);
+/* device-side barrier over the peer windows (graph-capturable; one tiny
+ * kernel: store epoch to every peer, wait for every peer's epoch) */
+int epb_group_barrier(epb_group* g, void* stream);
 /* reads (and with clear!=0 resets) the device error word; synchronises */
 int epb_group_poll_error(epb_group* g, int clear, int32_t* code);
 int epb_group_destroy(epb_group* g);

@@ -94,6 +94,7 @@ SIGNATURES = {
     "epb_group_set_peers": [_P, ctypes.POINTER(_Q)],
     "epb_group_set_timeout": [_P, _Q],
     "epb_group_set_trace": [_P, _P],
+    "epb_group_barrier": [_P, _P],
     "epb_group_poll_error": [_P, ctypes.c_int, ctypes.POINTER(_I)],
     "epb_group_destroy": [_P],
     "epb_routing_layout": [_P, _P, _I, ctypes.POINTER(Layout), _P],

@@ -188,6 +188,16 @@ class EpGroup:
     def set_timeout(self, seconds: float) -> None:
         _lib.call("epb_group_set_timeout", self._g, int(seconds * 1e9))
 
+    def device_barrier(self) -> None:
+        """Stream-ordered barrier of all ranks over the peer windows (no host
+        sync, capturable in a CUDA graph).  Collective.  Emulated ranks share
+        one stream, so a host barrier already orders them (a spinning kernel
+        per rank on one GPU would wait on kernels queued behind it)."""
+        if not self.fabric.process_mode and self.config.num_ranks > 1:
+            self.fabric.phase(self.rank)
+            return
+        _lib.call("epb_group_barrier", self._g, ctypes.c_void_p(self.stream.cuda_stream))
+
     # -- kernel launches (optionally bracketed by timing marks) -------------
     def trace_phases(self, marks: Optional[list]) -> None:
         """With a list, every kernel launch of this group is preceded by a

@@ -35,6 +35,7 @@ struct LLGeom {
   uint64_t disp_ctr, disp_flag, comb_flag, disp_slot, comb_slot;  // offsets within a parity
   int grid;  // CTAs of every LL launch (kLLGrid)
   uint64_t parity_bytes, window_bytes, logical_bytes;
+  uint64_t barrier;  // [N] u64 device-barrier flags (after both parities)
 };
 
 // HT:
@@ -47,6 +48,7 @@ struct HTGeom {
   int RB, RBp, WBp, HBp, rec_stride, crow_stride;
   uint64_t meta, meta_flag, dflag, cflag, rec, crow;
   uint64_t window_bytes, logical_bytes;
+  uint64_t barrier;  // [N] u64 device-barrier flags
 };
 
 inline int experts_per_rank(int e, int n) { return (e + n - 1) / n; }
@@ -82,7 +84,8 @@ inline void make_ll_geom(const epb_config& c, LLGeom& g) {
   g.disp_slot = a256(g.comb_flag + (uint64_t)g.N * g.grid * 8);
   g.comb_slot = a256(g.disp_slot + (uint64_t)g.n_disp * g.slot_stride);
   g.parity_bytes = a256(g.comb_slot + (uint64_t)g.n_comb * g.comb_stride);
-  g.window_bytes = 2 * g.parity_bytes;
+  g.barrier = 2 * g.parity_bytes;
+  g.window_bytes = a256(g.barrier + (uint64_t)g.N * 8);
   // reference ll_regions (ll.py:58-121)
   const uint64_t ref_slot = (uint64_t)(g.HB + g.RB + g.SB);
   const uint64_t ref_parity = pairs * 8 + (uint64_t)g.E * 8 + g.n_disp * ref_slot +
@@ -106,7 +109,8 @@ inline void make_ht_geom(const epb_config& c, HTGeom& g) {
   g.cflag = g.dflag + g.N * 8;
   g.rec = a256(g.cflag + g.N * 8);
   g.crow = a256(g.rec + (uint64_t)g.N * g.B * g.rec_stride);
-  g.window_bytes = a256(g.crow + (uint64_t)g.B * g.K * g.crow_stride);
+  g.barrier = a256(g.crow + (uint64_t)g.B * g.K * g.crow_stride);
+  g.window_bytes = a256(g.barrier + (uint64_t)g.N * 8);
   // reference ht_regions (ht.py:78-174)
   const int nodes = c.num_ranks / c.ranks_per_node;
   const uint64_t record = 8 + 4 * c.top_k + 4 * c.top_k + (uint64_t)g.RB +

@@ -9,6 +9,7 @@
 
 #include <string>
 
+#include "common.cuh"
 #include "internal.h"
 
 namespace epb {
@@ -55,11 +56,46 @@ static int validate_config(const epb_config* c) {
   return EPB_OK;
 }
 
+// Device-side barrier over the peer windows: every rank stores the epoch in
+// slot [rank] of every peer's barrier array, then waits until all N slots of
+// its own array show it.  Used to align ranks outside timed regions and as a
+// graph-capturable alternative to a host barrier.
+__global__ void group_barrier_kernel(const uint64_t* peers, uint64_t off, int n, int rank, uint32_t* epoch_ctr,
+                                     int* err, uint64_t timeout_ns, int sys) {
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) {
+    s_epoch = *reinterpret_cast<volatile uint32_t*>(epoch_ctr) + 1;
+    *epoch_ctr = s_epoch;
+  }
+  __syncthreads();
+  const uint32_t ep = s_epoch;
+  if ((int)threadIdx.x < n) {
+    uint64_t* slot = reinterpret_cast<uint64_t*>(peers[threadIdx.x] + off) + rank;
+    if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"((uint64_t)ep) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(slot), "l"((uint64_t)ep) : "memory");
+    const uint64_t* mine = reinterpret_cast<const uint64_t*>(peers[rank] + off) + threadIdx.x;
+    uint64_t v;
+    wait_tag(mine, ep, 0, 0xFFFFFFFFu, timeout_ns, err, &v);
+  }
+}
+
 }  // namespace epb
 
 using namespace epb;
 
 extern "C" {
+
+int epb_group_barrier(epb_group* g, void* stream) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  if (!g->peers_ready) return fail(EPB_HANDLE_STATE_ERROR, "peer windows not mapped");
+  const uint64_t off = g->cfg.algorithm == EPB_LL ? g->ll.barrier : g->ht.barrier;
+  group_barrier_kernel<<<1, 64, 0, as_stream(stream)>>>(g->d_peers, off, g->cfg.num_ranks, g->rank,
+                                                         reinterpret_cast<uint32_t*>(g->d_scratch) + 2, g->d_err,
+                                                         g->timeout_ns, g->sys_scope ? 1 : 0);
+  EPB_LAUNCH_CHECK();
+  return EPB_OK;
+}
+
 
 int epb_version(void) { return 1; }
 
