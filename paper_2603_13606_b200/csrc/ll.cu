@@ -713,6 +713,17 @@ int sm_count() {
   return n;
 }
 
+// EPB_COOP=0 launches the fused kernels without the cooperative attribute
+// (co-residency then rests on grid <= SMs x occupancy, checked below)
+bool coop_attr_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EPB_COOP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <typename Params>
 cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const Params& p, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -725,6 +736,10 @@ cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm * sm_count() < grid) return cudaErrorCooperativeLaunchTooLarge;
+    if (!coop_attr_enabled()) {
+      kern<<<grid, kThreads, smem, s>>>(p);
+      return cudaGetLastError();
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
