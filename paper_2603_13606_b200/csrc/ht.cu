@@ -165,6 +165,41 @@ struct HTDisp {
   uint32_t tag;
 };
 
+constexpr int kFlush = 4;  // sender CTAs publish progress every kFlush tokens
+
+// dispatch flag word: (tag << 40) | (tokens of the source << 20) | tokens done by the CTA
+EPB_DEV void ht_publish_progress(const HTDisp& p, int c, int done) {
+  if ((int)threadIdx.x < p.g.N && (int)threadIdx.x != p.rank) {
+    fence_sys();
+    uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, threadIdx.x) + p.g.dflag) +
+                     (int64_t)p.rank * kHTSendCTAs + c;
+    st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 40) | ((uint64_t)p.b << 20) | (uint64_t)done);
+  }
+}
+
+// wait until sender CTA c of this source has published this round and either
+// advanced past `processed` or finished; backs off so the spinning receivers
+// leave the memory system to the incoming records.  ~0 on timeout / error.
+EPB_DEV uint64_t ht_wait_progress(const uint64_t* f, uint32_t tag, int c, int processed, uint64_t timeout_ns,
+                                  int* err) {
+  uint64_t start = 0;
+  for (int spins = 0;; ++spins) {
+    const uint64_t v = ld_acquire_sys(f);
+    if ((uint32_t)(v >> 40) == tag) {
+      const int bs = (int)((v >> 20) & 0xFFFFF), done = (int)(v & 0xFFFFF);
+      const int n_c = c < bs ? (bs - c + kHTSendCTAs - 1) / kHTSendCTAs : 0;
+      if (done > processed || done >= n_c) return v;
+    }
+    if (*(volatile int*)err != 0) return ~0ull;
+    if (spins == 0) start = globaltimer();
+    else if ((spins & 63) == 0 && globaltimer() - start > timeout_ns) {
+      atomicCAS(err, 0, EPB_TRANSPORT_CLOSED);
+      return ~0ull;
+    }
+    __nanosleep(200);
+  }
+}
+
 // K5b: one cooperative launch, two roles.
 //  * sender CTA c (< kHTSendCTAs) owns tokens t = c, c + kHTSendCTAs, ...;
 //    each goes once to every remote rank it touches, into that rank's record
@@ -217,6 +252,11 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_kernel(HTDisp p) {
       for (int i = 0; i < kTB; ++i) {
         const int t = base + i * G;
         if (t >= p.b) break;
+        if (i > 0 && (i & (kFlush - 1)) == 0) {
+          // progress: tokens [0, done) of this CTA are complete at every destination
+          __syncthreads();
+          ht_publish_progress(p, c0, (base - c0) / G + i);
+        }
         const int64_t slot = (int64_t)me * B + t;
         // record: [row][K weights][tag, t, K, ids[K], positions[K]]
         const int words = K + 3 + 2 * K;
@@ -263,12 +303,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_kernel(HTDisp p) {
       }
     }
     __syncthreads();
-    if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
-      fence_sys();
-      uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, threadIdx.x) + g.dflag) +
-                       (int64_t)me * kHTSendCTAs + c0;
-      st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | (uint32_t)p.b);
-    }
+    ht_publish_progress(p, c0, c0 < p.b ? (p.b - c0 + G - 1) / G : 0);
     return;
   }
   if (!sender && (p.phases & 2)) {
@@ -278,18 +313,22 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_kernel(HTDisp p) {
     const int lo = me * L, hi = min(lo + L, g.E);
     const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
     constexpr int NCH = 0;  (void)NCH;
-    // items: (sender CTA c, remote src) in c-major order
+    // items: (sender CTA c, remote src) in c-major order; each is consumed
+    // in the increments its sender publishes
     for (int item = rw; item < kHTSendCTAs * N; item += nrw) {
       const int c = item / N, s = item - c * N;
       if (s == me) continue;
+      const uint64_t* flag = &flags[(int64_t)s * kHTSendCTAs + c];
+      int processed = 0;
+      for (;;) {
       uint64_t v = 0;
-      if (lane == 0) {
-        if (!wait_tag(&flags[(int64_t)s * kHTSendCTAs + c], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) v = ~0ull;
-      }
+      if (lane == 0) v = ht_wait_progress(flag, p.tag, c, processed, p.timeout_ns, p.err);
       v = __shfl_sync(0xffffffffu, v, 0);
       if (v == ~0ull) return;
-      const int bs = (int)(v & 0xFFFFFFFFu);  // tokens of source s
-      for (int t = c; t < bs; t += kHTSendCTAs) {
+      const int bs = (int)((v >> 20) & 0xFFFFF);  // tokens of source s
+      const int done = (int)(v & 0xFFFFF);
+      const int n_c = c < bs ? (bs - c + kHTSendCTAs - 1) / kHTSendCTAs : 0;
+      for (int t = c + processed * kHTSendCTAs; t < min(bs, c + done * kHTSendCTAs); t += kHTSendCTAs) {
         const uint8_t* rec = p.win + g.rec + ((int64_t)s * B + t) * g.rec_stride;
         const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
         if (hdr[0] != p.tag) continue;  // t does not touch this rank this round
@@ -332,6 +371,9 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_kernel(HTDisp p) {
             for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
           }
         }
+      }
+      processed = done;
+      if (processed >= n_c) break;
       }
     }
   }
@@ -621,7 +663,7 @@ using namespace epb;
 
 namespace {
 
-uint32_t ht_tag(uint32_t round) { return (round % 0xFFFFFFFu) + 1u; }
+uint32_t ht_tag(uint32_t round) { return (round % 0xFFFFFFu) + 1u; }  // fits the 24-bit flag field
 
 int hsm_count() {
   static int n = 0;
