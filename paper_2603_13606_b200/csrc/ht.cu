@@ -307,32 +307,34 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_kernel(HTDisp p) {
     return;
   }
   if (!sender && (p.phases & 2)) {
+    // receiver CTAs: items = (sender CTA c, remote src), c-major; one CTA per
+    // item, its warps split the (token, k) copies of every published step
+    __shared__ uint64_t s_v;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int rw = ((int)blockIdx.x - kHTSendCTAs) * nw + warp;  // receiver warp id
-    const int nrw = ((int)gridDim.x - kHTSendCTAs) * nw;
+    const int nrc = (int)gridDim.x - kHTSendCTAs;
     const int lo = me * L, hi = min(lo + L, g.E);
     const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
-    constexpr int NCH = 0;  (void)NCH;
-    // items: (sender CTA c, remote src) in c-major order; each is consumed
-    // in the increments its sender publishes
-    for (int item = rw; item < kHTSendCTAs * N; item += nrw) {
+    for (int item = (int)blockIdx.x - kHTSendCTAs; item < kHTSendCTAs * N; item += nrc) {
       const int c = item / N, s = item - c * N;
       if (s == me) continue;
       const uint64_t* flag = &flags[(int64_t)s * kHTSendCTAs + c];
       int processed = 0;
       for (;;) {
-      uint64_t v = 0;
-      if (lane == 0) v = ht_wait_progress(flag, p.tag, c, processed, p.timeout_ns, p.err);
-      v = __shfl_sync(0xffffffffu, v, 0);
-      if (v == ~0ull) return;
-      const int bs = (int)((v >> 20) & 0xFFFFF);  // tokens of source s
-      const int done = (int)(v & 0xFFFFF);
-      const int n_c = c < bs ? (bs - c + kHTSendCTAs - 1) / kHTSendCTAs : 0;
-      for (int t = c + processed * kHTSendCTAs; t < min(bs, c + done * kHTSendCTAs); t += kHTSendCTAs) {
-        const uint8_t* rec = p.win + g.rec + ((int64_t)s * B + t) * g.rec_stride;
-        const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
-        if (hdr[0] != p.tag) continue;  // t does not touch this rank this round
-        for (int k = 0; k < K; ++k) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_v = ht_wait_progress(flag, p.tag, c, processed, p.timeout_ns, p.err);
+        __syncthreads();
+        const uint64_t v = s_v;
+        if (v == ~0ull) return;
+        const int bs = (int)((v >> 20) & 0xFFFFF);  // tokens of source s
+        const int done = (int)(v & 0xFFFFF);
+        const int n_c = c < bs ? (bs - c + kHTSendCTAs - 1) / kHTSendCTAs : 0;
+        const int ntok = max(0, min(done, n_c) - processed);
+        for (int f = warp; f < ntok * K; f += nw) {
+          const int i = processed + f / K, k = f - (f / K) * K;
+          const int t = c + i * kHTSendCTAs;
+          const uint8_t* rec = p.win + g.rec + ((int64_t)s * B + t) * g.rec_stride;
+          const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
+          if (hdr[0] != p.tag) continue;  // t does not touch this rank this round
           const int e = (int)hdr[3 + k];
           if (e < lo || e >= hi) continue;
           const int64_t pos = hdr[3 + K + k];
@@ -371,9 +373,8 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_kernel(HTDisp p) {
             for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
           }
         }
-      }
-      processed = done;
-      if (processed >= n_c) break;
+        processed = max(processed, min(done, n_c));
+        if (processed >= n_c) break;
       }
     }
   }
