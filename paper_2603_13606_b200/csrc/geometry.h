@@ -13,10 +13,6 @@
 namespace epb {
 
 constexpr int kMaxRanksHost = 64;
-// HT dispatch: one cooperative launch of kHTSendCTAs sender CTAs (token
-// t goes with CTA t % kHTSendCTAs) plus kHTRecvCTAs receiver CTAs
-constexpr int kHTSendCTAs = 192;
-constexpr int kHTRecvCTAs = 104;
 // LL kernels run a fixed, rank-independent grid (one 512-thread CTA per B200
 // SM, co-resident for the cooperative fused launch) so every rank knows how
 // many per-CTA flags each peer publishes
@@ -104,14 +100,14 @@ inline void make_ht_geom(const epb_config& c, HTGeom& g) {
   g.RB = c.hidden * width_of(c.token_dtype);
   g.RBp = (int)a16(g.RB);
   g.WBp = (int)a16(4 * c.top_k);
-  g.HBp = (int)a16(12 + 8 * c.top_k);  // tag, t, kcount, K ids, K output positions
+  g.HBp = (int)a16(8 + 8 * c.top_k);
   g.rec_stride = g.RBp + g.WBp + g.HBp;
   g.crow_stride = (int)a16(4 * (size_t)c.hidden);
   g.meta = 0;
   g.meta_flag = a256((uint64_t)2 * g.N * (g.E + g.N) * 4);
-  g.dflag = g.meta_flag + 2 * g.N * 8;               // [N src][kHTSendCTAs]
-  g.cflag = g.dflag + (uint64_t)g.N * kHTSendCTAs * 8;  // [N src]
-  g.rec = a256(g.cflag + g.N * 8);                     // [N src][B token] records
+  g.dflag = g.meta_flag + 2 * g.N * 8;
+  g.cflag = g.dflag + g.N * 8;
+  g.rec = a256(g.cflag + g.N * 8);
   g.crow = a256(g.rec + (uint64_t)g.N * g.B * g.rec_stride);
   g.barrier = a256(g.crow + (uint64_t)g.B * g.K * g.crow_stride);
   g.window_bytes = a256(g.barrier + (uint64_t)g.N * 8);

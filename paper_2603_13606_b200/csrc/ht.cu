@@ -146,236 +146,226 @@ __global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
 // ---------------------------------------------------------------------------
 // K5b: dispatch
 // ---------------------------------------------------------------------------
-struct HTDisp {
+struct HTSend {
   const void* x;
   const float* w;
   const int64_t* topk;
+  const int32_t* q;
   const int32_t* tok_rank;
   const int32_t* tok_slot;
   const int32_t* offsets;  // [E, N]
   const uint64_t* peers;
-  const uint8_t* win;
-  void* out;               // own sorted output
+  void* out;               // own sorted output (self rows land here directly)
   int32_t* origin;
   float* origin_w;
-  int* err;
+  int* done;
   HTGeom g;
-  uint64_t timeout_ns;
-  int b, rank, phases;
+  int b, rank;
   uint32_t tag;
 };
 
-constexpr int kFlush = 4;  // sender CTAs publish progress every kFlush tokens
-
-// dispatch flag word: (tag << 40) | (tokens of the source << 20) | tokens done by the CTA
-EPB_DEV void ht_publish_progress(const HTDisp& p, int c, int done) {
-  if ((int)threadIdx.x < p.g.N && (int)threadIdx.x != p.rank) {
-    fence_sys();
-    uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, threadIdx.x) + p.g.dflag) +
-                     (int64_t)p.rank * kHTSendCTAs + c;
-    st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 40) | ((uint64_t)p.b << 20) | (uint64_t)done);
-  }
+EPB_DEV void ht_publish_records(const HTSend& p, int d) {
+  uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, d) + p.g.dflag) + p.rank;
+  st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | (uint32_t)p.q[d]);
 }
 
-// wait until sender CTA c of this source has published this round and either
-// advanced past `processed` or finished; backs off so the spinning receivers
-// leave the memory system to the incoming records.  ~0 on timeout / error.
-EPB_DEV uint64_t ht_wait_progress(const uint64_t* f, uint32_t tag, int c, int processed, uint64_t timeout_ns,
-                                  int* err) {
-  uint64_t start = 0;
-  for (int spins = 0;; ++spins) {
-    const uint64_t v = ld_acquire_sys(f);
-    if ((uint32_t)(v >> 40) == tag) {
-      const int bs = (int)((v >> 20) & 0xFFFFF), done = (int)(v & 0xFFFFF);
-      const int n_c = c < bs ? (bs - c + kHTSendCTAs - 1) / kHTSendCTAs : 0;
-      if (done > processed || done >= n_c) return v;
-    }
-    if (*(volatile int*)err != 0) return ~0ull;
-    if (spins == 0) start = globaltimer();
-    else if ((spins & 63) == 0 && globaltimer() - start > timeout_ns) {
-      atomicCAS(err, 0, EPB_TRANSPORT_CLOSED);
-      return ~0ull;
-    }
-    __nanosleep(200);
-  }
-}
-
-// K5b: one cooperative launch, two roles.
-//  * sender CTA c (< kHTSendCTAs) owns tokens t = c, c + kHTSendCTAs, ...;
-//    each goes once to every remote rank it touches, into that rank's record
-//    slot [src][t] (header carries the round tag), and straight into this
-//    rank's own sorted output for its local experts.  Afterwards the CTA
-//    fences and raises flag [src][c] at every remote rank.
-//  * receiver CTAs walk the (src, sender CTA) pairs: once a pair's flag is up
-//    its records are scattered to their sorted positions while other pairs
-//    are still in flight, so the HBM scatter overlaps the NVLink transfer.
 template <int XT, int WT, int OT>
-__global__ void __launch_bounds__(kHTThreads) ht_dispatch_kernel(HTDisp p) {
+__global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) {
+  // a CTA owns tokens blockIdx.x + i*gridDim.x; their routing metadata is
+  // gathered for kTB tokens at once (one latency for the batch), then rows
+  // move token by token
   constexpr int kTB = 16;
+  __shared__ int s_e[kTB][kMaxTopK], s_pos[kTB][kMaxTopK];
+  __shared__ float s_w[kTB][kMaxTopK];
+  __shared__ int s_j[kTB][kMaxRanks];
+  __shared__ int s_cnt[kMaxRanks];
   const HTGeom& g = p.g;
-  const int K = g.K, N = g.N, H = g.H, L = g.L, B = g.B;
+  const int K = g.K, N = g.N, H = g.H, L = g.L, G = gridDim.x;
   const int me = p.rank;
   constexpr int EPC = Elems<WT>::n;
   constexpr int XW = XT == EPB_F32 ? 4 : 2;
   constexpr int OW = OT == EPB_F32 ? 4 : 2;
-  const bool sender = (int)blockIdx.x < kHTSendCTAs;
-  if (sender && (p.phases & 1)) {
-    __shared__ int s_e[kTB][kMaxTopK], s_pos[kTB][kMaxTopK];
-    __shared__ float s_w[kTB][kMaxTopK];
-    __shared__ int s_go[kTB][kMaxRanks];
-    const int c0 = blockIdx.x;
-    const int G = kHTSendCTAs;
-    for (int base = c0; base < p.b; base += G * kTB) {
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < kTB * K; idx += blockDim.x) {
-        const int i = idx / K, k = idx - i * K, t = base + i * G;
-        if (t >= p.b) continue;
-        const int e = (int)p.topk[(int64_t)t * K + k];
-        const int pos = p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k];
-        const float wk = p.w[(int64_t)t * K + k];
-        s_e[i][k] = e;
-        s_pos[i][k] = pos;
-        s_w[i][k] = wk;
-        if (e / L == me) {
-          p.origin[(int64_t)pos * 4 + 0] = e;
-          p.origin[(int64_t)pos * 4 + 1] = me;
-          p.origin[(int64_t)pos * 4 + 2] = t;
-          p.origin[(int64_t)pos * 4 + 3] = k;
-          p.origin_w[pos] = wk;
-        }
+  const int64_t rec0 = (int64_t)me * g.B;
+  if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
+  for (int base = blockIdx.x; base < p.b; base += G * kTB) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kTB * K; idx += blockDim.x) {
+      const int i = idx / K, k = idx - i * K, t = base + i * G;
+      if (t >= p.b) continue;
+      const int e = (int)p.topk[(int64_t)t * K + k];
+      const int pos = p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k];
+      const float wk = p.w[(int64_t)t * K + k];
+      s_e[i][k] = e;
+      s_pos[i][k] = pos;
+      s_w[i][k] = wk;
+      if (e / L == me) {
+        p.origin[(int64_t)pos * 4 + 0] = e;
+        p.origin[(int64_t)pos * 4 + 1] = me;
+        p.origin[(int64_t)pos * 4 + 2] = t;
+        p.origin[(int64_t)pos * 4 + 3] = k;
+        p.origin_w[pos] = wk;
       }
-      for (int idx = threadIdx.x; idx < kTB * N; idx += blockDim.x) {
-        const int i = idx / N, d = idx - i * N, t = base + i * G;
-        s_go[i][d] = (t < p.b && d != me && p.tok_slot[(int64_t)t * N + d] >= 0) ? 1 : 0;
-      }
-      __syncthreads();
-      for (int i = 0; i < kTB; ++i) {
-        const int t = base + i * G;
-        if (t >= p.b) break;
-        if (i > 0 && (i & (kFlush - 1)) == 0) {
-          // progress: tokens [0, done) of this CTA are complete at every destination
-          __syncthreads();
-          ht_publish_progress(p, c0, (base - c0) / G + i);
-        }
-        const int64_t slot = (int64_t)me * B + t;
-        // record: [row][K weights][tag, t, K, ids[K], positions[K]]
-        const int words = K + 3 + 2 * K;
-        for (int idx = threadIdx.x; idx < N * words; idx += blockDim.x) {
-          const int d = idx / words, wd = idx - d * words;
-          if (!s_go[i][d]) continue;
-          uint8_t* rec = hpeer(p.peers, d) + g.rec + slot * g.rec_stride;
-          if (wd < K) {
-            reinterpret_cast<float*>(rec + g.RBp)[wd] = s_w[i][wd];
-          } else {
-            const int h = wd - K;
-            const uint32_t v = h == 0 ? p.tag : h == 1 ? (uint32_t)t : h == 2 ? (uint32_t)K
-                               : h < 3 + K ? (uint32_t)s_e[i][h - 3] : (uint32_t)s_pos[i][h - 3 - K];
-            reinterpret_cast<uint32_t*>(rec + g.RBp + g.WBp)[h] = v;
-          }
-        }
-        const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
-        if ((H & 15) == 0) {
-          for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
-            float f[EPC];
-            load_elems_vec<XT, EPC>(xrow, (int64_t)c * EPC, f);
-            const int4 v = pack16<WT>(f);
-            for (int d = 0; d < N; ++d)
-              if (s_go[i][d]) st_na_v4(hpeer(p.peers, d) + g.rec + slot * g.rec_stride + (int64_t)c * 16, v);
-            float fw[EPC];
-            unpack16<WT>(v, fw);  // the wire image, exactly what a record carries
-            for (int k = 0; k < K; ++k)
-              if (s_e[i][k] / L == me)
-                store_f32_chunk<OT, EPC>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW,
-                                         (int64_t)c * EPC, fw);
-          }
+    }
+    for (int idx = threadIdx.x; idx < kTB * N; idx += blockDim.x) {
+      const int i = idx / N, d = idx - i * N, t = base + i * G;
+      int j = -1;
+      if (t < p.b && d != me) j = p.tok_slot[(int64_t)t * N + d];
+      s_j[i][d] = j;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < N)
+      for (int i = 0; i < kTB; ++i) s_cnt[threadIdx.x] += s_j[i][threadIdx.x] >= 0;
+    for (int i = 0; i < kTB; ++i) {
+      const int t = base + i * G;
+      if (t >= p.b) break;
+      // record header (reference fields + output positions) and weights
+      const int words = K + 2 + 2 * K;
+      for (int idx = threadIdx.x; idx < N * words; idx += blockDim.x) {
+        const int d = idx / words, wd = idx - d * words;
+        if (s_j[i][d] < 0) continue;
+        uint8_t* rec = hpeer(p.peers, d) + g.rec + (rec0 + s_j[i][d]) * g.rec_stride;
+        if (wd < K) {
+          reinterpret_cast<float*>(rec + g.RBp)[wd] = s_w[i][wd];
         } else {
-          for (int el = threadIdx.x; el < H; el += blockDim.x) {
-            const float f = load_elem(xrow, XT, el);
-            for (int d = 0; d < N; ++d)
-              if (s_go[i][d]) store_elem(hpeer(p.peers, d) + g.rec + slot * g.rec_stride, WT, el, f);
-            const float fw = WT == EPB_F32 ? f
-                             : (WT == EPB_BF16 ? bf16_widen(bf16_bits_rne(f)) : f16_widen(f16_bits_rne(f)));
-            for (int k = 0; k < K; ++k)
-              if (s_e[i][k] / L == me)
-                store_elem(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW, OT, el, fw);
+          const int h = wd - K;
+          const uint32_t v = h == 0 ? (uint32_t)t : h == 1 ? (uint32_t)K
+                             : h < 2 + K ? (uint32_t)s_e[i][h - 2] : (uint32_t)s_pos[i][h - 2 - K];
+          reinterpret_cast<uint32_t*>(rec + g.RBp + g.WBp)[h] = v;
+        }
+      }
+      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
+      if ((H & 15) == 0) {
+        for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
+          float f[EPC];
+          load_elems_vec<XT, EPC>(xrow, (int64_t)c * EPC, f);
+          const int4 v = pack16<WT>(f);
+          for (int d = 0; d < N; ++d) {
+            const int j = s_j[i][d];
+            if (j >= 0) st_na_v4(hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride + (int64_t)c * 16, v);
           }
+          float fw[EPC];
+          unpack16<WT>(v, fw);  // the wire image, exactly what a record carries
+          for (int k = 0; k < K; ++k)
+            if (s_e[i][k] / L == me)
+              store_f32_chunk<OT, EPC>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW,
+                                       (int64_t)c * EPC, fw);
+        }
+      } else {
+        for (int el = threadIdx.x; el < H; el += blockDim.x) {
+          const float f = load_elem(xrow, XT, el);
+          for (int d = 0; d < N; ++d) {
+            const int j = s_j[i][d];
+            if (j >= 0) store_elem(hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride, WT, el, f);
+          }
+          const float fw = WT == EPB_F32 ? f : (WT == EPB_BF16 ? bf16_widen(bf16_bits_rne(f)) : f16_widen(f16_bits_rne(f)));
+          for (int k = 0; k < K; ++k)
+            if (s_e[i][k] / L == me)
+              store_elem(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW, OT, el, fw);
         }
       }
     }
-    __syncthreads();
-    ht_publish_progress(p, c0, c0 < p.b ? (p.b - c0 + G - 1) / G : 0);
-    return;
   }
-  if (!sender && (p.phases & 2)) {
-    // receiver CTAs: items = (sender CTA c, remote src), c-major; one CTA per
-    // item, its warps split the (token, k) copies of every published step
-    __shared__ uint64_t s_v;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int nrc = (int)gridDim.x - kHTSendCTAs;
-    const int lo = me * L, hi = min(lo + L, g.E);
-    const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
-    for (int item = (int)blockIdx.x - kHTSendCTAs; item < kHTSendCTAs * N; item += nrc) {
-      const int c = item / N, s = item - c * N;
-      if (s == me) continue;
-      const uint64_t* flag = &flags[(int64_t)s * kHTSendCTAs + c];
-      int processed = 0;
-      for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_v = ht_wait_progress(flag, p.tag, c, processed, p.timeout_ns, p.err);
-        __syncthreads();
-        const uint64_t v = s_v;
-        if (v == ~0ull) return;
-        const int bs = (int)((v >> 20) & 0xFFFFF);  // tokens of source s
-        const int done = (int)(v & 0xFFFFF);
-        const int n_c = c < bs ? (bs - c + kHTSendCTAs - 1) / kHTSendCTAs : 0;
-        const int ntok = max(0, min(done, n_c) - processed);
-        for (int f = warp; f < ntok * K; f += nw) {
-          const int i = processed + f / K, k = f - (f / K) * K;
-          const int t = c + i * kHTSendCTAs;
-          const uint8_t* rec = p.win + g.rec + ((int64_t)s * B + t) * g.rec_stride;
-          const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
-          if (hdr[0] != p.tag) continue;  // t does not touch this rank this round
-          const int e = (int)hdr[3 + k];
-          if (e < lo || e >= hi) continue;
-          const int64_t pos = hdr[3 + K + k];
-          if (lane == 0) {
-            p.origin[pos * 4 + 0] = e;
-            p.origin[pos * 4 + 1] = s;
-            p.origin[pos * 4 + 2] = t;
-            p.origin[pos * 4 + 3] = k;
-            p.origin_w[pos] = reinterpret_cast<const float*>(rec + g.RBp)[k];
-          }
-          uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + pos * H * OW;
-          if ((H & 15) == 0) {
-            const int nch = H / EPC;
-            for (int bb = 0; bb < nch; bb += 32 * kHU) {
-              int4 q[kHU];
+  __syncthreads();
+  if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
+    const int d = threadIdx.x;
+    const int c = s_cnt[d];
+    if (c > 0) {
+      fence_sys();
+      const int old = atomicAdd(&p.done[d], c);
+      if (old + c == p.q[d]) {
+        p.done[d] = 0;
+        fence_sys();
+        ht_publish_records(p, d);
+      }
+    } else if (blockIdx.x == 0 && p.q[d] == 0) {
+      ht_publish_records(p, d);
+    }
+  }
+}
+
+struct HTRecv {
+  void* out;
+  int32_t* origin;
+  float* origin_w;
+  const uint8_t* win;
+  int* err;
+  HTGeom g;
+  uint64_t timeout_ns;
+  int rank;
+  uint32_t tag;
+};
+
+template <int WT, int OT>
+__global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) {
+  __shared__ int s_pre[kMaxRanks + 1], s_q[kMaxRanks];
+  __shared__ int s_fail;
+  const HTGeom& g = p.g;
+  const int N = g.N, K = g.K, H = g.H, L = g.L;
+  const int me = p.rank;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
+  for (int s = threadIdx.x; s < N; s += blockDim.x) {
+    uint64_t v = 0;
+    if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    s_q[s] = s == me ? 0 : (int)(v & 0xFFFFFFFFu);  // own rows were placed by the sender
+  }
+  __syncthreads();
+  if (s_fail) return;
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int s = 0; s < N; ++s) { s_pre[s] = run; run += s_q[s]; }
+    s_pre[N] = run;
+  }
+  __syncthreads();
+  const int items = s_pre[N] * K;  // (record, k); non-local k exit at once
+  const int lo = me * L, hi = min(lo + L, g.E);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int OW = OT == EPB_F32 ? 4 : 2;
+  constexpr int EPC = Elems<WT>::n;
+  for (int f = warp * gridDim.x + blockIdx.x; f < items; f += gridDim.x * nw) {
+    const int rj = f / K, k = f - rj * K;
+    int s = 0;
+    while (s_pre[s + 1] <= rj) ++s;
+    const int j = rj - s_pre[s];
+    const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
+    const int e = (int)hdr[2 + k];
+    if (e < lo || e >= hi) continue;
+    const int64_t pos = hdr[2 + K + k];
+    if (lane == 0) {
+      p.origin[pos * 4 + 0] = e;
+      p.origin[pos * 4 + 1] = s;
+      p.origin[pos * 4 + 2] = (int32_t)hdr[0];
+      p.origin[pos * 4 + 3] = k;
+      p.origin_w[pos] = reinterpret_cast<const float*>(rec + g.RBp)[k];
+    }
+    uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + pos * H * OW;
+    if ((H & 15) == 0) {
+      const int nch = H / EPC;
+      for (int base = 0; base < nch; base += 32 * kHU) {
+        int4 v[kHU];
 #pragma unroll
-              for (int u = 0; u < kHU; ++u) {
-                const int cc = bb + u * 32 + lane;
-                if (cc < nch) q[u] = ld_plain_v4(rec + (int64_t)cc * 16);
-              }
+        for (int u = 0; u < kHU; ++u) {
+          const int c = base + u * 32 + lane;
+          if (c < nch) v[u] = ld_plain_v4(rec + (int64_t)c * 16);
+        }
 #pragma unroll
-              for (int u = 0; u < kHU; ++u) {
-                const int cc = bb + u * 32 + lane;
-                if (cc < nch) {
-                  if constexpr (OT == WT) {
-                    st_plain_v4(orow + (int64_t)cc * 16, q[u]);
-                  } else {
-                    float fv[EPC];
-                    unpack16<WT>(q[u], fv);
-                    store_f32_chunk<OT, EPC>(orow, (int64_t)cc * EPC, fv);
-                  }
-                }
-              }
+        for (int u = 0; u < kHU; ++u) {
+          const int c = base + u * 32 + lane;
+          if (c < nch) {
+            if constexpr (OT == WT) {
+              st_plain_v4(orow + (int64_t)c * 16, v[u]);
+            } else {
+              float fv[EPC];
+              unpack16<WT>(v[u], fv);
+              store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, fv);
             }
-          } else {
-            for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
           }
         }
-        processed = max(processed, min(done, n_c));
-        if (processed >= n_c) break;
       }
+    } else {
+      for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
     }
   }
 }
@@ -664,7 +654,7 @@ using namespace epb;
 
 namespace {
 
-uint32_t ht_tag(uint32_t round) { return (round % 0xFFFFFFu) + 1u; }  // fits the 24-bit flag field
+uint32_t ht_tag(uint32_t round) { return (round % 0xFFFFFFFu) + 1u; }
 
 int hsm_count() {
   static int n = 0;
@@ -685,46 +675,31 @@ int check_ht(epb_group* g, int phases) {
   return EPB_OK;
 }
 
-int ht_coop_grid(void (*kern)(HTDisp)) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHTThreads, 0);
-  return per_sm * hsm_count();
-}
-
 template <int XT, int WT, int OT>
-cudaError_t launch_hdisp(const HTDisp& p, cudaStream_t s) {
-  auto kern = ht_dispatch_kernel<XT, WT, OT>;
-  const int grid = kHTSendCTAs + kHTRecvCTAs;
-  if (p.phases == 3) {
-    // sender and receiver CTAs wait on each other's flags: all co-resident
-    if (ht_coop_grid(kern) < grid) return cudaErrorCooperativeLaunchTooLarge;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kHTThreads);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, p);
-  }
-  kern<<<grid, kHTThreads, 0, s>>>(p);
+cudaError_t launch_hsend(const HTSend& p, cudaStream_t s) {
+  const int grid = std::max(1, std::min(p.b, 2 * hsm_count()));
+  ht_dispatch_send_kernel<XT, WT, OT><<<grid, kHTThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 template <int XT, int WT>
-cudaError_t launch_hdisp_o(const HTDisp& p, int out_dtype, cudaStream_t s) {
-  return out_dtype == EPB_F32 ? launch_hdisp<XT, WT, EPB_F32>(p, s) : launch_hdisp<XT, WT, WT>(p, s);
+cudaError_t launch_hsend_o(const HTSend& p, int out_dtype, cudaStream_t s) {
+  return out_dtype == EPB_F32 ? launch_hsend<XT, WT, EPB_F32>(p, s) : launch_hsend<XT, WT, WT>(p, s);
 }
 
 template <int XT>
-cudaError_t launch_hdisp_x(const HTDisp& p, int out_dtype, cudaStream_t s) {
+cudaError_t launch_hsend_x(const HTSend& p, int out_dtype, cudaStream_t s) {
   switch (p.g.wire) {
-    case EPB_F32: return launch_hdisp<XT, EPB_F32, EPB_F32>(p, s);
-    case EPB_BF16: return launch_hdisp_o<XT, EPB_BF16>(p, out_dtype, s);
-    default: return launch_hdisp_o<XT, EPB_F16>(p, out_dtype, s);
+    case EPB_F32: return launch_hsend<XT, EPB_F32, EPB_F32>(p, s);
+    case EPB_BF16: return launch_hsend_o<XT, EPB_BF16>(p, out_dtype, s);
+    default: return launch_hsend_o<XT, EPB_F16>(p, out_dtype, s);
   }
+}
+
+template <int WT, int OT>
+cudaError_t launch_hrecv(const HTRecv& p, cudaStream_t s) {
+  ht_dispatch_recv_kernel<WT, OT><<<2 * hsm_count(), kHTThreads, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -764,21 +739,38 @@ int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases, const epb_ht_d
   if (a->out_dtype != EPB_F32 && a->out_dtype != wire)
     return fail(EPB_TAG_MISMATCH, "dispatch output must be f32 or the wire dtype");
   if (!a16(a->out)) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
-  if ((phases & 1) && a->num_tokens > 0 && !a16(a->x)) return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
-  HTDisp p;
-  p.x = a->x; p.w = a->weights; p.topk = a->topk_idx; p.tok_rank = a->tok_rank; p.tok_slot = a->tok_slot;
-  p.offsets = a->offsets; p.peers = g->d_peers; p.win = g->window; p.out = a->out; p.origin = a->origin;
-  p.origin_w = a->origin_w; p.err = g->d_err; p.g = g->ht; p.timeout_ns = g->timeout_ns; p.b = a->num_tokens;
-  p.rank = g->rank; p.phases = phases; p.tag = ht_tag(round);
   cudaStream_t s = as_stream(stream);
-  cudaError_t e;
-  switch (a->x_dtype) {
-    case EPB_F32: e = launch_hdisp_x<EPB_F32>(p, a->out_dtype, s); break;
-    case EPB_BF16: e = launch_hdisp_x<EPB_BF16>(p, a->out_dtype, s); break;
-    case EPB_F16: e = launch_hdisp_x<EPB_F16>(p, a->out_dtype, s); break;
-    default: return fail(EPB_TAG_MISMATCH, "HT dispatch input must be f32/bf16/f16");
+  if (phases & 1) {
+    if (a->num_tokens > 0 && !a16(a->x)) return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
+    HTSend p;
+    p.x = a->x; p.w = a->weights; p.topk = a->topk_idx; p.q = a->rank_count; p.tok_rank = a->tok_rank;
+    p.tok_slot = a->tok_slot; p.offsets = a->offsets; p.peers = g->d_peers; p.out = a->out;
+    p.origin = a->origin; p.origin_w = a->origin_w; p.done = g->d_done; p.g = g->ht;
+    p.b = a->num_tokens; p.rank = g->rank; p.tag = ht_tag(round);
+    cudaError_t e;
+    switch (a->x_dtype) {
+      case EPB_F32: e = launch_hsend_x<EPB_F32>(p, a->out_dtype, s); break;
+      case EPB_BF16: e = launch_hsend_x<EPB_BF16>(p, a->out_dtype, s); break;
+      case EPB_F16: e = launch_hsend_x<EPB_F16>(p, a->out_dtype, s); break;
+      default: return fail(EPB_TAG_MISMATCH, "HT dispatch input must be f32/bf16/f16");
+    }
+    if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_send");
   }
-  if (e != cudaSuccess) return cuda_check(e, "ht_dispatch");
+  if (phases & 2) {
+    HTRecv p;
+    p.out = a->out; p.origin = a->origin; p.origin_w = a->origin_w; p.win = g->window; p.err = g->d_err;
+    p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank; p.tag = ht_tag(round);
+    cudaError_t e;
+    switch (wire) {
+      case EPB_F32: e = launch_hrecv<EPB_F32, EPB_F32>(p, s); break;
+      case EPB_BF16:
+        e = a->out_dtype == EPB_F32 ? launch_hrecv<EPB_BF16, EPB_F32>(p, s) : launch_hrecv<EPB_BF16, EPB_BF16>(p, s);
+        break;
+      default:
+        e = a->out_dtype == EPB_F32 ? launch_hrecv<EPB_F16, EPB_F32>(p, s) : launch_hrecv<EPB_F16, EPB_F16>(p, s);
+    }
+    if (e != cudaSuccess) return cuda_check(e, "ht_dispatch_recv");
+  }
   return EPB_OK;
 }
 
