@@ -164,6 +164,9 @@ typedef struct epb_ll_dispatch_args {
   float* counts_f32;        /*   [L, N] RECV_EXPERT_COUNTER                  */
   int32_t* counts_i32;      /*   [L, N] (combine input)                      */
   int32_t* src_info;        /*   [L, N*B] = t*K + k of each valid row        */
+  int32_t* self_row;        /* send: [b, K] output row of (t, k) when e_tk is
+                               this rank's own expert (placed directly, no
+                               window hop), else -1; combine input           */
 } epb_ll_dispatch_args;
 
 /* K2 + K3: LL dispatch (ll.py:227-400) */
@@ -179,6 +182,7 @@ typedef struct epb_ll_combine_args {
   int32_t num_tokens;
   void* out;                /*   [b, H] f32|bf16                             */
   int32_t out_dtype;
+  const int32_t* self_row;  /* [b, K] from the dispatch (own rows read in place) */
 } epb_ll_combine_args;
 
 /* K4a + K4b: LL combine (ll.py:404-507) */

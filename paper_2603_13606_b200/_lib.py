@@ -43,14 +43,14 @@ class LLDispatchArgs(ctypes.Structure):
                 ("topk_idx", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("out_scales", ctypes.c_void_p),
                 ("counts_f32", ctypes.c_void_p), ("counts_i32", ctypes.c_void_p),
-                ("src_info", ctypes.c_void_p)]
+                ("src_info", ctypes.c_void_p), ("self_row", ctypes.c_void_p)]
 
 
 class LLCombineArgs(ctypes.Structure):
     _fields_ = [("expert_out", ctypes.c_void_p), ("in_dtype", ctypes.c_int32),
                 ("counts_i32", ctypes.c_void_p), ("src_info", ctypes.c_void_p),
                 ("weights", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
-                ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32)]
+                ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("self_row", ctypes.c_void_p)]
 
 
 class HTDispatchArgs(ctypes.Structure):

@@ -546,10 +546,12 @@ class EpHandle:
             cnt_f, back_c = self._dev_out(out_counts, full=True)
             self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
             self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
+            self._self_row = torch.empty(max(b, 1) * cfg.top_k, dtype=torch.int32, device=dev)
             a = _lib.LLDispatchArgs(x.data_ptr(), tokens.dtype.code, xs.data_ptr() if xs is not None else None,
                                     self.routing.data_ptr(), b, out_t.data_ptr(), out_tokens.dtype.code,
                                     out_s.data_ptr() if out_s is not None else None, cnt_f.data_ptr(),
-                                    self._counts_i32.data_ptr(), self._src_info.data_ptr())
+                                    self._counts_i32.data_ptr(), self._src_info.data_ptr(),
+                                    self._self_row.data_ptr())
             self._ll_args = a
             self._keep_alive = (x, xs)
             self._staged = (out_tokens, out_counts, out_scales, out_t, out_s, cnt_f, back_t, back_s, back_c)
@@ -652,7 +654,8 @@ class EpHandle:
                 return
             o, back = self._dev_out(out, full=True)
             a = _lib.LLCombineArgs(y.data_ptr(), rows_in.dtype.code, self._counts_i32.data_ptr(),
-                                   self._src_info.data_ptr(), w.data_ptr(), b, o.data_ptr(), out.dtype.code)
+                                   self._src_info.data_ptr(), w.data_ptr(), b, o.data_ptr(), out.dtype.code,
+                                   self._self_row.data_ptr())
             self._ll_cargs = a
             self._staged = (out, o, back, w, y)
             if send_only:

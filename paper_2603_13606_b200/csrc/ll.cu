@@ -149,6 +149,7 @@ struct LLDisp {
   float* counts_f32;
   int32_t* counts_i32;
   int32_t* src_info;
+  int32_t* self_row;     // [b*K] row of (t, k) in this rank's output if e_tk is local, else -1
   const uint64_t* peers;
   const uint8_t* win;
   int* err;
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   constexpr int NV = (EPC * XW) >= 16 ? (EPC * XW) / 16 : 0;  // 16-B input loads per chunk
   const bool vec = (H & 15) == 0;
   const int nch = vec ? H / EPC : 0;
+  constexpr int OB = OT == EPB_F32 ? 4 : (OT == EPB_FP8 ? 1 : 2);  // output element bytes
 
   // prefetch this CTA's first token chunk: its DRAM latency overlaps the
   // routing pass below
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     int* s_q = s_m + E;                                                        // [N]
     __shared__ int s_bad, s_nd;
     __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks];
+    __shared__ int s_self[kMaxTopK];  // output row of (t, k) for this rank's own experts, else -1
     __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
     for (int i = threadIdx.x; i < (E + N) * W + E + N; i += blockDim.x) reinterpret_cast<int*>(s_ebits)[i] = 0;
     if (threadIdx.x == 0) s_bad = 0;
@@ -343,7 +346,10 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           ci += __popc(s_ebits[e * W + wt] & below);
           cj += __popc(s_dbits[d * W + wt] & below);
         }
-        bool first = lane < K;
+        // rows for this rank's own experts skip the window: they go straight
+        // to the expert-major output (and the combine reads them in place)
+        const bool mine = lane < K && d == p.rank;
+        bool first = lane < K && !mine;
         for (int j = 0; j < K; ++j) {
           const int dj = __shfl_sync(0xffffffffu, d, j);
           first &= !(j < lane && dj == d);
@@ -352,6 +358,10 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         if (lane < K) {
           s_hdr[2 + lane] = (uint32_t)e;
           s_hdr[2 + K + lane] = (uint32_t)ci;
+          const int srow = mine ? (e - p.rank * L) * N * B + p.rank * B + ci : -1;
+          s_self[lane] = srow;
+          if (p.self_row) p.self_row[(int64_t)t * K + lane] = srow;
+          if (mine) p.src_info[srow] = t * K + lane;
           if (first) {
             const int pos = __popc(fm & ((1u << lane) - 1u));
             s_dst[pos] = d;
@@ -415,6 +425,25 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
               if ((c & 7) == 0) reinterpret_cast<float*>(slot + g.RBp)[c >> 3] = scale;
             }
           }
+          for (int k = 0; k < K; ++k) {
+            const int srow = s_self[k];
+            if (srow < 0) continue;
+            uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)srow * H * OB;
+            if constexpr (OT == WT) {
+              st_v4(orow + (int64_t)c * 16, v);
+              if constexpr (SC) {
+                if ((c & 7) == 0) p.out_scales[(int64_t)srow * (H / 128) + (c >> 3)] = scale;
+              }
+            } else {
+              float fw[EPC];  // the f32 image of what a slot would carry
+              unpack16<WT>(v, fw);
+              if constexpr (SC) {
+#pragma unroll
+                for (int i = 0; i < EPC; ++i) fw[i] = __fmul_rn(fw[i], scale);
+              }
+              store_f32_chunk<EPB_F32, EPC>(orow, (int64_t)c * EPC, fw);
+            }
+          }
         }
       } else {
         // hidden not a multiple of 16: element path (scales need H % 128 == 0)
@@ -426,6 +455,15 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           for (int i = 0; i < nd; ++i) {
             uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
             store_elem(slot, WT, el, f);
+          }
+          for (int k = 0; k < K; ++k) {
+            const int srow = s_self[k];
+            if (srow < 0) continue;
+            uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)srow * H * OB;
+            uint32_t wire = 0;
+            store_elem(&wire, WT, 0, f);
+            if constexpr (OT == WT) store_elem(orow, WT, el, load_elem(&wire, WT, 0));
+            else reinterpret_cast<float*>(orow)[el] = load_elem(&wire, WT, 0);
           }
         }
       }
@@ -477,7 +515,8 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       }
     }
     if (nloc == 0) return;
-    if ((int)threadIdx.x < N) s_rq[threadIdx.x] = (int)((ctr[threadIdx.x] >> 20) & 0xFFFFF);
+    // own rows were placed by the send phase; only remote slots remain
+    if ((int)threadIdx.x < N) s_rq[threadIdx.x] = (int)threadIdx.x == p.rank ? 0 : (int)((ctr[threadIdx.x] >> 20) & 0xFFFFF);
     __syncthreads();
     if (threadIdx.x == 0) {
       int run = 0;
@@ -516,6 +555,7 @@ struct LLComb {
   const void* y;
   const int32_t* counts;
   const int32_t* src_info;
+  const int32_t* self_row;  // [b*K] from the dispatch: rows of own experts are read in place
   const float* w;
   void* out;
   const uint32_t* hseq;
@@ -585,6 +625,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
       }
       const int pair = lo_i;
       const int l = pair / N, s = pair - l * N, i = r - s_pre[pair];
+      if (s == p.rank) continue;  // own tokens: the home reads these rows in place
       const int64_t row = (int64_t)l * N * B + (int64_t)s * B + i;
       const int info = p.src_info[row];
       uint8_t* dst = peer_base(p.peers, s) + parity_off + g.comb_slot + (int64_t)info * g.comb_stride;
@@ -651,18 +692,38 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
         const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
         const float* wt = p.w + (int64_t)t * K;
+        // lane k: row k of this token is this rank's own expert row (read in
+        // place from the expert output, wire-rounded) or a combine slot
+        const int my_self = (p.self_row && lane < K) ? p.self_row[(int64_t)t * K + lane] : -1;
 #pragma unroll
         for (int h = 0; h < kSeg / 32; ++h) {
+          if (sg * kSeg + h * 32 >= nch) break;
           const int c = sg * kSeg + h * 32 + lane;
-          if (c >= nch) break;
+          const bool ok = c < nch;
           float acc[EPC];
 #pragma unroll
           for (int i = 0; i < EPC; ++i) acc[i] = 0.0f;
           for (int k0 = 0; k0 < K; k0 += 8) {
             int4 v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (k0 + u < K) v[u] = ld_weak_v4(tsl + (int64_t)(k0 + u) * g.comb_stride + (int64_t)c * 16);
+            for (int u = 0; u < 8; ++u) {
+              if (k0 + u < K) {
+                const int sr = __shfl_sync(0xffffffffu, my_self, (k0 + u) & 31);
+                if (!ok) continue;
+                if (sr >= 0) {
+                  const uint8_t* yrow = reinterpret_cast<const uint8_t*>(p.y) + (int64_t)sr * H * dtype_width(IT);
+                  if constexpr (IT == WT) {
+                    v[u] = ld_nc_v4(yrow + (int64_t)c * 16);
+                  } else {
+                    float f[EPC];
+                    load_elems_vec<IT, EPC>(yrow, (int64_t)c * EPC, f);
+                    v[u] = pack16<WT>(f);
+                  }
+                } else {
+                  v[u] = ld_weak_v4(tsl + (int64_t)(k0 + u) * g.comb_stride + (int64_t)c * 16);
+                }
+              }
+            }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               if (k0 + u < K) {
@@ -674,7 +735,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
               }
             }
           }
-          store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, acc);
+          if (ok) store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, acc);
         }
       }
     } else {
@@ -686,8 +747,19 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
         for (int el = threadIdx.x; el < H; el += blockDim.x) {
           float acc = 0.0f;
-          for (int k = 0; k < K; ++k)
-            acc = __fadd_rn(acc, __fmul_rn(s_w[k], load_elem(tsl + (int64_t)k * g.comb_stride, WT, el)));
+          for (int k = 0; k < K; ++k) {
+            const int sr = p.self_row ? p.self_row[(int64_t)t * K + k] : -1;
+            float y;
+            if (sr >= 0) {
+              uint32_t wire = 0;  // own expert row, rounded through the wire dtype
+              store_elem(&wire, WT, 0,
+                         load_elem(reinterpret_cast<const uint8_t*>(p.y) + (int64_t)sr * H * dtype_width(IT), IT, el));
+              y = load_elem(&wire, WT, 0);
+            } else {
+              y = load_elem(tsl + (int64_t)k * g.comb_stride, WT, el);
+            }
+            acc = __fadd_rn(acc, __fmul_rn(s_w[k], y));
+          }
           store_elem(orow, OT, el, acc);
         }
       }
@@ -836,7 +908,7 @@ int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases, const epb_ll_d
   LLDisp p;
   p.x = a->x; p.x_scales = a->x_scales; p.topk = a->topk_idx; p.hseq = hseq;
   p.out = a->out; p.out_scales = a->out_scales; p.counts_f32 = a->counts_f32; p.counts_i32 = a->counts_i32;
-  p.src_info = a->src_info; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err;
+  p.src_info = a->src_info; p.self_row = a->self_row; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err;
   p.dseq = reinterpret_cast<uint32_t*>(g->d_scratch); p.drd = g->d_scratch + 1; p.trace = g->trace;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;
@@ -871,7 +943,8 @@ int epb_ll_combine(epb_group* g, const uint32_t* hseq, int32_t phases, const epb
   }
   if (a->in_dtype != EPB_F32 && a->in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
   LLComb p;
-  p.y = a->expert_out; p.counts = a->counts_i32; p.src_info = a->src_info; p.w = a->weights; p.out = a->out;
+  p.y = a->expert_out; p.counts = a->counts_i32; p.src_info = a->src_info; p.self_row = a->self_row;
+  p.w = a->weights; p.out = a->out;
   p.hseq = hseq; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err; p.trace = g->trace;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;
