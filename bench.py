@@ -196,10 +196,16 @@ class LLStep:
         self.W = ep.tensor_from_torch(self.w, T.TOPK_WEIGHTS)
         self.OUT = ep.tensor_from_torch(self.out, T.TOKENS)
 
-    def step(self):
+    def step(self, upto="combine"):
+        """One LL step; `upto` truncates it ("dispatch", "handle") for the
+        marginal per-kernel timing in run_ll."""
         h = self.g.create_handle(self.topk)
-        h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT])
-        h.combine([self.Y, self.W], [self.OUT])
+        if upto != "handle":
+            h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT])
+        if upto == "combine":
+            h.combine([self.Y, self.W], [self.OUT])
+        elif upto == "dispatch":
+            h.state = self.ep.HandleState.COMBINED  # timing only: this round's combine is skipped
         h.destroy()
 
     # algorithmic bytes per kernel launch (this rank), headers not credited
@@ -289,30 +295,108 @@ def replay_timed(graph, marks, steps, flush, sync_each=False, align=None):
     return total, phase
 
 
+def capture_steps(step_obj, group, nsteps, flush, phases, upto="combine"):
+    """One CUDA graph holding `nsteps` whole steps, each preceded by an L2
+    flush and a device barrier of all ranks (untimed) and bracketed by
+    external event nodes — per-step device time without the per-launch cost
+    of a graph (a decode step's EP ops are nodes inside a bigger graph).
+    With `phases`, every kernel launch is also preceded by an event."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            step_obj.step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    per_step = []
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(nsteps):
+            flush.zero_()
+            group.device_barrier()
+            marks = []
+            group.trace_phases(marks)
+            group.mark("step:start")
+            if not phases:
+                group.trace_phases(None)
+            step_obj.step(upto)
+            group.trace_phases(marks)
+            group.mark("step:end")
+            group.trace_phases(None)
+            per_step.append(marks)
+    torch.cuda.synchronize()
+    return graph, per_step
+
+
+def replay_steps(graph, per_step, replays):
+    """Replay; returns (sum of step times ms, {phase: summed ms}, steps)."""
+    import torch
+    total, phase, n = 0.0, {}, 0
+    for _ in range(replays):
+        graph.replay()
+        torch.cuda.synchronize()
+        for marks in per_step:
+            evs = [m[1] for m in marks]
+            total += evs[0].elapsed_time(evs[-1])
+            for i in range(len(marks) - 1):
+                phase[marks[i][0]] = phase.get(marks[i][0], 0.0) + evs[i].elapsed_time(evs[i + 1])
+            n += 1
+    return total, phase, n
+
+
+def steps_per_graph(steps):
+    return max(d for d in range(1, min(steps, 10) + 1) if steps % d == 0)
+
+
 def run_ll(args, world, rank):
     import torch
     st = LLStep(world, rank, args.tokens)
-    graph, marks = capture(st, st.g, phases=False)
-    graph_b, marks_b = capture(st, st.g, phases=True)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    for _ in range(args.warmup):
-        flush.zero_()
-        st.g.device_barrier()
+    S = steps_per_graph(args.steps)
+    graph, per_step = capture_steps(st, st.g, S, flush, phases=False)
+    graph_b, per_step_b = capture_steps(st, st.g, S, flush, phases=True)
+    for _ in range(max(1, -(-args.warmup // S))):
         graph.replay()
+    torch.cuda.synchronize()
     barrier(world)
     with ClockSampler(torch.cuda.current_device()) as clk:
         barrier(world)
-        total, _ = replay_timed(graph, marks, args.steps, flush, align=st.g.device_barrier)
+        total, _, n = replay_steps(graph, per_step, args.steps // S)
         barrier(world)
+    assert n == args.steps
     # per-kernel breakdown from the instrumented graph (events between launches)
-    nb = max(10, min(args.steps, 100))
     barrier(world)
-    _, phase = replay_timed(graph_b, marks_b, nb, flush, sync_each=True, align=st.g.device_barrier)
+    nb = max(10, min(args.steps, 100))
+    _, phase, nph = replay_steps(graph_b, per_step_b, -(-nb // S))
+    # per-kernel device time as the marginal cost inside the graph: step
+    # truncated after dispatch / after create_handle, same bracketing events
+    marg = {}
+    for upto in ("dispatch", "handle"):
+        g2, ps2 = capture_steps(st, st.g, S, flush, phases=False, upto=upto)
+        g2.replay()
+        barrier(world)
+        t2, _, n2 = replay_steps(g2, ps2, -(-nb // S))
+        marg[upto] = allreduce_max(t2 / n2, world) * 1000.0
+        del g2
+    marg["combine"] = allreduce_max(total / n, world) * 1000.0
+    # the same step as its own graph launch per step (graph launch included)
+    graph1, marks1 = capture(st, st.g, phases=False)
+    for _ in range(3):
+        flush.zero_()
+        st.g.device_barrier()
+        graph1.replay()
+    barrier(world)
+    t1, _ = replay_timed(graph1, marks1, args.steps, flush, align=st.g.device_barrier)
     st.g.check()
     total_max = allreduce_max(total, world)
-    per_phase = {n: v / nb * 1000.0 for n, v in phase.items()}  # us
-    launches = sum(1 for n, _ in marks_b if n.startswith("epb_"))
-    return st, total_max / args.steps, per_phase, launches * args.steps, clk.report()
+    t1_max = allreduce_max(t1, world)
+    per_phase = {k: v / nph * 1000.0 for k, v in phase.items()}  # us
+    launches = sum(1 for n_, _ in per_step_b[0] if n_.startswith("epb_"))
+    kernel_us = {"epb_ll_dispatch": marg["dispatch"] - marg["handle"],
+                 "epb_ll_combine": marg["combine"] - marg["dispatch"]}
+    return (st, total_max / args.steps, per_phase, launches * args.steps, clk.report(),
+            t1_max / args.steps * 1000.0, kernel_us)
 
 
 def run_e2e(args, world, rank, st):
@@ -471,11 +555,11 @@ def main():
         return main_reference(args)
     import torch
     world, rank = init_dist()
-    st, step_ms, phases, launches, clocks = run_ll(args, world, rank)
+    st, step_ms, phases, launches, clocks, own_graph_us, kernel_us = run_ll(args, world, rank)
     value_us = step_ms * 1000.0
     # roofline of the dominant kernel
     algo, remote = st.algo_bytes()
-    kernels = {k: v for k, v in phases.items() if k.startswith("epb_")}
+    kernels = kernel_us
     dom = max(kernels, key=kernels.get)
     peaks = {}
     try:
@@ -507,12 +591,17 @@ def main():
                    "hidden": H, "tokens_per_rank": args.tokens, "ranks": world,
                    "parallelism": f"ep{world}", "l2": "flushed (256 MB memset) before every step",
                    "align": "device barrier of all ranks before each step (untimed)",
-                   "graph": "one CUDA graph per step (create_handle+dispatch+combine)"},
-        "phase_us": {k: round(v, 2) for k, v in phases.items()},
+                   "graph": (f"{steps_per_graph(args.steps)} steps per CUDA graph (create_handle+dispatch+combine "
+                             "each, bracketed by in-graph events; flush + barrier between, untimed)")},
+        "step_us_own_graph_launch": round(own_graph_us, 2),
+        "kernel_us": {k: round(v, 2) for k, v in kernel_us.items()},
+        "phase_us_event_nodes": {k: round(v, 2) for k, v in phases.items()},
         "gpu_launches": launches,
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "algorithmic_bytes": int(algo[dom]), "traffic": traffic,
+                     "duration": "kernel_us: marginal in-graph event time of the launch (step truncated "
+                                 "before it vs after it, same bracketing events)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
         "nvlink_bytes_per_step": remote if world > 1 else None,
         "clocks": clocks,
@@ -526,7 +615,7 @@ def main():
         for bb in (1, 2, 4, 8, 16, 32, 64, 128):
             a2 = argparse.Namespace(**vars(args))
             a2.tokens, a2.steps, a2.warmup = bb, max(20, args.steps // 4), 5
-            s2, ms2, _, _, _ = run_ll(a2, world, rank)
+            s2, ms2, _, _, _, _, _ = run_ll(a2, world, rank)
             sweep[bb] = round(ms2 * 1000, 2)
             s2.g.destroy()
         result["ll_sweep_us"] = sweep

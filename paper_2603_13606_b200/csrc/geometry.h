@@ -34,6 +34,8 @@ struct LLGeom {
   int64_t n_disp, n_comb;
   uint64_t disp_ctr, disp_flag, comb_flag, disp_slot, comb_slot;  // offsets within a parity
   int grid;  // CTAs of every LL launch (kLLGrid)
+  uint64_t Lmagic;  // ceil(2^32 / L): owner rank e / L = (e * Lmagic) >> 32 (exact for e * L < 2^32)
+  uint64_t Kmagic;  // ceil(2^32 / K): token of a routing item i / K (i * K < 2^32)
   uint64_t parity_bytes, window_bytes, logical_bytes;
   uint64_t barrier;  // [N] u64 device-barrier flags (after both parities)
 };
@@ -66,6 +68,8 @@ inline void make_ll_geom(const epb_config& c, LLGeom& g) {
   g.HB = 8 + 4 * c.top_k;
   g.HBp = (int)a16(g.HB + 4 * c.top_k);
   g.slot_stride = g.RBp + g.SBp + g.HBp;
+  g.Lmagic = ((1ull << 32) + (uint64_t)g.L - 1) / (uint64_t)g.L;
+  g.Kmagic = ((1ull << 32) + (uint64_t)g.K - 1) / (uint64_t)g.K;
   g.comb_stride = (int)a16(g.CB);
   const int64_t pairs = (int64_t)g.L * g.N;
   if (c.layout == EPB_LAYOUT_LEGACY) {

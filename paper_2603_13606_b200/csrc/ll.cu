@@ -43,7 +43,14 @@ constexpr int kParts = 4;  // combine send: warps per row
   } while (0)
 
 EPB_DEV uint32_t ll_tag_of(uint32_t seq) { return (seq % 0xFFFFFFu) + 1u; }
-EPB_DEV uint32_t ld_volatile_u32(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
+// round counters: written by an earlier kernel (visible at the kernel
+// boundary) and not again until every CTA has read them — a relaxed GPU-scope
+// load suffices (a volatile, i.e. system-scope, load measured ~2 us slower)
+EPB_DEV uint32_t ld_round_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 EPB_DEV uint8_t* peer_base(const uint64_t* peers, int r) { return reinterpret_cast<uint8_t*>(peers[r]); }
 
 EPB_DEV void fence_scoped(bool sys) {
@@ -96,29 +103,6 @@ EPB_DEV void warp_copy16(const uint8_t* src, uint8_t* dst, int c0, int c1, int l
     for (int u = 0; u < kUnroll; ++u) {
       const int c = base + u * 32 + lane;
       if (c < c1) st_weak_v4(dst + (int64_t)c * 16, v[u]);
-    }
-  }
-}
-
-// The round sequence lives on the device (graph-replayable): the send phase
-// reads the group counter; the last CTA to read it stores it into the
-// handle word and advances the counter.  Recv-only launches read the handle.
-EPB_DEV uint32_t ll_round_seq(uint32_t* dseq, uint32_t* hseq, bool alloc) {
-  __shared__ uint32_t s_seq;
-  if (threadIdx.x == 0) s_seq = ld_volatile_u32(alloc ? dseq : hseq);
-  __syncthreads();
-  return s_seq;
-}
-
-// end of a send phase: the last CTA (all have read the counter by now)
-// records the round in the handle word and advances the group counter
-EPB_DEV void ll_round_commit(uint32_t* dseq, int* drd, uint32_t* hseq, uint32_t seq) {
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(drd, 1) == (int)gridDim.x - 1) {
-      *drd = 0;
-      *hseq = seq;
-      *dseq = seq + 1;
     }
   }
 }
@@ -235,21 +219,44 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   const int nch = vec ? H / EPC : 0;
   constexpr int OB = OT == EPB_F32 ? 4 : (OT == EPB_FP8 ? 1 : 2);  // output element bytes
 
+  // split: warps 1.. quantise a token's chunks (<= 2 each, in registers)
+  // while warp 0 resolves its destinations; else every thread loops
+  const int nq = (int)blockDim.x - 32;
+  const bool split = vec && nch <= 2 * nq;
+  const int c_first = split ? (int)threadIdx.x - 32 : (int)threadIdx.x;  // first chunk of this thread
   // prefetch this CTA's first token chunk: its DRAM latency overlaps the
   // routing pass below
   int4 xr[NV > 0 ? NV : 1];
-  const bool pre = (p.phases & kPhaseSend) && NV > 0 && vec && (int)blockIdx.x < b && (int)threadIdx.x < nch;
+  const bool pre = (p.phases & kPhaseSend) && NV > 0 && vec && (int)blockIdx.x < b && c_first >= 0 && c_first < nch;
   if (pre) {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(p.x) +
-                         ((int64_t)blockIdx.x * H + (int64_t)threadIdx.x * EPC) * XW;
+                         ((int64_t)blockIdx.x * H + (int64_t)c_first * EPC) * XW;
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) xr[v] = ld_nc_v4(src + 16 * v);
   }
+  // prefetch this thread's first two routing items (t*K + k) and, for
+  // top-k <= 8, the routing row of token t = threadIdx.x (validation)
+  int64_t rid0 = 0, rid1 = 0;
+  int64_t row[8];
+  const bool row_pre = (p.phases & kPhaseSend) && K <= 8 && (int)threadIdx.x < b;
+  if (p.phases & kPhaseSend) {
+    const int i0 = (int)threadIdx.x, i1 = i0 + (int)blockDim.x;
+    if (i0 < b * K) rid0 = __ldg(p.topk + i0);
+    if (i1 < b * K) rid1 = __ldg(p.topk + i1);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) row[k] = (row_pre && k < K) ? __ldg(p.topk + (int64_t)threadIdx.x * K + k) : -1 - k;
   LL_STAMP(p, 0);
-  const uint32_t seq = ll_round_seq(p.dseq, p.hseq, p.phases & kPhaseSend);
-  const uint32_t tag = ll_tag_of(seq);
-  const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
-  LL_STAMP(p, 1);
+  // round sequence: thread 0 issues the load now; it lands in shared memory
+  // at the first block barrier after the routing pass (send) or right away
+  __shared__ uint32_t s_seq;
+  uint32_t seq_ld = 0;
+  if (threadIdx.x == 0) seq_ld = ld_round_u32((p.phases & kPhaseSend) ? p.dseq : p.hseq);
+  uint32_t seq = 0, tag = 0;
+  uint64_t parity_off = 0;
+  // per-expert token counts of this round (send phase; the fused receive
+  // takes its own-rank counts from here)
+  int* s_m = nullptr;
 
   if (p.phases & kPhaseSend) {
     // shared: routing snapshot, per-expert and per-destination token bitmaps
@@ -258,77 +265,196 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     int* s_topk = smem;                                                        // [b*K]
     uint32_t* s_ebits = reinterpret_cast<uint32_t*>(s_topk + b * K);           // [E][W]
     uint32_t* s_dbits = s_ebits + E * W;                                       // [N][W]
-    int* s_m = reinterpret_cast<int*>(s_dbits + N * W);                        // [E]
+    s_m = reinterpret_cast<int*>(s_dbits + N * W);                             // [E]
     int* s_q = s_m + E;                                                        // [N]
     __shared__ int s_bad, s_nd;
     __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks];
     __shared__ int s_self[kMaxTopK];  // output row of (t, k) for this rank's own experts, else -1
     __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
-    for (int i = threadIdx.x; i < (E + N) * W + E + N; i += blockDim.x) reinterpret_cast<int*>(s_ebits)[i] = 0;
+    for (int i = threadIdx.x; i < E * W; i += blockDim.x) s_ebits[i] = 0;
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
-    // routing rows: snapshot, validation (api.py:150-170), counts, bitmaps
+    LL_STAMP(p, 8);
+    // routing (api.py:150-170).  Rows: range check and distinct experts,
+    // from registers (one token per thread).  Items (t, k), one per thread
+    // per pass (coalesced): snapshot and the token bitmap of each expert.
+    // No value-returning atomics and no dependent shared-memory chains on
+    // this path: each link of such a chain costs ~30+ cycles.
     for (int t = threadIdx.x; t < b; t += blockDim.x) {
       bool ok = true;
-      uint64_t mask = 0;
-      const uint32_t bit = 1u << (t & 31);
-      const int wi = t >> 5;
       if (K <= 8) {
-        // register path (top-k <= 8): no local-memory row copy
-        int ids[8];
+        int64_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = (t == (int)threadIdx.x && row_pre) ? row[k] : (k < K ? p.topk[(int64_t)t * K + k] : -1 - k);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int64_t e = k < K ? p.topk[(int64_t)t * K + k] : -1 - k;
-          ok &= (k >= K) || (e >= 0 && e < E);
-          ids[k] = (int)e;
-        }
+          ok &= k >= K || (v[k] >= 0 && v[k] < E);
 #pragma unroll
-        for (int k = 1; k < 8; ++k)
-#pragma unroll
-          for (int j = 0; j < k; ++j) ok &= (k >= K) || ids[j] != ids[k];
-        if (!ok) { s_bad = 1; continue; }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (k < K) {
-            s_topk[t * K + k] = ids[k];
-            atomicAdd(&s_m[ids[k]], 1);
-            atomicOr(&s_ebits[ids[k] * W + wi], bit);
-            mask |= 1ull << (ids[k] / L);
-          }
+          for (int j = 0; j < k; ++j) ok &= v[j] != v[k];
         }
       } else {
-        int ids[kMaxTopK];
         for (int k = 0; k < K; ++k) {
           const int64_t e = p.topk[(int64_t)t * K + k];
-          ok &= (e >= 0 && e < E);
-          ids[k] = (int)e;
-        }
-        for (int k = 0; ok && k < K; ++k)
-          for (int j = 0; j < k; ++j) ok &= ids[j] != ids[k];
-        if (!ok) { s_bad = 1; continue; }
-        for (int k = 0; k < K; ++k) {
-          s_topk[t * K + k] = ids[k];
-          atomicAdd(&s_m[ids[k]], 1);
-          atomicOr(&s_ebits[ids[k] * W + wi], bit);
-          mask |= 1ull << (ids[k] / L);
+          ok &= e >= 0 && e < E;
+          for (int j = 0; j < k; ++j) ok &= p.topk[(int64_t)t * K + j] != e;
         }
       }
-      for (uint64_t mm = mask; mm; mm &= mm - 1) {
-        const int d = __ffsll(mm) - 1;
-        atomicAdd(&s_q[d], 1);
-        atomicOr(&s_dbits[d * W + wi], bit);
-      }
+      if (!ok) s_bad = 1;
+    }
+    const int items = b * K;
+    for (int i = threadIdx.x, r = 0; i < items; i += blockDim.x, ++r) {
+      const int64_t e = r == 0 ? rid0 : (r == 1 ? rid1 : p.topk[i]);
+      const int t = (int)(((uint64_t)i * g.Kmagic) >> 32);
+      s_topk[i] = (int)e;
+      if (e >= 0 && e < E) atomicOr(&s_ebits[(int)e * W + (t >> 5)], 1u << (t & 31));
     }
     __syncthreads();
+    LL_STAMP(p, 13);
+    // per expert (threads [0, E)): token count = popcount of its bitmap;
+    // per destination word (threads [E, E + N*W)): OR of its experts' words
+    for (int u = threadIdx.x; u < E + N * W; u += blockDim.x) {
+      if (u < E) {
+        int m = 0;
+        if (W <= 16) {
+#pragma unroll
+          for (int w = 0; w < 16; ++w) m += w < W ? __popc(s_ebits[u * W + min(w, W - 1)]) : 0;
+        } else {
+          for (int w = 0; w < W; ++w) m += __popc(s_ebits[u * W + w]);
+        }
+        s_m[u] = m;
+      } else {
+        const int d = (u - E) / W, w = (u - E) - d * W;
+        const int e0 = d * L, e1 = min(E, e0 + L);
+        uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+        int e = e0;
+        for (; e + 4 <= e1; e += 4) {
+          o0 |= s_ebits[e * W + w];
+          o1 |= s_ebits[(e + 1) * W + w];
+          o2 |= s_ebits[(e + 2) * W + w];
+          o3 |= s_ebits[(e + 3) * W + w];
+        }
+        for (; e < e1; ++e) o0 |= s_ebits[e * W + w];
+        s_dbits[d * W + w] = o0 | o1 | o2 | o3;
+      }
+    }
+    LL_STAMP(p, 10);
+    uint32_t arrived = 0;
+    if (threadIdx.x == 0) {
+      s_seq = seq_ld;
+      LL_STAMP(p, 11);
+      // every CTA has read the round counter (its value is consumed above,
+      // so the read is complete): arrive now, act on the result at the end
+      // of the send phase (the round trip overlaps it)
+      arrived = atomicAdd(reinterpret_cast<unsigned*>(p.drd), 1u);
+      LL_STAMP(p, 12);
+    }
+    __syncthreads();
+    seq = s_seq;
+    tag = ll_tag_of(seq);
+    parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+    LL_STAMP(p, 1);
+    // the last CTA to arrive records the round in the handle word and
+    // advances the group counter (all CTAs have read it)
+    auto commit_round = [&]() {
+      if (threadIdx.x == 0 && arrived == (uint32_t)gridDim.x - 1) {
+        *p.drd = 0;
+        *p.hseq = seq;
+        *p.dseq = seq + 1;
+      }
+    };
     if (s_bad) {
       // validation before any traffic: every CTA reaches the same verdict
       if (threadIdx.x == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
+      commit_round();
       return;
     }
     LL_STAMP(p, 2);
+    // tokens per destination (count words), read at the publish below
+    for (int d = threadIdx.x; d < N; d += blockDim.x) {
+      int q = 0;
+      for (int w = 0; w < W; ++w) q += __popc(s_dbits[d * W + w]);
+      s_q[d] = q;
+    }
     const uint64_t slot_off = parity_off + g.disp_slot;
     const int64_t slot_base = (int64_t)p.rank * B;
+    // one token chunk: input (prefetched for the CTA's first token) ->
+    // f32 -> optional block-128 FP8 scale (x / scale, correctly rounded) ->
+    // 16-B wire image
+    auto quantize = [&](int t, int c, const uint8_t* xrow, const float* xsc, int4& v, float& scale) {
+      float f[EPC];
+      if (pre && t == (int)blockIdx.x && c == c_first) {
+        if constexpr (NV > 0) {
+          constexpr int PER = 16 / XW;  // input elements per 16-B load
+#pragma unroll
+          for (int u = 0; u < NV; ++u) unpack16<XT>(xr[u], f + u * PER);
+          if constexpr (XT == EPB_FP8) {
+            if (xsc != nullptr) {
+#pragma unroll
+              for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[((int64_t)c * EPC + i) >> 7]);
+            }
+          }
+        }
+      } else {
+        load_input_chunk<XT, EPC>(xrow, xsc, (int64_t)c * EPC, f);
+      }
+      scale = 0.0f;
+      if constexpr (SC) {
+        // block-128 = 8 consecutive 16-element chunks = 8 aligned lanes
+        float amax = 0.0f;
+#pragma unroll
+        for (int i = 0; i < EPC; ++i) amax = fmaxf(amax, fabsf(f[i]));
+        const unsigned gm = 0xFFu << (lane & 24);
+        amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 2));
+        amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 4));
+        scale = __fdiv_rn(amax, 448.0f);
+        const float div = scale > 0.0f ? scale : 1.0f;
+#pragma unroll
+        for (int i = 0; i < EPC; ++i) f[i] = __fdiv_rn(f[i], div);
+      }
+      v = pack16<WT>(f);
+    };
+    // chunk c to every destination slot and every own-expert output row
+    auto emit = [&](int c, const int4& v, float scale, int nd) {
+      for (int i = 0; i < nd; ++i) {
+        uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
+        st_na_v4(slot + (int64_t)c * 16, v);
+        if constexpr (SC) {
+          if ((c & 7) == 0) reinterpret_cast<float*>(slot + g.RBp)[c >> 3] = scale;
+        }
+      }
+      for (int k = 0; k < K; ++k) {
+        const int srow = s_self[k];
+        if (srow < 0) continue;
+        uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)srow * H * OB;
+        if constexpr (OT == WT) {
+          st_v4(orow + (int64_t)c * 16, v);
+          if constexpr (SC) {
+            if ((c & 7) == 0) p.out_scales[(int64_t)srow * (H / 128) + (c >> 3)] = scale;
+          }
+        } else {
+          float fw[EPC];  // the f32 image of what a slot would carry
+          unpack16<WT>(v, fw);
+          if constexpr (SC) {
+#pragma unroll
+            for (int i = 0; i < EPC; ++i) fw[i] = __fmul_rn(fw[i], scale);
+          }
+          store_f32_chunk<EPB_F32, EPC>(orow, (int64_t)c * EPC, fw);
+        }
+      }
+    };
     for (int t = blockIdx.x; t < b; t += G) {
+      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
+      const float* xsc = p.x_scales ? p.x_scales + (int64_t)t * (H / 128) : nullptr;
+      int4 qv[2];
+      float qs[2] = {0.0f, 0.0f};
+      if (split && warp > 0) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int c = c_first + r * nq;
+          if (c < nch) quantize(t, c, xrow, xsc, qv[r], qs[r]);
+        }
+      }
       if (warp == 0) {
         // lane k: i = #{t' < t routed to e_tk} (popc of e's bitmap below t)
         // and, for its owner d_k, j = #{t' < t touching d_k}; lanes keep the
@@ -338,13 +464,23 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         int e = -1, d = -1, ci = 0, cj = 0;
         if (lane < K) {
           e = s_topk[t * K + lane];
-          d = e / L;
-          for (int w = 0; w < wt; ++w) {
-            ci += __popc(s_ebits[e * W + w]);
-            cj += __popc(s_dbits[d * W + w]);
+          d = (int)(((uint64_t)e * g.Lmagic) >> 32);
+          if (W <= 16) {
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+              const int wc = min(w, W - 1);
+              const uint32_t mk = w < wt ? 0xFFFFFFFFu : (w == wt ? below : 0u);
+              ci += __popc(s_ebits[e * W + wc] & mk);
+              cj += __popc(s_dbits[d * W + wc] & mk);
+            }
+          } else {
+            for (int w = 0; w < wt; ++w) {
+              ci += __popc(s_ebits[e * W + w]);
+              cj += __popc(s_dbits[d * W + w]);
+            }
+            ci += __popc(s_ebits[e * W + wt] & below);
+            cj += __popc(s_dbits[d * W + wt] & below);
           }
-          ci += __popc(s_ebits[e * W + wt] & below);
-          cj += __popc(s_dbits[d * W + wt] & below);
         }
         // rows for this rank's own experts skip the window: they go straight
         // to the expert-major output (and the combine reads them in place)
@@ -382,68 +518,20 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
           reinterpret_cast<uint32_t*>(slot + g.RBp + g.SBp)[w] = s_hdr[w];
         }
-      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
-      const float* xsc = p.x_scales ? p.x_scales + (int64_t)t * (H / 128) : nullptr;
-      if (vec) {
+      if (split) {
+        if (warp > 0) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int c = c_first + r * nq;
+            if (c < nch) emit(c, qv[r], qs[r], nd);
+          }
+        }
+      } else if (vec) {
         for (int c = threadIdx.x; c < nch; c += blockDim.x) {
-          float f[EPC];
-          if (pre && t == (int)blockIdx.x && c == (int)threadIdx.x) {
-            if constexpr (NV > 0) {
-              constexpr int PER = 16 / XW;  // input elements per 16-B load
-#pragma unroll
-              for (int v = 0; v < NV; ++v) unpack16<XT>(xr[v], f + v * PER);
-              if constexpr (XT == EPB_FP8) {
-                if (xsc != nullptr) {
-#pragma unroll
-                  for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[((int64_t)c * EPC + i) >> 7]);
-                }
-              }
-            }
-          } else {
-            load_input_chunk<XT, EPC>(xrow, xsc, (int64_t)c * EPC, f);
-          }
-          float scale = 0.0f;
-          if constexpr (SC) {
-            // block-128 = 8 consecutive 16-element chunks = 8 aligned lanes
-            float amax = 0.0f;
-#pragma unroll
-            for (int i = 0; i < EPC; ++i) amax = fmaxf(amax, fabsf(f[i]));
-            const unsigned gm = 0xFFu << (lane & 24);
-            amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 1));
-            amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 2));
-            amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 4));
-            scale = __fdiv_rn(amax, 448.0f);
-            const float div = scale > 0.0f ? scale : 1.0f;
-#pragma unroll
-            for (int i = 0; i < EPC; ++i) f[i] = __fdiv_rn(f[i], div);
-          }
-          const int4 v = pack16<WT>(f);
-          for (int i = 0; i < nd; ++i) {
-            uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
-            st_na_v4(slot + (int64_t)c * 16, v);
-            if constexpr (SC) {
-              if ((c & 7) == 0) reinterpret_cast<float*>(slot + g.RBp)[c >> 3] = scale;
-            }
-          }
-          for (int k = 0; k < K; ++k) {
-            const int srow = s_self[k];
-            if (srow < 0) continue;
-            uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)srow * H * OB;
-            if constexpr (OT == WT) {
-              st_v4(orow + (int64_t)c * 16, v);
-              if constexpr (SC) {
-                if ((c & 7) == 0) p.out_scales[(int64_t)srow * (H / 128) + (c >> 3)] = scale;
-              }
-            } else {
-              float fw[EPC];  // the f32 image of what a slot would carry
-              unpack16<WT>(v, fw);
-              if constexpr (SC) {
-#pragma unroll
-                for (int i = 0; i < EPC; ++i) fw[i] = __fmul_rn(fw[i], scale);
-              }
-              store_f32_chunk<EPB_F32, EPC>(orow, (int64_t)c * EPC, fw);
-            }
-          }
+          int4 v;
+          float scale;
+          quantize(t, c, xrow, xsc, v, scale);
+          emit(c, v, scale, nd);
         }
       } else {
         // hidden not a multiple of 16: element path (scales need H % 128 == 0)
@@ -470,6 +558,8 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       __syncthreads();
     }
     LL_STAMP(p, 3);
+    commit_round();
+    __syncthreads();  // s_q
     // publish: CTA 0 writes the count words of every (local expert, src)
     // pair at every destination; then every CTA fences and flags each
     // destination (a receiver waits for all grid CTAs of all sources)
@@ -482,13 +572,14 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       }
     }
     __syncthreads();
-    if ((int)threadIdx.x < N) {
+    // (no flags to self: own rows went straight to the output and the fused
+    // receive reads its own counts from shared memory)
+    if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
       fence_scoped(sys);
       uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.disp_flag) +
                        (int64_t)p.rank * G + blockIdx.x;
       st_flag(flag, (uint64_t)tag, sys);
     }
-    ll_round_commit(p.dseq, p.drd, p.hseq, seq);
     LL_STAMP(p, 4);
   }
 
@@ -498,18 +589,33 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     LL_STAMP(p, 5);
     const int lo = p.rank * L;
     const int nloc = max(0, min(L, E - lo));
-    if (threadIdx.x == 0) s_fail = 0;
+    if (threadIdx.x == 0) {
+      s_fail = 0;
+      if (!(p.phases & kPhaseSend)) s_seq = seq_ld;
+    }
     __syncthreads();
+    if (!(p.phases & kPhaseSend)) {
+      seq = s_seq;
+      tag = ll_tag_of(seq);
+      parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+    }
+    // every CTA of every peer source (no flags from self)
     const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.disp_flag);
     for (int i = threadIdx.x; i < N * G; i += blockDim.x)
-      if (!wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
+      if (i / G != p.rank && !wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
     __syncthreads();
     if (s_fail) return;
     LL_STAMP(p, 6);
     const volatile uint64_t* ctr = reinterpret_cast<const volatile uint64_t*>(p.win + parity_off + g.disp_ctr);
     if (blockIdx.x == 0) {
       for (int i = threadIdx.x; i < L * N; i += blockDim.x) {
-        const int m = i < nloc * N ? (int)(ctr[i] & 0xFFFFF) : 0;
+        const int l = i / N, s = i - l * N;
+        int m = 0;
+        if (i < nloc * N) {
+          // own counts: this launch's routing pass (fused) or the earlier
+          // send launch's count word (split phases, stream-ordered)
+          m = (s == p.rank && s_m != nullptr) ? s_m[lo + l] : (int)(ctr[i] & 0xFFFFF);
+        }
         p.counts_i32[i] = m;
         p.counts_f32[i] = (float)m;
       }
@@ -578,23 +684,31 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
   const bool sys = p.sys;
   LL_STAMP(p, 0);
   __shared__ uint32_t s_seq;
-  if (threadIdx.x == 0) s_seq = ld_volatile_u32(p.hseq);
+  __shared__ int s_wsum[kThreads / 32];
+  // the round load is in flight while the send phase loads its counts
+  uint32_t seq_ld = 0;
+  if (threadIdx.x == 0) seq_ld = ld_round_u32(p.hseq);
+  constexpr int EPC = Elems<WT>::n;
+  const bool vec = (H & 15) == 0;
+  const int nch = vec ? H / EPC : 0;
+  // rows of this rank's own source tokens never travel: only N > 1 sends
+  const bool send = (p.phases & kPhaseSend) && N > 1;
+  const int P = L * N;
+  const int per = (P + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per;
+  int local = 0;
+  if (send) {
+    // counts of the (l, src) pairs, own-source pairs excluded
+    for (int i = i0; i < min(P, i0 + per); ++i) local += (i % N == p.rank) ? 0 : p.counts[i];
+  }
+  if (threadIdx.x == 0) s_seq = seq_ld;
   __syncthreads();
   const uint32_t seq = s_seq;
   const uint32_t tag = ll_tag_of(seq);
   const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
-  constexpr int EPC = Elems<WT>::n;
-  const bool vec = (H & 15) == 0;
-  const int nch = vec ? H / EPC : 0;
 
-  if (p.phases & kPhaseSend) {
-    __shared__ int s_wsum[kThreads / 32];
-    const int P = L * N;
-    // block-wide exclusive scan of the (l, src) counts
-    const int per = (P + blockDim.x - 1) / blockDim.x;
-    const int i0 = threadIdx.x * per;
-    int local = 0;
-    for (int i = i0; i < min(P, i0 + per); ++i) local += p.counts[i];
+  if (send) {
+    // block-wide exclusive scan of the remote (l, src) counts
     int incl = local;
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -607,7 +721,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     int run = wbase + incl - local;
     for (int i = i0; i < min(P, i0 + per); ++i) {
       s_pre[i] = run;
-      run += p.counts[i];
+      run += (i % N == p.rank) ? 0 : p.counts[i];
     }
     if (threadIdx.x == blockDim.x - 1) s_pre[P] = run;
     __syncthreads();
@@ -659,7 +773,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     }
     __syncthreads();
     LL_STAMP(p, 2);
-    if ((int)threadIdx.x < N) {
+    if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
       fence_scoped(sys);
       uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.comb_flag) +
                        (int64_t)p.rank * G + blockIdx.x;
@@ -672,71 +786,101 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     __shared__ float s_w[kMaxTopK];
     __shared__ int s_fail;
     LL_STAMP(p, 4);
+    const uint8_t* slots = p.win + parity_off + g.comb_slot;
+    constexpr int kSeg = 64;  // 16-B chunks per warp task (2 per lane)
+    const int segs = vec ? (nch + kSeg - 1) / kSeg : 0;
+    const int tasks = p.b * segs;
+    const int tstride = gridDim.x * nw;
+    int task = warp * gridDim.x + blockIdx.x;
+    // lane k of a warp task: row k of the token — this rank's own expert row
+    // (read in place from the expert output) or its combine slot — and w_k;
+    // the first task's rows are resolved before the flag wait
+    int my_self = -1;
+    float my_w = 0.0f;
+    if (vec && task < tasks && lane < K) {
+      const int t = task / segs;
+      my_self = p.self_row ? p.self_row[(int64_t)t * K + lane] : -1;
+      my_w = p.w[(int64_t)t * K + lane];
+    }
     if (threadIdx.x == 0) s_fail = 0;
     __syncthreads();
     const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.comb_flag);
     for (int i = threadIdx.x; i < N * G; i += blockDim.x)
-      if (!wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
+      if (i / G != p.rank && !wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
     __syncthreads();
     if (s_fail) return;
     LL_STAMP(p, 5);
-    const uint8_t* slots = p.win + parity_off + g.comb_slot;
     if (vec) {
-      // warp tasks: (token, 64-chunk segment); each lane reduces 2 chunks
-      // with all K slot loads of a chunk in flight
-      constexpr int kSeg = 64;
-      const int segs = (nch + kSeg - 1) / kSeg;
-      const int tasks = p.b * segs;
-      for (int task = warp * gridDim.x + blockIdx.x; task < tasks; task += gridDim.x * nw) {
+      for (; task < tasks; task += tstride) {
         const int t = task / segs, sg = task - t * segs;
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
-        const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
-        const float* wt = p.w + (int64_t)t * K;
-        // lane k: row k of this token is this rank's own expert row (read in
-        // place from the expert output, wire-rounded) or a combine slot
-        const int my_self = (p.self_row && lane < K) ? p.self_row[(int64_t)t * K + lane] : -1;
+        const int cbase = sg * kSeg + lane;
+        const bool ok0 = cbase < nch, ok1 = cbase + 32 < nch;
+        const uint8_t* my_row =
+            my_self >= 0 ? reinterpret_cast<const uint8_t*>(p.y) + (int64_t)my_self * H * dtype_width(IT)
+                         : slots + ((int64_t)t * K + lane) * g.comb_stride;
+        const bool my_in_y = my_self >= 0;
+        float acc0[EPC], acc1[EPC];
 #pragma unroll
-        for (int h = 0; h < kSeg / 32; ++h) {
-          if (sg * kSeg + h * 32 >= nch) break;
-          const int c = sg * kSeg + h * 32 + lane;
-          const bool ok = c < nch;
-          float acc[EPC];
+        for (int i = 0; i < EPC; ++i) acc0[i] = acc1[i] = 0.0f;
+        for (int k0 = 0; k0 < K; k0 += 8) {
+          // all row pointers first, then 16 loads in flight per lane
+          const uint8_t* rp[8];
+          bool iny[8];
 #pragma unroll
-          for (int i = 0; i < EPC; ++i) acc[i] = 0.0f;
-          for (int k0 = 0; k0 < K; k0 += 8) {
-            int4 v[8];
+          for (int u = 0; u < 8; ++u) {
+            rp[u] = reinterpret_cast<const uint8_t*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_row), (k0 + u) & 31));
+            iny[u] = __shfl_sync(0xffffffffu, my_in_y, (k0 + u) & 31);
+          }
+          int4 v0[8], v1[8];
+          if constexpr (IT == WT) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               if (k0 + u < K) {
-                const int sr = __shfl_sync(0xffffffffu, my_self, (k0 + u) & 31);
-                if (!ok) continue;
-                if (sr >= 0) {
-                  const uint8_t* yrow = reinterpret_cast<const uint8_t*>(p.y) + (int64_t)sr * H * dtype_width(IT);
-                  if constexpr (IT == WT) {
-                    v[u] = ld_nc_v4(yrow + (int64_t)c * 16);
-                  } else {
-                    float f[EPC];
-                    load_elems_vec<IT, EPC>(yrow, (int64_t)c * EPC, f);
-                    v[u] = pack16<WT>(f);
-                  }
+                if (ok0) v0[u] = ld_weak_v4(rp[u] + (int64_t)cbase * 16);
+                if (ok1) v1[u] = ld_weak_v4(rp[u] + (int64_t)(cbase + 32) * 16);
+              }
+            }
+          } else {
+            // own rows hold the input dtype: rounded through the wire dtype
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              if (k0 + u < K) {
+                if (iny[u]) {
+                  float f[EPC];
+                  if (ok0) { load_elems_vec<IT, EPC>(rp[u], (int64_t)cbase * EPC, f); v0[u] = pack16<WT>(f); }
+                  if (ok1) { load_elems_vec<IT, EPC>(rp[u], (int64_t)(cbase + 32) * EPC, f); v1[u] = pack16<WT>(f); }
                 } else {
-                  v[u] = ld_weak_v4(tsl + (int64_t)(k0 + u) * g.comb_stride + (int64_t)c * 16);
+                  if (ok0) v0[u] = ld_weak_v4(rp[u] + (int64_t)cbase * 16);
+                  if (ok1) v1[u] = ld_weak_v4(rp[u] + (int64_t)(cbase + 32) * 16);
                 }
               }
             }
+          }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              if (k0 + u < K) {
-                float y[EPC];
-                unpack16<WT>(v[u], y);
-                const float wk = wt[k0 + u];
+          for (int u = 0; u < 8; ++u) {
+            if (k0 + u < K) {
+              const float wk = __shfl_sync(0xffffffffu, my_w, (k0 + u) & 31);
+              float y[EPC];
+              unpack16<WT>(v0[u], y);
 #pragma unroll
-                for (int i = 0; i < EPC; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(wk, y[i]));
-              }
+              for (int i = 0; i < EPC; ++i) acc0[i] = __fadd_rn(acc0[i], __fmul_rn(wk, y[i]));
+              unpack16<WT>(v1[u], y);
+#pragma unroll
+              for (int i = 0; i < EPC; ++i) acc1[i] = __fadd_rn(acc1[i], __fmul_rn(wk, y[i]));
             }
           }
-          if (ok) store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, acc);
         }
+        // the next task's rows (their loads overlap these stores)
+        const int nt = task + tstride;
+        if (nt < tasks && lane < K) {
+          const int t2 = nt / segs;
+          my_self = p.self_row ? p.self_row[(int64_t)t2 * K + lane] : -1;
+          my_w = p.w[(int64_t)t2 * K + lane];
+        }
+        if (ok0) store_f32_chunk<OT, EPC>(orow, (int64_t)cbase * EPC, acc0);
+        if (ok1) store_f32_chunk<OT, EPC>(orow, (int64_t)(cbase + 32) * EPC, acc1);
       }
     } else {
       for (int t = blockIdx.x; t < p.b; t += gridDim.x) {

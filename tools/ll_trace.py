@@ -18,7 +18,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2603_13606_b200 import _lib  # noqa: E402
 
-DISP = ["start", "seq", "routed", "stored", "published", "recv", "waited", "copied", "prefixed", "hdr"]
+DISP = ["start", "seq", "routed", "stored", "published", "recv", "waited", "copied", "zeroed", "hdr",
+        "rt-loop", "t0-seq", "t0-arrive", "pass1"]
 COMB = ["start", "prefix", "sent", "published", "recv", "waited", "reduced"]
 
 
@@ -39,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", type=int, default=128)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--flush", default="write", choices=["write", "read", "none"])
     a = ap.parse_args()
     world, rank = bench.init_dist()
     st = bench.LLStep(world, rank, a.tokens)
@@ -51,7 +53,10 @@ def main():
     for rep in range(a.reps):
         tr_d.zero_()
         tr_c.zero_()
-        flush.zero_()
+        if a.flush == "write":
+            flush.zero_()
+        elif a.flush == "read":
+            flush.view(torch.int32).sum()
         bench.barrier(world)
         h = g.create_handle(st.topk)
         _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(tr_d.data_ptr()))
@@ -62,7 +67,7 @@ def main():
         h.destroy()
         torch.cuda.synchronize()
         if rank == 0:
-            print(f"== rep {rep} (rank 0 of {world})")
+            print(f"== rep {rep} (rank 0 of {world}, L2 flush: {a.flush})")
             show("dispatch", tr_d, DISP)
             show("combine", tr_c, COMB)
         bench.barrier(world)
