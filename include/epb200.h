@@ -183,6 +183,9 @@ typedef struct epb_ll_combine_args {
   void* out;                /*   [b, H] f32|bf16                             */
   int32_t out_dtype;
   const int32_t* self_row;  /* [b, K] from the dispatch (own rows read in place) */
+  const int64_t* topk;      /* [b, K] routing of the handle; required by the
+                               legacy layout (combine slot e*B + t,
+                               ll.py:433-436), unused by the optimized one  */
 } epb_ll_combine_args;
 
 /* K4a + K4b: LL combine (ll.py:404-507) */

@@ -50,7 +50,8 @@ class LLCombineArgs(ctypes.Structure):
     _fields_ = [("expert_out", ctypes.c_void_p), ("in_dtype", ctypes.c_int32),
                 ("counts_i32", ctypes.c_void_p), ("src_info", ctypes.c_void_p),
                 ("weights", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
-                ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("self_row", ctypes.c_void_p)]
+                ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("self_row", ctypes.c_void_p),
+                ("topk", ctypes.c_void_p)]
 
 
 class HTDispatchArgs(ctypes.Structure):

@@ -655,7 +655,7 @@ class EpHandle:
             o, back = self._dev_out(out, full=True)
             a = _lib.LLCombineArgs(y.data_ptr(), rows_in.dtype.code, self._counts_i32.data_ptr(),
                                    self._src_info.data_ptr(), w.data_ptr(), b, o.data_ptr(), out.dtype.code,
-                                   self._self_row.data_ptr())
+                                   self._self_row.data_ptr(), self.routing.data_ptr() if b else None)
             self._ll_cargs = a
             self._staged = (out, o, back, w, y)
             if send_only:

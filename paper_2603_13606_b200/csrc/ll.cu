@@ -26,6 +26,8 @@
 // validation, counts and prefix ranks are one parallel shared-memory pass;
 // flags replace atomics; copies keep 8 x 16 B loads in flight per lane;
 // fences/flags use GPU scope when every rank lives on this GPU.
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -105,6 +107,32 @@ EPB_DEV void warp_copy16(const uint8_t* src, uint8_t* dst, int c0, int c1, int l
       if (c < c1) st_weak_v4(dst + (int64_t)c * 16, v[u]);
     }
   }
+}
+
+// Block-wide exclusive scan of val(0..P-1) into s_pre[0..P] (s_pre[P] =
+// total); all threads call it; ends with a block barrier.
+template <class F>
+EPB_DEV void block_exclusive_scan(int P, F val, int* s_pre, int* s_wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (P + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per;
+  int local = 0;
+  for (int i = i0; i < min(P, i0 + per); ++i) local += val(i);
+  int incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  int run = incl - local;
+  for (int w2 = 0; w2 < warp; ++w2) run += s_wsum[w2];
+  for (int i = i0; i < min(P, i0 + per); ++i) {
+    s_pre[i] = run;
+    run += val(i);
+  }
+  if (threadIdx.x == blockDim.x - 1) s_pre[P] = run;
+  __syncthreads();
 }
 
 template <int XT, int EPC>
@@ -268,6 +296,9 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     s_m = reinterpret_cast<int*>(s_dbits + N * W);                             // [E]
     int* s_q = s_m + E;                                                        // [N]
     __shared__ int s_bad, s_nd;
+    // per destination entry: rank and absolute slot index in its window
+    // (optimized: one slot per (token, dst) at src*B + j; legacy: one slot
+    // per (token, expert) at ((e - dL)*N + src)*B + i)
     __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks];
     __shared__ int s_self[kMaxTopK];  // output row of (t, k) for this rank's own experts, else -1
     __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
@@ -376,7 +407,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       s_q[d] = q;
     }
     const uint64_t slot_off = parity_off + g.disp_slot;
-    const int64_t slot_base = (int64_t)p.rank * B;
+    const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
     // one token chunk: input (prefetched for the CTA's first token) ->
     // f32 -> optional block-128 FP8 scale (x / scale, correctly rounded) ->
     // 16-B wire image
@@ -417,7 +448,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     // chunk c to every destination slot and every own-expert output row
     auto emit = [&](int c, const int4& v, float scale, int nd) {
       for (int i = 0; i < nd; ++i) {
-        uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
+        uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (int64_t)s_j[i] * g.slot_stride;
         st_na_v4(slot + (int64_t)c * 16, v);
         if constexpr (SC) {
           if ((c & 7) == 0) reinterpret_cast<float*>(slot + g.RBp)[c >> 3] = scale;
@@ -486,9 +517,11 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         // to the expert-major output (and the combine reads them in place)
         const bool mine = lane < K && d == p.rank;
         bool first = lane < K && !mine;
-        for (int j = 0; j < K; ++j) {
-          const int dj = __shfl_sync(0xffffffffu, d, j);
-          first &= !(j < lane && dj == d);
+        if (!legacy) {  // optimized: one slot per destination (dedup)
+          for (int j = 0; j < K; ++j) {
+            const int dj = __shfl_sync(0xffffffffu, d, j);
+            first &= !(j < lane && dj == d);
+          }
         }
         const unsigned fm = __ballot_sync(0xffffffffu, first);
         if (lane < K) {
@@ -501,7 +534,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           if (first) {
             const int pos = __popc(fm & ((1u << lane) - 1u));
             s_dst[pos] = d;
-            s_j[pos] = cj;
+            s_j[pos] = legacy ? ((e - d * L) * N + p.rank) * B + ci : p.rank * B + cj;
           }
         }
         if (lane == 0) {
@@ -515,7 +548,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const int nd = s_nd;
       for (int w = threadIdx.x; w < 2 + 2 * K; w += blockDim.x)
         for (int i = 0; i < nd; ++i) {
-          uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
+          uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (int64_t)s_j[i] * g.slot_stride;
           reinterpret_cast<uint32_t*>(slot + g.RBp + g.SBp)[w] = s_hdr[w];
         }
       if (split) {
@@ -541,7 +574,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
             if (xsc != nullptr) f = __fmul_rn(f, xsc[el >> 7]);
           }
           for (int i = 0; i < nd; ++i) {
-            uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (slot_base + s_j[i]) * g.slot_stride;
+            uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (int64_t)s_j[i] * g.slot_stride;
             store_elem(slot, WT, el, f);
           }
           for (int k = 0; k < K; ++k) {
@@ -621,6 +654,40 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       }
     }
     if (nloc == 0) return;
+    const int ob = (OT == EPB_F32 ? 4 : dtype_width(OT));
+    const int64_t orow_bytes = (int64_t)H * ob;
+    const int nw = blockDim.x >> 5;
+    if (g.layout == EPB_LAYOUT_LEGACY) {
+      // legacy (ll.py:362-376): slot (l*N + r)*B + i holds recv[l, r*B + i]
+      // — the same linear index; rows of remote pairs, prefix over pairs
+      __shared__ int s_wsum[kThreads / 32];
+      int* s_pp = smem;  // [L*N + 1] (the send phase is done with it)
+      __syncthreads();
+      block_exclusive_scan(nloc * N, [&](int i) { return i % N == p.rank ? 0 : (int)(ctr[i] & 0xFFFFF); }, s_pp,
+                           s_wsum);
+      const int rows = s_pp[nloc * N];
+      for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * rows; f2 += gridDim.x * nw) {
+        const int r = f2 >> 1, half = f2 & 1;
+        int lo_i = 0, hi_i = nloc * N;  // largest pair with s_pp[pair] <= r
+        while (hi_i - lo_i > 1) {
+          const int mid = (lo_i + hi_i) >> 1;
+          if (s_pp[mid] <= r) lo_i = mid; else hi_i = mid;
+        }
+        const int64_t lin = (int64_t)lo_i * B + (r - s_pp[lo_i]);
+        const uint8_t* slot = p.win + parity_off + g.disp_slot + lin * g.slot_stride;
+        if (lane == 0 && half == 0) {
+          const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
+          const int e = lo + lo_i / N;
+          int k = 0;
+          while (k < K - 1 && (int)hdr[2 + k] != e) ++k;
+          p.src_info[lin] = (int32_t)(hdr[0] * K + k);
+        }
+        ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + lin * orow_bytes,
+                                SC ? p.out_scales + lin * (H / 128) : nullptr, lane, half, 2);
+      }
+      LL_STAMP(p, 7);
+      return;
+    }
     // own rows were placed by the send phase; only remote slots remain
     if ((int)threadIdx.x < N) s_rq[threadIdx.x] = (int)threadIdx.x == p.rank ? 0 : (int)((ctr[threadIdx.x] >> 20) & 0xFFFFF);
     __syncthreads();
@@ -631,9 +698,6 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     }
     __syncthreads();
     const int items = s_pre[N] * K;
-    const int nw = blockDim.x >> 5;
-    const int ob = (OT == EPB_F32 ? 4 : dtype_width(OT));
-    const int64_t orow_bytes = (int64_t)H * ob;
     // items = (slot, k, half row); CTA-major order spreads them over every SM
     for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * items; f2 += gridDim.x * nw) {
       const int f = f2 >> 1, half = f2 & 1;
@@ -662,6 +726,7 @@ struct LLComb {
   const int32_t* counts;
   const int32_t* src_info;
   const int32_t* self_row;  // [b*K] from the dispatch: rows of own experts are read in place
+  const int64_t* topk;      // [b*K] routing (legacy layout: slot e*B + t)
   const float* w;
   void* out;
   const uint32_t* hseq;
@@ -742,7 +807,11 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
       if (s == p.rank) continue;  // own tokens: the home reads these rows in place
       const int64_t row = (int64_t)l * N * B + (int64_t)s * B + i;
       const int info = p.src_info[row];
-      uint8_t* dst = peer_base(p.peers, s) + parity_off + g.comb_slot + (int64_t)info * g.comb_stride;
+      // optimized slot t*K + k (layout.py:108-110); legacy e*B + t (ll.py:433-436)
+      const int64_t cs = g.layout == EPB_LAYOUT_LEGACY
+                             ? (int64_t)(p.rank * L + l) * B + (int64_t)(((uint64_t)info * g.Kmagic) >> 32)
+                             : (int64_t)info;
+      uint8_t* dst = peer_base(p.peers, s) + parity_off + g.comb_slot + cs * g.comb_stride;
       const uint8_t* yrow = reinterpret_cast<const uint8_t*>(p.y) + row * H * dtype_width(IT);
       if (vec) {
         const int c0 = q * part, c1 = min(nch, c0 + part);
@@ -795,13 +864,17 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // lane k of a warp task: row k of the token — this rank's own expert row
     // (read in place from the expert output) or its combine slot — and w_k;
     // the first task's rows are resolved before the flag wait
-    int my_self = -1;
+    const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
+    int my_self = -1, my_slot = 0;
     float my_w = 0.0f;
-    if (vec && task < tasks && lane < K) {
-      const int t = task / segs;
-      my_self = p.self_row ? p.self_row[(int64_t)t * K + lane] : -1;
-      my_w = p.w[(int64_t)t * K + lane];
-    }
+    auto fetch = [&](int tk) {  // lane k's row of token tk
+      if (lane < K) {
+        my_self = p.self_row ? p.self_row[(int64_t)tk * K + lane] : -1;
+        my_w = p.w[(int64_t)tk * K + lane];
+        my_slot = legacy ? (int)p.topk[(int64_t)tk * K + lane] * B + tk : tk * K + lane;
+      }
+    };
+    if (vec && task < tasks) fetch(task / segs);
     if (threadIdx.x == 0) s_fail = 0;
     __syncthreads();
     const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.comb_flag);
@@ -818,7 +891,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         const bool ok0 = cbase < nch, ok1 = cbase + 32 < nch;
         const uint8_t* my_row =
             my_self >= 0 ? reinterpret_cast<const uint8_t*>(p.y) + (int64_t)my_self * H * dtype_width(IT)
-                         : slots + ((int64_t)t * K + lane) * g.comb_stride;
+                         : slots + (int64_t)my_slot * g.comb_stride;
         const bool my_in_y = my_self >= 0;
         float acc0[EPC], acc1[EPC];
 #pragma unroll
@@ -874,11 +947,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         }
         // the next task's rows (their loads overlap these stores)
         const int nt = task + tstride;
-        if (nt < tasks && lane < K) {
-          const int t2 = nt / segs;
-          my_self = p.self_row ? p.self_row[(int64_t)t2 * K + lane] : -1;
-          my_w = p.w[(int64_t)t2 * K + lane];
-        }
+        if (nt < tasks) fetch(nt / segs);
         if (ok0) store_f32_chunk<OT, EPC>(orow, (int64_t)cbase * EPC, acc0);
         if (ok1) store_f32_chunk<OT, EPC>(orow, (int64_t)(cbase + 32) * EPC, acc1);
       }
@@ -888,7 +957,6 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         if ((int)threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
         __syncthreads();
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
-        const uint8_t* tsl = slots + (int64_t)t * K * g.comb_stride;
         for (int el = threadIdx.x; el < H; el += blockDim.x) {
           float acc = 0.0f;
           for (int k = 0; k < K; ++k) {
@@ -900,7 +968,8 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
                          load_elem(reinterpret_cast<const uint8_t*>(p.y) + (int64_t)sr * H * dtype_width(IT), IT, el));
               y = load_elem(&wire, WT, 0);
             } else {
-              y = load_elem(tsl + (int64_t)k * g.comb_stride, WT, el);
+              const int64_t cs = legacy ? p.topk[(int64_t)t * K + k] * B + t : (int64_t)t * K + k;
+              y = load_elem(slots + cs * g.comb_stride, WT, el);
             }
             acc = __fadd_rn(acc, __fmul_rn(s_w[k], y));
           }
@@ -1019,8 +1088,6 @@ int check_ll(epb_group* g, int phases) {
   if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
   if (g->cfg.algorithm != EPB_LL) return fail(EPB_HANDLE_STATE_ERROR, "group is not LL");
   if (!g->peers_ready) return fail(EPB_HANDLE_STATE_ERROR, "peer windows not mapped");
-  if (g->cfg.layout != EPB_LAYOUT_OPTIMIZED)
-    return fail(EPB_INVALID_ARGUMENT, "legacy LL layout is not implemented on the GPU path");
   if (phases < 1 || phases > 3) return fail(EPB_INVALID_ARGUMENT, "phases must be 1 (send), 2 (recv) or 3");
   return EPB_OK;
 }
@@ -1058,7 +1125,9 @@ int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases, const epb_ll_d
   p.sys = g->sys_scope;
   const int E = g->ll.E, N = g->ll.N, K = g->ll.K;
   const size_t W = (size_t)(b + 31) / 32;
-  const size_t smem = (phases & kPhaseSend) ? sizeof(int) * ((size_t)b * K + (E + N) * W + E + N) : 0;
+  size_t smem = (phases & kPhaseSend) ? sizeof(int) * ((size_t)b * K + (E + N) * W + E + N) : 0;
+  if ((phases & kPhaseRecv) && g->cfg.layout == EPB_LAYOUT_LEGACY)  // receive: pair prefix [L*N + 1]
+    smem = std::max(smem, sizeof(int) * ((size_t)g->ll.L * N + 1));
   if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "LL batch too large for the fused dispatch kernel");
   cudaStream_t s = as_stream(stream);
   cudaError_t e;
@@ -1087,8 +1156,10 @@ int epb_ll_combine(epb_group* g, const uint32_t* hseq, int32_t phases, const epb
   }
   if (a->in_dtype != EPB_F32 && a->in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
   LLComb p;
+  if ((phases & kPhaseRecv) && g->cfg.layout == EPB_LAYOUT_LEGACY && b > 0 && !a->topk)
+    return fail(EPB_INVALID_ARGUMENT, "legacy layout combine needs the routing (topk)");
   p.y = a->expert_out; p.counts = a->counts_i32; p.src_info = a->src_info; p.self_row = a->self_row;
-  p.w = a->weights; p.out = a->out;
+  p.topk = a->topk; p.w = a->weights; p.out = a->out;
   p.hseq = hseq; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err; p.trace = g->trace;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;

@@ -46,7 +46,7 @@ def dispatch_inputs(cfg, tokens, weights, mode="reference"):
 
 
 def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="reference",
-           wire_out=False, bf16_expert=False, rounds=1):
+           wire_out=False, bf16_expert=False, rounds=1, layout="optimized"):
     """Returns per rank dict(recv, counts, out, recv_total)."""
     n = cfg.num_ranks
     bmax, h = cfg.max_tokens_per_rank, cfg.hidden
@@ -54,7 +54,7 @@ def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="referen
     fabric = ep.Fabric(ep.NodeTopology(n, cfg.ranks_per_node))
 
     def body(rank):
-        g = ep.create_group(fabric, rank, cfg)
+        g = ep.create_group(fabric, rank, cfg, layout=layout)
         res = []
         try:
             for _ in range(rounds):

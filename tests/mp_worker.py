@@ -30,10 +30,11 @@ def bf16r(x):
     return oc.bf16_to_f32(oc.f32_to_bf16(x))
 
 
-def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, staged, mode, rounds=1):
+def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, staged, mode, rounds=1,
+            layout="optimized"):
     cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, bmax, dtype, scales, combine_dtype=combine_dtype)
     fab = ep.ProcessFabric(ep.NodeTopology(world, world))
-    g = ep.create_group(fab, rank, cfg)
+    g = ep.create_group(fab, rank, cfg, layout=layout)
     ell = cfg.experts_per_rank
     for rnd in range(rounds):
         wl = owl.make_workload(e, world, bmax, k, h, seed + rnd)
@@ -157,6 +158,10 @@ def main():
         ("ll staged bf16 uneven", lambda: ll_case(world, rank, 3 * world + 1, 3, 256, 12, ep.Dtype.BF16, False, None,
                                                   3, True, "ref", rounds=3)),
         ("ll pipelined parities", lambda: ll_pipelined(world, rank)),
+        ("ll legacy layout c2 hot path", lambda: ll_case(world, rank, 256, 8, 7168, 64, ep.Dtype.FP8, True,
+                                                          ep.Dtype.BF16, 6, False, "bf16", rounds=2, layout="legacy")),
+        ("ll legacy layout staged uneven", lambda: ll_case(world, rank, 3 * world + 1, 3, 256, 12, ep.Dtype.BF16, False,
+                                                            None, 7, True, "ref", rounds=3, layout="legacy")),
         ("ht bf16 single node", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 4, False)),
         ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
     ]

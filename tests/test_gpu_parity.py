@@ -11,6 +11,7 @@ from oracle import ht as oht
 from oracle import ll as oll
 from oracle import workload as owl
 from tests._golden import HT_NAMES, LL_NAMES, ht_case, ll_case, load
+from paper_2603_13606_b200.harness import run_ranks
 from tests.gpu_util import bf16_round, make_cfg, run_ht, run_ll
 
 pytestmark = pytest.mark.gpu
@@ -193,6 +194,64 @@ def test_ll_parity_reuse_many_rounds():
     for r in range(2):
         for rnd in res[r]:
             np.testing.assert_array_equal(rnd["out"], comb[r])
+
+
+# ---------------------------------------------------------------------------
+# LL legacy layout (layout.py:146-194, ll.py:271-287, :362-376): per-(expert,
+# src) dispatch slots and per-(expert, token) combine slots, same outputs
+# ("layouts agree bitwise", test_ll.py:307-317)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["ll_f32_n4", "ll_fp8s", "ll_uneven", "ll_n1"])
+@pytest.mark.parametrize("staged", [False, True])
+def test_ll_legacy_layout_matches_reference_golden(name, staged):
+    c = ll_case(name)
+    cfg = make_cfg("ll", c["n"], c["rpn"], c["e"], c["bmax"], c["k"], c["h"], c["dtype"], c["scales"])
+    res = run_ll(cfg, c["tokens"], c["routing"], c["weights"], owl.EXPERT_STUBS[c["stub"]], staged=staged,
+                 layout="legacy")
+    g = c["g"]
+    for r in range(c["n"]):
+        np.testing.assert_array_equal(res[r]["counts"], g[f"counts{r}"])
+        pos = g[f"recvpos{r}"]
+        got = res[r]["recv"][pos[:, 0], pos[:, 1] * c["bmax"] + pos[:, 2]] if len(pos) else \
+            np.zeros((0, c["h"]), np.float32)
+        np.testing.assert_array_equal(got, g[f"recvrows{r}"])
+        np.testing.assert_array_equal(res[r]["out"], g[f"out{r}"])
+
+
+@pytest.mark.parametrize("n", [1, 4])
+def test_ll_legacy_layout_c2_hot_path(n):
+    cfg = ep.EpConfig(ep.Algorithm.LL, n, n, 256, 8, 7168, 32, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
+    wl = owl.make_workload(256, n, 32, 8, 7168, seed=40 + n)
+    wl.tokens = [bf16_round(t) for t in wl.tokens]
+    res = run_ll(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale, mode="bf16", wire_out=True,
+                 bf16_expert=True, layout="legacy", rounds=3)
+    d, comb = _ll_oracle(cfg, wl, owl.expert_scale, bf16_expert=True)
+    for rnd in range(3):
+        _check_ll(cfg, [res[r][rnd] for r in range(n)], d, comb)
+
+
+def test_ll_legacy_window_is_the_reference_footprint():
+    from oracle import layout as olay
+    cfg = ep.EpConfig(ep.Algorithm.LL, 2, 2, 64, 8, 1024, 16, ep.Dtype.FP8, True)
+    fabric = ep.Fabric(ep.NodeTopology(2, 2))
+
+    def body(rank):
+        out = {}
+        for lay in ("optimized", "legacy"):
+            g = ep.create_group(fabric, rank, cfg, layout=lay)
+            out[lay] = g.buffer_bytes
+            g.destroy()
+        return out
+
+    try:
+        res = run_ranks(2, body, on_error=fabric.shutdown)
+    finally:
+        fabric.shutdown()
+    for lay in ("optimized", "legacy"):
+        assert res[0][lay] == olay.ll_window_bytes(64, 2, 16, 8, 1024, "fp8", True, lay)
+    assert res[0]["legacy"] > res[0]["optimized"]
 
 
 @pytest.mark.parametrize("n,rpn", [(2, 2), (8, 8), (8, 2)])
