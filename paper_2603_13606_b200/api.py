@@ -30,6 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import stats as _stats
 from .core import (FP8_BLOCK, Algorithm, Dtype, EpConfig, EpError, ErrorCode, NDTensor,
                    TensorTag, raise_status)
 
@@ -107,12 +108,21 @@ class LLDispatchResult:
     src_info: torch.Tensor      # [L, N*B] int32: t*K + k of each valid row
     scales: Optional[torch.Tensor] = None
     _total: Optional[int] = None
+    _stats_fn: Optional[Callable] = None
+    _stats: object = None
 
     @property
     def recv_total(self) -> int:
         if self._total is None:
             self._total = int(self.counts.sum().item())
         return self._total
+
+    @property
+    def stats(self):
+        """LLStats of this dispatch (ll.py:39-55), computed on demand."""
+        if self._stats is None and self._stats_fn is not None:
+            self._stats = self._stats_fn()
+        return self._stats
 
 
 @dataclass
@@ -123,6 +133,15 @@ class HTDispatchResult:
     meta_m: np.ndarray          # [N, E] tokens_per_expert
     meta_q: np.ndarray          # [N, N] records_per_pair
     recv_total: int
+    _stats_fn: Optional[Callable] = None
+    _stats: object = None
+
+    @property
+    def stats(self):
+        """HTStats of this dispatch (ht.py:57-74), computed on demand."""
+        if self._stats is None and self._stats_fn is not None:
+            self._stats = self._stats_fn()
+        return self._stats
 
 
 class EpGroup:
@@ -580,7 +599,8 @@ class EpHandle:
             out_scales.view().copy_(out_s)
         if back_c:
             out_counts.view().copy_(cnt_f)
-        self._dispatch_result = LLDispatchResult(out_t, self._counts_i32, self._src_info, out_s)
+        self._dispatch_result = LLDispatchResult(out_t, self._counts_i32, self._src_info, out_s,
+                                                 _stats_fn=self._ll_dispatch_stats)
         self._keep_alive = None
         self.state = HandleState.DISPATCHED
 
@@ -616,7 +636,7 @@ class EpHandle:
         out_counts.view().copy_(meta["counts_dev"])
         self._round_open = False
         self._dispatch_result = HTDispatchResult(out_t, origin[:total], origin_w[:total], meta["m"],
-                                                 meta["q"], total)
+                                                 meta["q"], total, _stats_fn=self._ht_dispatch_stats)
         self.state = HandleState.DISPATCHED
 
     # -- combine ------------------------------------------------------------------
@@ -679,7 +699,7 @@ class EpHandle:
             g.check()
         if back:
             out.view().copy_(o)
-        self._combine_stats = {"op": "combine"}
+        self._combine_stats = None
         self.state = HandleState.COMBINED
 
     def _ht_combine(self, y, y_dtype, w, out) -> None:
@@ -704,7 +724,7 @@ class EpHandle:
             g.check()
         if back:
             out.view().copy_(o)
-        self._combine_stats = {"op": "combine"}
+        self._combine_stats = None
         self.state = HandleState.COMBINED
 
     def complete(self) -> None:
@@ -745,7 +765,33 @@ class EpHandle:
 
     @property
     def combine_stats(self):
+        """LLStats / HTStats of the last combine (ll.py:427-459,
+        ht.py:616-735), computed on demand from the receive plan."""
+        if self._combine_stats is None and self.state is HandleState.COMBINED:
+            self._combine_stats = self._combine_stats_now()
         return self._combine_stats
+
+    # -- stats (host-side accounting, never on the kernel path) -------------------
+    def _routing_np(self) -> np.ndarray:
+        return self.routing.detach().cpu().numpy().reshape(-1, self.config.top_k)
+
+    def _ll_dispatch_stats(self):
+        g = self.group
+        return _stats.ll_dispatch_stats(self.config, g.layout, self._routing_np(), g.buffer_bytes)
+
+    def _ht_dispatch_stats(self):
+        g = self.group
+        return _stats.ht_dispatch_stats(self.config, g.rank, self._routing_np(), self._dispatch_result.meta_q,
+                                        g.buffer_bytes)
+
+    def _combine_stats_now(self):
+        g, cfg = self.group, self.config
+        res = self._dispatch_result
+        if cfg.algorithm is Algorithm.HT:
+            return _stats.ht_combine_stats(cfg, g.rank, self._routing_np(), res.recv_total, res.meta_m,
+                                           g.buffer_bytes)
+        return _stats.ll_combine_stats(cfg, g.layout, g.rank, res.counts.cpu().numpy(), res.src_info.cpu().numpy(),
+                                       g.buffer_bytes)
 
     def destroy(self) -> None:
         """Retire the handle; legal only with no round in flight."""

@@ -54,6 +54,17 @@ HT_CASES = {
 }
 
 
+# issue-side accounting (ll.py:39-55, ht.py:57-74); fifo_stalls is
+# scheduling-dependent and never compared
+LL_STAT_FIELDS = ("bytes_put", "msgs", "signals", "slots_used", "buffer_bytes")
+HT_STAT_FIELDS = ("bytes_put", "msgs", "signals", "slots_used", "buffer_bytes", "inter_node_msgs",
+                  "intra_node_msgs")
+
+
+def _stat_vec(st, fields):
+    return np.array([getattr(st, f) for f in fields], dtype=np.int64)
+
+
 def make_ll(core, harness, layout_mod, oracle, name, spec):
     n, rpn, e, bmax, b, k, h, dt, scales, stub, seed = spec
     cfg = core.EpConfig(algorithm=core.Algorithm.LL, num_ranks=n, ranks_per_node=rpn,
@@ -83,6 +94,14 @@ def make_ll(core, harness, layout_mod, oracle, name, spec):
         out[f"recvrows{r}"] = np.array(rows, dtype=np.float32).reshape(-1, h)
         out[f"out{r}"] = res.per_rank[r].tokens_out
         out[f"recv_total{r}"] = np.array(d.recv_total)
+        out[f"dstats{r}"] = _stat_vec(d.stats, LL_STAT_FIELDS)
+        out[f"cstats{r}"] = _stat_vec(res.per_rank[r].combine_stats, LL_STAT_FIELDS)
+    # the legacy layout: same outputs (test_ll.py:307-317), its own stats
+    leg = harness.run_ll_round(cfg, "legacy", wl, oracle.EXPERT_STUBS[stub], delay_seed=seed)
+    for r in range(n):
+        assert np.array_equal(leg.per_rank[r].tokens_out, res.per_rank[r].tokens_out)
+        out[f"dstats_leg{r}"] = _stat_vec(leg.per_rank[r].dispatch.stats, LL_STAT_FIELDS)
+        out[f"cstats_leg{r}"] = _stat_vec(leg.per_rank[r].combine_stats, LL_STAT_FIELDS)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
 
 
@@ -109,6 +128,8 @@ def make_ht(core, harness, layout_mod, oracle, name, spec):
             out["m"] = d.meta.tokens_per_expert
             out["q"] = d.meta.records_per_pair
         out[f"recv_total{r}"] = np.array(d.meta.recv_total)
+        out[f"dstats{r}"] = _stat_vec(d.stats, HT_STAT_FIELDS)
+        out[f"cstats{r}"] = _stat_vec(res.per_rank[r].combine_stats, HT_STAT_FIELDS)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
 
 

@@ -88,7 +88,8 @@ def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="referen
                 if staged:
                     hd.complete()
                 res.append(dict(recv=recv, counts=counts, out=comb_out.read_f32(),
-                                recv_total=hd.get_num_recv_tokens(), rows=rows))
+                                recv_total=hd.get_num_recv_tokens(), rows=rows,
+                                dstats=hd.dispatch_result.stats, cstats=hd.combine_stats))
                 hd.destroy()
         finally:
             _teardown(g)
@@ -124,7 +125,8 @@ def run_ht(cfg, tokens, routing, weights, expert_fn, bf16_expert=False):
             comb_out = ep.tensor_create((routing[rank].shape[0], h), ep.Dtype.F32, ep.TensorTag.TOKENS)
             hd.combine(comb_in, [comb_out])
             out = dict(rows=rows, origin=origin, origin_w=origin_w, counts=out_cnt.read_f32(),
-                       out=comb_out.read_f32(), recv_total=total, m=res.meta_m, q=res.meta_q, y=y)
+                       out=comb_out.read_f32(), recv_total=total, m=res.meta_m, q=res.meta_q, y=y,
+                       dstats=res.stats, cstats=hd.combine_stats)
             hd.destroy()
             return out
         finally:

@@ -99,6 +99,20 @@ def test_ll_matches_reference_golden(name, staged):
         np.testing.assert_array_equal(got, g[f"recvrows{r}"])
         assert res[r]["recv_total"] == int(g[f"recv_total{r}"])
         np.testing.assert_array_equal(res[r]["out"], g[f"out{r}"])
+        _check_stats(res[r], g, r, LL_STAT_F)
+
+
+LL_STAT_F = ("bytes_put", "msgs", "signals", "slots_used", "buffer_bytes")
+HT_STAT_F = LL_STAT_F + ("inter_node_msgs", "intra_node_msgs")
+
+
+def _check_stats(res, g, r, fields, sfx=""):
+    """handle.dispatch_result.stats / handle.combine_stats against the
+    reference engine's LLStats / HTStats of the golden round."""
+    for key, st in (("dstats", res["dstats"]), ("cstats", res["cstats"])):
+        assert st.as_dict()["op"] == ("dispatch" if key == "dstats" else "combine")
+        got = np.array([getattr(st, f) for f in fields], dtype=np.int64)
+        np.testing.assert_array_equal(got, g[f"{key}{sfx}{r}"], err_msg=key)
 
 
 @pytest.mark.parametrize("name", HT_NAMES)
@@ -115,6 +129,8 @@ def test_ht_matches_reference_golden(name):
         np.testing.assert_array_equal(res[r]["origin_w"], g[f"originw{r}"])
         assert res[r]["recv_total"] == int(g[f"recv_total{r}"])
         np.testing.assert_array_equal(res[r]["out"], g[f"out{r}"])
+        if c["rpn"] == c["n"]:
+            _check_stats(res[r], g, r, HT_STAT_F)
 
 
 # ---------------------------------------------------------------------------
@@ -218,6 +234,7 @@ def test_ll_legacy_layout_matches_reference_golden(name, staged):
             np.zeros((0, c["h"]), np.float32)
         np.testing.assert_array_equal(got, g[f"recvrows{r}"])
         np.testing.assert_array_equal(res[r]["out"], g[f"out{r}"])
+        _check_stats(res[r], g, r, LL_STAT_F, sfx="_leg")
 
 
 @pytest.mark.parametrize("n", [1, 4])
