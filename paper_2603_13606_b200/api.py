@@ -461,7 +461,7 @@ class EpHandle:
         counts[:hi - lo] = meta_h[:, lo:hi].T
         self._meta = dict(m=meta_h[:, :e].astype(np.int64), q=meta_h[:, e:].astype(np.int64),
                           recv_total=int(total.item()), offsets=offsets,
-                          counts_dev=torch.from_numpy(counts).to(dev))
+                          counts_host=counts, counts_dev=torch.from_numpy(counts).to(dev))
         self._round_open = True
 
     # -- staging helpers ----------------------------------------------------------
@@ -471,11 +471,16 @@ class EpHandle:
             v = v.to(self.group.device, non_blocking=True)
         return v.contiguous()
 
-    def _dev_out(self, t: NDTensor, full: bool = False):
+    def _dev_out(self, t: NDTensor, full: bool = False, mapped: bool = False):
         """(device tensor to write, needs_copy_back).  `full`: the kernel
-        overwrites every element, so a host output needs no upload."""
+        overwrites every element, so a host output needs no upload.
+        `mapped`: a pinned host tensor is written in place by the kernel
+        (pinned memory is device-mapped under UVA) — for small outputs such
+        as the expert counters."""
         v = t.view()
         if v.device == self.group.device and v.is_contiguous():
+            return v, False
+        if mapped and v.device.type == "cpu" and v.is_pinned() and v.is_contiguous():
             return v, False
         if full:
             return torch.empty(t.shape, dtype=t.dtype.torch_dtype, device=self.group.device), True
@@ -562,7 +567,7 @@ class EpHandle:
             dev = g.device
             out_t, back_t = self._dev_out(out_tokens)
             out_s, back_s = self._dev_out(out_scales) if out_scales is not None else (None, False)
-            cnt_f, back_c = self._dev_out(out_counts, full=True)
+            cnt_f, back_c = self._dev_out(out_counts, full=True, mapped=True)
             self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
             self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
             self._self_row = torch.empty(max(b, 1) * cfg.top_k, dtype=torch.int32, device=dev)
@@ -633,7 +638,11 @@ class EpHandle:
         ell, n = cfg.experts_per_rank, cfg.num_ranks
         lo = g.rank * ell
         hi = min(lo + ell, cfg.num_experts)
-        out_counts.view().copy_(meta["counts_dev"])
+        oc = out_counts.view()
+        if oc.device.type == "cpu":
+            oc.copy_(torch.from_numpy(meta["counts_host"]).reshape(oc.shape))  # host-known since the meta round
+        else:
+            oc.copy_(meta["counts_dev"])
         self._round_open = False
         self._dispatch_result = HTDispatchResult(out_t, origin[:total], origin_w[:total], meta["m"],
                                                  meta["q"], total, _stats_fn=self._ht_dispatch_stats)

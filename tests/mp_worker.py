@@ -118,6 +118,33 @@ def ll_pipelined(world, rank):
     g.destroy()
 
 
+def buffer_ll(world, rank):
+    """Buffer wrapper, one process per GPU: own comm stream, pinned mapped
+    counters, cached dispatch."""
+    e, k, h, b = 256, 8, 7168, 64
+    cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, b, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
+    wl = owl.make_workload(e, world, b, k, h, 70)
+    wl.tokens = [bf16r(t) for t in wl.tokens]
+    d = oll.dispatch(wl.tokens, wl.routing, e, world, b, h, "fp8", True)
+    ys = [bf16r(oll.apply_experts(d[r]["recv"], d[r]["counts"], r, e, world, b, owl.expert_scale))
+          for r in range(world)]
+    want = oll.combine(ys, wl.routing, wl.weights, e, world, b, h, "bf16")[rank]
+    buf = ep.Buffer(ep.ProcessFabric(ep.NodeTopology(world, world)), rank, cfg)
+    x = torch.from_numpy(wl.tokens[rank]).cuda().to(torch.bfloat16)
+    topk = torch.from_numpy(wl.routing[rank]).cuda()
+    w = torch.from_numpy(wl.weights[rank]).cuda()
+    y = torch.from_numpy(ys[rank]).cuda().to(torch.bfloat16)
+    hd = None
+    for _ in range(2):
+        (rx, rs), ri, _, hd, _ = buf.dispatch(x, topk, w, handle=hd)
+        assert buf.get_tokens_per_expert_list() == d[rank]["counts"].sum(axis=1).tolist()
+        out, _, ev = buf.combine(y, hd, w)
+        ev.synchronize()
+        np.testing.assert_array_equal(out.float().cpu().numpy(), bf16r(want))
+    buf.destroy_handle(hd)
+    buf.destroy()
+
+
 def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert):
     cfg = ep.EpConfig(ep.Algorithm.HT, world, rpn, e, k, h, b, ep.Dtype.BF16)
     fab = ep.ProcessFabric(ep.NodeTopology(world, rpn))
@@ -162,6 +189,7 @@ def main():
                                                           ep.Dtype.BF16, 6, False, "bf16", rounds=2, layout="legacy")),
         ("ll legacy layout staged uneven", lambda: ll_case(world, rank, 3 * world + 1, 3, 256, 12, ep.Dtype.BF16, False,
                                                             None, 7, True, "ref", rounds=3, layout="legacy")),
+        ("buffer wrapper ll c2 path", lambda: buffer_ll(world, rank)),
         ("ht bf16 single node", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 4, False)),
         ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
     ]
