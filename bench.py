@@ -88,6 +88,17 @@ def allreduce_max(v: float, world: int) -> float:
     return float(t.item())
 
 
+def allgather_f(v: float, world: int) -> list:
+    if world == 1:
+        return [v]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
 def barrier(world):
     import torch
     if world > 1:
@@ -502,8 +513,12 @@ def run_ht(args, world, rank):
         tc.append(ev["epb_ht_combine"].elapsed_time(ev["combine:end"]))
     g.check()
     barrier(world)
-    t_d = allreduce_max(statistics.median(td), world) / 1e3
-    t_c = allreduce_max(statistics.median(tc), world) / 1e3
+    per_d = allgather_f(statistics.median(td), world)
+    per_c = allgather_f(statistics.median(tc), world)
+    ph_send = allgather_f(tphase.get("epb_ht_dispatch", 0.0) / args.ht_steps, world)
+    ph_recv = allgather_f(tphase.get("epb_ht_dispatch:recv", 0.0) / args.ht_steps, world)
+    t_d = max(per_d) / 1e3
+    t_c = max(per_c) / 1e3
     owner = wl.routing[rank] // L
     dsts = [set(r) for r in owner]
     d_all = sum(len(s) for s in dsts) * H * 2
@@ -519,6 +534,9 @@ def run_ht(args, world, rank):
         "dispatch_nvlink_GBps": round(d_remote / t_d / 1e9, 1) if world > 1 else None,
         "combine_nvlink_GBps": round(c_remote / t_c / 1e9, 1) if world > 1 else None,
         "phase_us": {k: round(v / args.ht_steps * 1e3, 1) for k, v in tphase.items()},
+        "per_rank_us": {"dispatch": [round(v * 1e3, 1) for v in per_d], "combine": [round(v * 1e3, 1) for v in per_c],
+                        "dispatch_send": [round(v * 1e3, 1) for v in ph_send],
+                        "dispatch_recv": [round(v * 1e3, 1) for v in ph_recv]},
         "note": "payload = bf16 rows per (token, destination rank) for dispatch and per (token, k) "
                 "for combine, all destinations incl. self; nvlink = remote part only",
     }

@@ -240,6 +240,10 @@ typedef struct epb_ht_combine_args {
   const float* dispatch_weights; /* [b, K] weights given at dispatch, checked
                                     against `weights` before any traffic
                                     (ht.py:605-609); NULL skips the check */
+  uint64_t* row_ptr;         /* [b*K] scratch: the send phase stores the
+                                address of every (t, k) expert row the
+                                receive reduces (own rows in place, others in
+                                the combine slots); NULL: resolved inline */
 } epb_ht_combine_args;
 int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases,
                    const epb_ht_combine_args* args, void* stream);

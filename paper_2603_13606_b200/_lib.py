@@ -67,7 +67,7 @@ class HTCombineArgs(ctypes.Structure):
                 ("recv_total", ctypes.c_int32), ("topk_idx", ctypes.c_void_p), ("weights", ctypes.c_void_p),
                 ("num_tokens", ctypes.c_int32), ("tok_rank", ctypes.c_void_p), ("offsets", ctypes.c_void_p),
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
-                ("dispatch_weights", ctypes.c_void_p)]
+                ("dispatch_weights", ctypes.c_void_p), ("row_ptr", ctypes.c_void_p)]
 
 
 PHASE_SEND, PHASE_RECV, PHASE_BOTH = 1, 2, 3

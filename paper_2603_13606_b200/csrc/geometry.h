@@ -43,12 +43,14 @@ struct LLGeom {
 // HT:
 //   [meta rows: 2 x N x (E+N) u32][meta flags: 2 x N u64]
 //   [dispatch flags: N u64][combine flags: N u64]
-//   [records: N x B x rec_stride]   rec = [row RBp][w: K f32][hdr + pos]
+//   [stage: B x RBp]  this rank's token rows in the wire dtype; receivers
+//                     pull the rows they need from it over NVLink
+//   [records: N x B x rec_stride]   rec = [w: K f32][hdr + pos]
 //   [combine rows: B x K x crow_stride]  (f32 capacity: 4H)
 struct HTGeom {
   int N, E, L, K, H, B, rpn, wire;
   int RB, RBp, WBp, HBp, rec_stride, crow_stride;
-  uint64_t meta, meta_flag, dflag, cflag, rec, crow;
+  uint64_t meta, meta_flag, dflag, cflag, stage, rec, crow;
   uint64_t window_bytes, logical_bytes;
   uint64_t barrier;  // [N] u64 device-barrier flags
 };
@@ -105,13 +107,14 @@ inline void make_ht_geom(const epb_config& c, HTGeom& g) {
   g.RBp = (int)a16(g.RB);
   g.WBp = (int)a16(4 * c.top_k);
   g.HBp = (int)a16(8 + 8 * c.top_k);
-  g.rec_stride = g.RBp + g.WBp + g.HBp;
+  g.rec_stride = g.WBp + g.HBp;  // record = weights + header/positions; the row stays in `stage`
   g.crow_stride = (int)a16(4 * (size_t)c.hidden);
   g.meta = 0;
   g.meta_flag = a256((uint64_t)2 * g.N * (g.E + g.N) * 4);
   g.dflag = g.meta_flag + 2 * g.N * 8;
   g.cflag = g.dflag + g.N * 8;
-  g.rec = a256(g.cflag + g.N * 8);
+  g.stage = a256(g.cflag + g.N * 8);
+  g.rec = a256(g.stage + (uint64_t)g.B * g.RBp);
   g.crow = a256(g.rec + (uint64_t)g.N * g.B * g.rec_stride);
   g.barrier = a256(g.crow + (uint64_t)g.B * g.K * g.crow_stride);
   g.window_bytes = a256(g.barrier + (uint64_t)g.N * 8);

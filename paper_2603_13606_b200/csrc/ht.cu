@@ -6,13 +6,18 @@
 //    receive shapes and the sorted-output offsets follow from them
 //    (HTMeta.expert_offsets, ht.py:185-193).
 //  * dispatch (ht.py:381-468, 553-583): one record per (token, destination
-//    rank) = header + K f32 weights + row; the receiver places a copy of the
-//    row for every local expert it names, sorted by (local expert, src, t).
-//    The sender also writes, per k, the final output row on the owner
-//    (offset(e, src) + rank of t within (e, src)), so placement is a parallel
-//    scatter that never depends on arrival order.  Rows a rank routes to its
-//    OWN experts skip the window: the sender writes them straight to their
-//    sorted output position.
+//    rank) = header + K f32 weights (+ the row); the receiver places a copy
+//    of the row for every local expert it names, sorted by (local expert,
+//    src, t).  The sender also writes, per k, the final output row on the
+//    owner (offset(e, src) + rank of t within (e, src)), so placement is a
+//    parallel scatter that never depends on arrival order.
+//    B200 transport: PULL.  The sender converts its rows once into its own
+//    window (`stage`, local HBM) and pushes only the small records; each
+//    receiver reads every row it needs once over NVLink (peer loads measured
+//    ~765 GB/s vs ~710 GB/s for peer stores on this system) and fans it out
+//    to its local experts' output rows, so the NVLink transfer and the local
+//    placement are one pass.  Rows a rank routes to its OWN experts never
+//    leave: the sender writes them straight to their sorted positions.
 //  * combine (ht.py:587-735): p = f32(w * y) from the f32 expert row; per
 //    token, per node holding its experts (ascending), a partial = first p
 //    then f32 adds in ascending k; out = f32(0 + partial_0) + partial_1 ...
@@ -148,6 +153,7 @@ __global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
 // ---------------------------------------------------------------------------
 struct HTSend {
   const void* x;
+  uint8_t* stage;          // own window: [B][RBp] wire rows
   const float* w;
   const int64_t* topk;
   const int32_t* q;
@@ -155,9 +161,6 @@ struct HTSend {
   const int32_t* tok_slot;
   const int32_t* offsets;  // [E, N]
   const uint64_t* peers;
-  void* out;               // own sorted output (self rows land here directly)
-  int32_t* origin;
-  float* origin_w;
   int* done;
   HTGeom g;
   int b, rank;
@@ -169,121 +172,97 @@ EPB_DEV void ht_publish_records(const HTSend& p, int d) {
   st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | (uint32_t)p.q[d]);
 }
 
-template <int XT, int WT, int OT>
+// Send: (1) every token row, converted once to the wire dtype, into this
+// rank's own stage (a flat streaming copy, 4 x 16 B in flight per thread);
+// (2) one record (weights, header, output positions) per (token, rank it
+// touches) — this rank included — into that rank's window, a warp per
+// token; (3) per destination, the last CTA to finish publishes the flag
+// (tag | record count) after a system-scope release.
+template <int XT, int WT>
 __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) {
-  // a CTA owns tokens blockIdx.x + i*gridDim.x; their routing metadata is
-  // gathered for kTB tokens at once (one latency for the batch), then rows
-  // move token by token
-  constexpr int kTB = 16;
-  __shared__ int s_e[kTB][kMaxTopK], s_pos[kTB][kMaxTopK];
-  __shared__ float s_w[kTB][kMaxTopK];
-  __shared__ int s_j[kTB][kMaxRanks];
-  __shared__ int s_cnt[kMaxRanks];
   const HTGeom& g = p.g;
-  const int K = g.K, N = g.N, H = g.H, L = g.L, G = gridDim.x;
+  const int K = g.K, N = g.N, H = g.H, L = g.L;
   const int me = p.rank;
   constexpr int EPC = Elems<WT>::n;
   constexpr int XW = XT == EPB_F32 ? 4 : 2;
-  constexpr int OW = OT == EPB_F32 ? 4 : 2;
-  const int64_t rec0 = (int64_t)me * g.B;
-  if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
-  for (int base = blockIdx.x; base < p.b; base += G * kTB) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < kTB * K; idx += blockDim.x) {
-      const int i = idx / K, k = idx - i * K, t = base + i * G;
-      if (t >= p.b) continue;
-      const int e = (int)p.topk[(int64_t)t * K + k];
-      const int pos = p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + k];
-      const float wk = p.w[(int64_t)t * K + k];
-      s_e[i][k] = e;
-      s_pos[i][k] = pos;
-      s_w[i][k] = wk;
-      if (e / L == me) {
-        p.origin[(int64_t)pos * 4 + 0] = e;
-        p.origin[(int64_t)pos * 4 + 1] = me;
-        p.origin[(int64_t)pos * 4 + 2] = t;
-        p.origin[(int64_t)pos * 4 + 3] = k;
-        p.origin_w[pos] = wk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // (1) stage
+  if ((H % EPC) == 0 && g.RBp == H * (int)sizeof(uint16_t) * (WT == EPB_F32 ? 2 : 1)) {
+    const int64_t nq = (int64_t)p.b * (H / EPC);
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nq; q0 += 4 * gs) {
+      float f[4][EPC];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + u * gs;
+        if (q < nq) load_elems_vec<XT, EPC>(xb, q * EPC, f[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + u * gs;
+        if (q < nq) st_plain_v4(p.stage + q * 16, pack16<WT>(f[u]));
       }
     }
-    for (int idx = threadIdx.x; idx < kTB * N; idx += blockDim.x) {
-      const int i = idx / N, d = idx - i * N, t = base + i * G;
-      int j = -1;
-      if (t < p.b && d != me) j = p.tok_slot[(int64_t)t * N + d];
-      s_j[i][d] = j;
-    }
-    __syncthreads();
-    if ((int)threadIdx.x < N)
-      for (int i = 0; i < kTB; ++i) s_cnt[threadIdx.x] += s_j[i][threadIdx.x] >= 0;
-    for (int i = 0; i < kTB; ++i) {
-      const int t = base + i * G;
-      if (t >= p.b) break;
-      // record header (reference fields + output positions) and weights
-      const int words = K + 2 + 2 * K;
-      for (int idx = threadIdx.x; idx < N * words; idx += blockDim.x) {
-        const int d = idx / words, wd = idx - d * words;
-        if (s_j[i][d] < 0) continue;
-        uint8_t* rec = hpeer(p.peers, d) + g.rec + (rec0 + s_j[i][d]) * g.rec_stride;
-        if (wd < K) {
-          reinterpret_cast<float*>(rec + g.RBp)[wd] = s_w[i][wd];
-        } else {
-          const int h = wd - K;
-          const uint32_t v = h == 0 ? (uint32_t)t : h == 1 ? (uint32_t)K
-                             : h < 2 + K ? (uint32_t)s_e[i][h - 2] : (uint32_t)s_pos[i][h - 2 - K];
-          reinterpret_cast<uint32_t*>(rec + g.RBp + g.WBp)[h] = v;
-        }
-      }
+  } else {
+    for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
       const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
-      if ((H & 15) == 0) {
-        for (int c = threadIdx.x; c < H / EPC; c += blockDim.x) {
-          float f[EPC];
-          load_elems_vec<XT, EPC>(xrow, (int64_t)c * EPC, f);
-          const int4 v = pack16<WT>(f);
-          for (int d = 0; d < N; ++d) {
-            const int j = s_j[i][d];
-            if (j >= 0) st_na_v4(hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride + (int64_t)c * 16, v);
-          }
-          float fw[EPC];
-          unpack16<WT>(v, fw);  // the wire image, exactly what a record carries
-          for (int k = 0; k < K; ++k)
-            if (s_e[i][k] / L == me)
-              store_f32_chunk<OT, EPC>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW,
-                                       (int64_t)c * EPC, fw);
-        }
-      } else {
-        for (int el = threadIdx.x; el < H; el += blockDim.x) {
-          const float f = load_elem(xrow, XT, el);
-          for (int d = 0; d < N; ++d) {
-            const int j = s_j[i][d];
-            if (j >= 0) store_elem(hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride, WT, el, f);
-          }
-          const float fw = WT == EPB_F32 ? f : (WT == EPB_BF16 ? bf16_widen(bf16_bits_rne(f)) : f16_widen(f16_bits_rne(f)));
-          for (int k = 0; k < K; ++k)
-            if (s_e[i][k] / L == me)
-              store_elem(reinterpret_cast<uint8_t*>(p.out) + (int64_t)s_pos[i][k] * H * OW, OT, el, fw);
+      for (int el = threadIdx.x; el < H; el += blockDim.x)
+        store_elem(p.stage + (int64_t)t * g.RBp, WT, el, load_elem(xrow, XT, el));
+    }
+  }
+  // (2) records: lane k holds (e_k, w_k, pos_k); lane d < N (and d + 32)
+  // the token's slot at rank d
+  const int words = K + 2 + 2 * K;
+  const int64_t rec0 = (int64_t)me * g.B;
+  for (int t = blockIdx.x * nw + warp; t < p.b; t += gridDim.x * nw) {
+    int e = 0, pos = 0;
+    float wk = 0.0f;
+    if (lane < K) {
+      const int64_t i = (int64_t)t * K + lane;
+      e = (int)p.topk[i];
+      wk = p.w[i];
+      pos = p.offsets[e * N + me] + p.tok_rank[i];
+    }
+    const int slot_lo = lane < N ? p.tok_slot[(int64_t)t * N + lane] : -1;
+    const int slot_hi = lane + 32 < N ? p.tok_slot[(int64_t)t * N + lane + 32] : -1;
+    for (int d = 0; d < N; ++d) {
+      const int j = __shfl_sync(0xffffffffu, d < 32 ? slot_lo : slot_hi, d & 31);
+      if (j < 0) continue;
+      uint8_t* rec = hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride;
+      for (int w0 = 0; w0 < words; w0 += 32) {
+        const int wd = w0 + lane;
+        const int h = wd - K;
+        const int src = wd < K ? wd : (h >= 2 && h < 2 + K ? h - 2 : (h >= 2 + K ? h - 2 - K : 0));
+        const float wv = __shfl_sync(0xffffffffu, wk, src & 31);
+        const int ev = __shfl_sync(0xffffffffu, e, src & 31);
+        const int pv = __shfl_sync(0xffffffffu, pos, src & 31);
+        if (wd < K) {
+          reinterpret_cast<float*>(rec)[wd] = wv;
+        } else if (wd < words) {
+          const uint32_t v = h == 0 ? (uint32_t)t : h == 1 ? (uint32_t)K : h < 2 + K ? (uint32_t)ev : (uint32_t)pv;
+          reinterpret_cast<uint32_t*>(rec + g.WBp)[h] = v;
         }
       }
     }
   }
+  (void)L;
+  // (3) publish: the last CTA (stage rows and records of every CTA done)
   __syncthreads();
   if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
     const int d = threadIdx.x;
-    const int c = s_cnt[d];
-    if (c > 0) {
+    fence_sys();
+    if (atomicAdd(&p.done[d], 1) == (int)gridDim.x - 1) {
+      p.done[d] = 0;
       fence_sys();
-      const int old = atomicAdd(&p.done[d], c);
-      if (old + c == p.q[d]) {
-        p.done[d] = 0;
-        fence_sys();
-        ht_publish_records(p, d);
-      }
-    } else if (blockIdx.x == 0 && p.q[d] == 0) {
       ht_publish_records(p, d);
     }
   }
 }
 
 struct HTRecv {
+  const uint64_t* peers;  // rows are pulled from each source's stage
+  const int32_t* q;       // this rank's own record count is q[rank]
   void* out;
   int32_t* origin;
   float* origin_w;
@@ -295,6 +274,13 @@ struct HTRecv {
   uint32_t tag;
 };
 
+// Receive: every record names a source token and the output rows of this
+// rank's experts it feeds; the warp reads the header once, pulls the row
+// from the source's stage (over NVLink, or locally for this rank's own
+// tokens) once, and stores it to each of those rows (the local fan-out of
+// ht.py:553-583).  Remote sources are visited in the order me+1, me+2, ...
+// so every source's stage is read by a different receiver at a time; a
+// share of the warps (1/N) handles this rank's own records concurrently.
 template <int WT, int OT>
 __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) {
   __shared__ int s_pre[kMaxRanks + 1], s_q[kMaxRanks];
@@ -308,64 +294,90 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
     if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
-    s_q[s] = s == me ? 0 : (int)(v & 0xFFFFFFFFu);  // own rows were placed by the sender
+    s_q[s] = s == me ? p.q[me] : (int)(v & 0xFFFFFFFFu);
   }
   __syncthreads();
   if (s_fail) return;
   if (threadIdx.x == 0) {
     int run = 0;
-    for (int s = 0; s < N; ++s) { s_pre[s] = run; run += s_q[s]; }
-    s_pre[N] = run;
+    for (int i = 0; i < N - 1; ++i) { s_pre[i] = run; run += s_q[(me + 1 + i) % N]; }
+    s_pre[N - 1] = run;
   }
   __syncthreads();
-  const int items = s_pre[N] * K;  // (record, k); non-local k exit at once
   const int lo = me * L, hi = min(lo + L, g.E);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // warps [0, sw) take this rank's own records, the rest the remote ones
+  const int sw = N == 1 ? nw : max(1, nw / N);
+  const bool self_warp = warp < sw;
+  const int items = self_warp ? 2 * s_q[me] : 2 * s_pre[N - 1];
+  const int wi = self_warp ? warp : warp - sw;
+  const int wn = self_warp ? sw : nw - sw;
   constexpr int OW = OT == EPB_F32 ? 4 : 2;
   constexpr int EPC = Elems<WT>::n;
-  for (int f = warp * gridDim.x + blockIdx.x; f < items; f += gridDim.x * nw) {
-    const int rj = f / K, k = f - rj * K;
-    int s = 0;
-    while (s_pre[s + 1] <= rj) ++s;
-    const int j = rj - s_pre[s];
-    const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
-    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.RBp + g.WBp);
-    const int e = (int)hdr[2 + k];
-    if (e < lo || e >= hi) continue;
-    const int64_t pos = hdr[2 + K + k];
-    if (lane == 0) {
-      p.origin[pos * 4 + 0] = e;
-      p.origin[pos * 4 + 1] = s;
-      p.origin[pos * 4 + 2] = (int32_t)hdr[0];
-      p.origin[pos * 4 + 3] = k;
-      p.origin_w[pos] = reinterpret_cast<const float*>(rec + g.RBp)[k];
+  for (int f2 = wi * gridDim.x + blockIdx.x; f2 < items; f2 += gridDim.x * wn) {
+    const int rj = f2 >> 1, half = f2 & 1;
+    int s, j;
+    if (self_warp) {
+      s = me;
+      j = rj;
+    } else {
+      int si = 0;
+      while (s_pre[si + 1] <= rj) ++si;
+      j = rj - s_pre[si];
+      s = (me + 1 + si) % N;
     }
-    uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + pos * H * OW;
+    const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.WBp);
+    const uint8_t* row = hpeer(p.peers, s) + g.stage + (int64_t)hdr[0] * g.RBp;
+    int e = -1, pos = 0;
+    if (lane < K) {
+      e = (int)hdr[2 + lane];
+      pos = (int)hdr[2 + K + lane];
+    }
+    const bool loc = lane < K && e >= lo && e < hi;
+    const unsigned lm = __ballot_sync(0xffffffffu, loc);
+    if (half == 0 && loc) {
+      p.origin[(int64_t)pos * 4 + 0] = e;
+      p.origin[(int64_t)pos * 4 + 1] = s;
+      p.origin[(int64_t)pos * 4 + 2] = (int32_t)hdr[0];
+      p.origin[(int64_t)pos * 4 + 3] = lane;
+      p.origin_w[pos] = reinterpret_cast<const float*>(rec)[lane];
+    }
     if ((H & 15) == 0) {
       const int nch = H / EPC;
-      for (int base = 0; base < nch; base += 32 * kHU) {
+      const int per = (nch + 1) / 2;
+      const int c0 = half * per, c1 = min(nch, c0 + per);
+      for (int base = c0; base < c1; base += 32 * kHU) {
         int4 v[kHU];
 #pragma unroll
         for (int u = 0; u < kHU; ++u) {
           const int c = base + u * 32 + lane;
-          if (c < nch) v[u] = ld_plain_v4(rec + (int64_t)c * 16);
+          if (c < c1) v[u] = ld_plain_v4(row + (int64_t)c * 16);
         }
+        for (unsigned mm = lm; mm; mm &= mm - 1) {
+          const int kk = __ffs(mm) - 1;
+          uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)__shfl_sync(0xffffffffu, pos, kk) * H * OW;
 #pragma unroll
-        for (int u = 0; u < kHU; ++u) {
-          const int c = base + u * 32 + lane;
-          if (c < nch) {
-            if constexpr (OT == WT) {
-              st_plain_v4(orow + (int64_t)c * 16, v[u]);
-            } else {
-              float fv[EPC];
-              unpack16<WT>(v[u], fv);
-              store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, fv);
+          for (int u = 0; u < kHU; ++u) {
+            const int c = base + u * 32 + lane;
+            if (c < c1) {
+              if constexpr (OT == WT) {
+                st_plain_v4(orow + (int64_t)c * 16, v[u]);
+              } else {
+                float fv[EPC];
+                unpack16<WT>(v[u], fv);
+                store_f32_chunk<OT, EPC>(orow, (int64_t)c * EPC, fv);
+              }
             }
           }
         }
       }
-    } else {
-      for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(rec, WT, el));
+    } else if (half == 0) {
+      for (unsigned mm = lm; mm; mm &= mm - 1) {
+        const int kk = __ffs(mm) - 1;
+        uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)__shfl_sync(0xffffffffu, pos, kk) * H * OW;
+        for (int el = lane; el < H; el += 32) store_elem(orow, OT, el, load_elem(row, WT, el));
+      }
     }
   }
 }
@@ -380,8 +392,14 @@ struct HTCombSend {
   const int32_t* meta;  // [N][E+N] (m rows)
   const uint64_t* peers;
   int* done;
+  // receive row table (filled here, read by the receive phase)
+  const int64_t* topk;
+  const int32_t* tok_rank;
+  const int32_t* offsets;
+  const uint8_t* win;
+  uint64_t* row_ptr;
   HTGeom g;
-  int rows, rank, in_dtype;
+  int rows, rank, in_dtype, b;
   uint32_t tag;
 };
 
@@ -406,10 +424,21 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
   const int me = p.rank;
   if (*reinterpret_cast<const volatile int*>(p.err) != 0) return;
   if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   constexpr int ib = IT == EPB_F32 ? 4 : 2;
   const int bytes = H * ib;
+  if (p.row_ptr) {
+    // address of every (t, k) row the receive phase reduces: own experts'
+    // rows in place in the expert output, the others in the combine slots
+    const int L = g.L;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.b * K; i += gridDim.x * blockDim.x) {
+      const int e = (int)p.topk[i];
+      p.row_ptr[i] = e / L == me
+          ? reinterpret_cast<uint64_t>(p.y) + (uint64_t)(p.offsets[e * N + me] + p.tok_rank[i]) * bytes
+          : reinterpret_cast<uint64_t>(p.win + g.crow + (int64_t)i * g.crow_stride);
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int nch = (bytes & 15) == 0 ? bytes / 16 : 0;
   // warp tasks: (row, half); rows of my own tokens stay (the home reads them in place)
   for (int task = warp * gridDim.x + blockIdx.x; task < 2 * p.rows; task += gridDim.x * nw) {
@@ -463,6 +492,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
 
 struct HTCombRecv {
   const int64_t* topk;
+  const uint64_t* row_ptr;   // [b*K] from the send phase, or null
   const float* w;
   const void* y_local;       // this rank's expert rows [recv_total, H] (own tokens read in place)
   const int32_t* tok_rank;   // [b, K]
@@ -517,21 +547,36 @@ __global__ void __launch_bounds__(kHTThreads, 2) ht_combine_recv_kernel(HTCombRe
     // place from the local expert output, others from the combine slots).
     const int nch = H / 8;
     const int segs = (nch + 31) / 32;
-    for (int task = warp * gridDim.x + blockIdx.x; task < p.b * segs; task += gridDim.x * nw) {
-      const int t = task / segs, c = (task - t * segs) * 32 + lane;
-      uint64_t my_row = 0;
-      float my_w = 0.0f;
-      int my_node = 0;
+    const int tstride = gridDim.x * nw;
+    int task = warp * gridDim.x + blockIdx.x;
+    // lane k's row of a task's token: the send phase's table (one load,
+    // prefetched a task ahead) or resolved from the routing
+    uint64_t my_row = 0;
+    float my_w = 0.0f;
+    int my_node = 0;
+    auto fetch = [&](int tk) {
       if (lane < K) {
-        const int e = (int)p.topk[(int64_t)t * K + lane];
-        const int owner = e / L;
-        my_node = owner / g.rpn;
-        my_w = p.w[(int64_t)t * K + lane];
-        my_row = owner == me
-            ? reinterpret_cast<uint64_t>(p.y_local) +
-                  (uint64_t)(p.offsets[e * N + me] + p.tok_rank[(int64_t)t * K + lane]) * H * YB
-            : reinterpret_cast<uint64_t>(crow + ((int64_t)t * K + lane) * g.crow_stride);
+        const int64_t i = (int64_t)tk * K + lane;
+        my_w = p.w[i];
+        if (p.row_ptr && one_node) {
+          my_row = p.row_ptr[i];
+        } else {
+          const int e = (int)p.topk[i];
+          const int owner = e / L;
+          my_node = owner / g.rpn;
+          my_row = owner == me
+              ? reinterpret_cast<uint64_t>(p.y_local) + (uint64_t)(p.offsets[e * N + me] + p.tok_rank[i]) * H * YB
+              : reinterpret_cast<uint64_t>(crow + i * g.crow_stride);
+        }
       }
+    };
+    if (task < p.b * segs) fetch(task / segs);
+    for (; task < p.b * segs; task += tstride) {
+      const int t = task / segs, c = (task - t * segs) * 32 + lane;
+      const uint64_t cur_row = my_row;
+      const float cur_w = my_w;
+      const int cur_node = my_node;
+      if (task + tstride < p.b * segs) fetch((task + tstride) / segs);  // next task's rows, in flight now
       float acc[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
@@ -545,8 +590,8 @@ __global__ void __launch_bounds__(kHTThreads, 2) ht_combine_recv_kernel(HTCombRe
           float wk[KB];
 #pragma unroll
           for (int u = 0; u < KB; ++u) {
-            const uint64_t row = __shfl_sync(0xffffffffu, my_row, (k0 + u) & 31);
-            wk[u] = __shfl_sync(0xffffffffu, my_w, (k0 + u) & 31);
+            const uint64_t row = __shfl_sync(0xffffffffu, cur_row, (k0 + u) & 31);
+            wk[u] = __shfl_sync(0xffffffffu, cur_w, (k0 + u) & 31);
             if (k0 + u < K && c < nch) {
 #pragma unroll
               for (int q = 0; q < NV; ++q)
@@ -580,16 +625,16 @@ __global__ void __launch_bounds__(kHTThreads, 2) ht_combine_recv_kernel(HTCombRe
         for (;;) {
           int nd = 0x7fffffff;
           for (int k = 0; k < K; ++k) {
-            const int n2 = __shfl_sync(0xffffffffu, my_node, k);
+            const int n2 = __shfl_sync(0xffffffffu, cur_node, k);
             if (n2 > prev && n2 < nd) nd = n2;
           }
           if (nd == 0x7fffffff) break;
           float part[8];
           bool started = false;
           for (int k = 0; k < K; ++k) {
-            const int n2 = __shfl_sync(0xffffffffu, my_node, k);
-            const uint64_t row = __shfl_sync(0xffffffffu, my_row, k);
-            const float wk = __shfl_sync(0xffffffffu, my_w, k);
+            const int n2 = __shfl_sync(0xffffffffu, cur_node, k);
+            const uint64_t row = __shfl_sync(0xffffffffu, cur_row, k);
+            const float wk = __shfl_sync(0xffffffffu, cur_w, k);
             if (n2 != nd) continue;
             float y[8];
             if (c < nch) ht_load8<IT>(reinterpret_cast<const uint8_t*>(row), c, y);
@@ -675,24 +720,19 @@ int check_ht(epb_group* g, int phases) {
   return EPB_OK;
 }
 
-template <int XT, int WT, int OT>
-cudaError_t launch_hsend(const HTSend& p, cudaStream_t s) {
-  const int grid = std::max(1, std::min(p.b, 2 * hsm_count()));
-  ht_dispatch_send_kernel<XT, WT, OT><<<grid, kHTThreads, 0, s>>>(p);
-  return cudaGetLastError();
-}
-
 template <int XT, int WT>
-cudaError_t launch_hsend_o(const HTSend& p, int out_dtype, cudaStream_t s) {
-  return out_dtype == EPB_F32 ? launch_hsend<XT, WT, EPB_F32>(p, s) : launch_hsend<XT, WT, WT>(p, s);
+cudaError_t launch_hsend(const HTSend& p, cudaStream_t s) {
+  ht_dispatch_send_kernel<XT, WT><<<2 * hsm_count(), kHTThreads, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 template <int XT>
 cudaError_t launch_hsend_x(const HTSend& p, int out_dtype, cudaStream_t s) {
+  (void)out_dtype;
   switch (p.g.wire) {
-    case EPB_F32: return launch_hsend<XT, EPB_F32, EPB_F32>(p, s);
-    case EPB_BF16: return launch_hsend_o<XT, EPB_BF16>(p, out_dtype, s);
-    default: return launch_hsend_o<XT, EPB_F16>(p, out_dtype, s);
+    case EPB_F32: return launch_hsend<XT, EPB_F32>(p, s);
+    case EPB_BF16: return launch_hsend<XT, EPB_BF16>(p, s);
+    default: return launch_hsend<XT, EPB_F16>(p, s);
   }
 }
 
@@ -744,9 +784,10 @@ int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases, const epb_ht_d
     if (a->num_tokens > 0 && !a16(a->x)) return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
     HTSend p;
     p.x = a->x; p.w = a->weights; p.topk = a->topk_idx; p.q = a->rank_count; p.tok_rank = a->tok_rank;
-    p.tok_slot = a->tok_slot; p.offsets = a->offsets; p.peers = g->d_peers; p.out = a->out;
-    p.origin = a->origin; p.origin_w = a->origin_w; p.done = g->d_done; p.g = g->ht;
+    p.tok_slot = a->tok_slot; p.offsets = a->offsets; p.peers = g->d_peers;
+    p.done = g->d_done; p.g = g->ht;
     p.b = a->num_tokens; p.rank = g->rank; p.tag = ht_tag(round);
+    p.stage = g->window + g->ht.stage;
     cudaError_t e;
     switch (a->x_dtype) {
       case EPB_F32: e = launch_hsend_x<EPB_F32>(p, a->out_dtype, s); break;
@@ -758,7 +799,8 @@ int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases, const epb_ht_d
   }
   if (phases & 2) {
     HTRecv p;
-    p.out = a->out; p.origin = a->origin; p.origin_w = a->origin_w; p.win = g->window; p.err = g->d_err;
+    p.peers = g->d_peers; p.q = a->rank_count; p.out = a->out; p.origin = a->origin; p.origin_w = a->origin_w;
+    p.win = g->window; p.err = g->d_err;
     p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank; p.tag = ht_tag(round);
     cudaError_t e;
     switch (wire) {
@@ -795,6 +837,8 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
                                               (uint64_t)(round & 1) * g->ht.N * (g->ht.E + g->ht.N) * 4);
     p.peers = g->d_peers; p.done = g->d_done + g->cfg.num_ranks; p.g = g->ht; p.rows = a->recv_total;
     p.rank = g->rank; p.in_dtype = a->in_dtype; p.tag = ht_tag(round);
+    p.topk = a->topk_idx; p.tok_rank = a->tok_rank; p.offsets = a->offsets; p.win = g->window;
+    p.row_ptr = a->row_ptr; p.b = a->num_tokens;
     const int grid = 2 * hsm_count();
     if (a->in_dtype == EPB_F32) ht_combine_send_kernel<EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
     else ht_combine_send_kernel<EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
@@ -804,7 +848,8 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
     if (a->out_dtype != EPB_F32 && a->out_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine output f32|bf16");
     if (!a16(a->out)) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
     HTCombRecv p;
-    p.topk = a->topk_idx; p.w = a->weights; p.y_local = a->expert_rows; p.tok_rank = a->tok_rank;
+    p.topk = a->topk_idx; p.row_ptr = a->row_ptr; p.w = a->weights; p.y_local = a->expert_rows;
+    p.tok_rank = a->tok_rank;
     p.offsets = a->offsets; p.out = a->out; p.win = g->window; p.err = g->d_err; p.g = g->ht;
     p.timeout_ns = g->timeout_ns; p.b = a->num_tokens; p.rank = g->rank; p.y_dtype = a->in_dtype;
     p.tag = ht_tag(round);
