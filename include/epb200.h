@@ -86,11 +86,18 @@ typedef struct epb_config {
   int32_t ht_chunk_tokens;  /* kept for fingerprint parity */
   int32_t ht_fifo_depth;
   int32_t combine_dtype;    /* LL combine wire dtype; -1 = token_dtype (reference) */
+  int32_t ht_expert_out;    /* HT: reserve a registered expert-output region in
+                               the window (N*B*min(K,L) bf16 rows); a combine
+                               whose input IS that region is pulled by the
+                               token's home rank over NVLink (no push pass) */
 } epb_config;
 
 typedef struct epb_window_info {
   uint64_t physical_bytes;  /* bytes this library needs (16-B aligned slots) */
   uint64_t logical_bytes;   /* the reference's window_bytes (footprint parity) */
+  uint64_t expert_out_offset; /* HT with ht_expert_out: byte offset of the
+                                 expert-output region in the window */
+  uint64_t expert_out_rows;   /* its capacity in rows of hidden bf16 */
 } epb_window_info;
 
 /* per-handle routing layout; caller-owned device buffers (K1 outputs) */
@@ -244,6 +251,9 @@ typedef struct epb_ht_combine_args {
                                 address of every (t, k) expert row the
                                 receive reduces (own rows in place, others in
                                 the combine slots); NULL: resolved inline */
+  int32_t expert_rows_in_window; /* 1: expert_rows is the window's expert-
+                                    output region (bf16); the receive pulls
+                                    every row from its owner over NVLink */
 } epb_ht_combine_args;
 int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases,
                    const epb_ht_combine_args* args, void* stream);

@@ -25,11 +25,12 @@ class Config(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "algorithm", "num_ranks", "ranks_per_node", "num_experts", "top_k", "hidden",
         "max_tokens_per_rank", "token_dtype", "with_scales", "layout",
-        "ht_chunk_tokens", "ht_fifo_depth", "combine_dtype")]
+        "ht_chunk_tokens", "ht_fifo_depth", "combine_dtype", "ht_expert_out")]
 
 
 class WindowInfo(ctypes.Structure):
-    _fields_ = [("physical_bytes", ctypes.c_uint64), ("logical_bytes", ctypes.c_uint64)]
+    _fields_ = [("physical_bytes", ctypes.c_uint64), ("logical_bytes", ctypes.c_uint64),
+                ("expert_out_offset", ctypes.c_uint64), ("expert_out_rows", ctypes.c_uint64)]
 
 
 class Layout(ctypes.Structure):
@@ -67,7 +68,8 @@ class HTCombineArgs(ctypes.Structure):
                 ("recv_total", ctypes.c_int32), ("topk_idx", ctypes.c_void_p), ("weights", ctypes.c_void_p),
                 ("num_tokens", ctypes.c_int32), ("tok_rank", ctypes.c_void_p), ("offsets", ctypes.c_void_p),
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
-                ("dispatch_weights", ctypes.c_void_p), ("row_ptr", ctypes.c_void_p)]
+                ("dispatch_weights", ctypes.c_void_p), ("row_ptr", ctypes.c_void_p),
+                ("expert_rows_in_window", ctypes.c_int32)]
 
 
 PHASE_SEND, PHASE_RECV, PHASE_BOTH = 1, 2, 3

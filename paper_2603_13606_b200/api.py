@@ -196,6 +196,22 @@ class EpGroup:
         self._next_seq += 1
         return seq
 
+    def expert_out_view(self, rows: int) -> torch.Tensor:
+        """[rows, H] bf16 view of the window's registered expert-output
+        region (config.ht_expert_out)."""
+        off, cap = getattr(self, "_expert_out", (0, 0))
+        if not cap or not isinstance(self._buffer, torch.Tensor):
+            raise EpError(ErrorCode.INVALID_ARGUMENT, "group has no expert-output region (EpConfig.ht_expert_out)")
+        if rows > cap:
+            raise EpError(ErrorCode.CAPACITY_EXCEEDED, f"{rows} expert rows exceed the region ({cap})")
+        h = self.config.hidden
+        return self._buffer[off:off + rows * h * 2].view(torch.bfloat16).view(rows, h)
+
+    def _in_expert_out(self, t: torch.Tensor) -> bool:
+        off, cap = getattr(self, "_expert_out", (0, 0))
+        return bool(cap) and isinstance(self._buffer, torch.Tensor) and t.dtype == torch.bfloat16 and \
+            t.data_ptr() == self._buffer.data_ptr() + off
+
     def check(self) -> None:
         """Synchronise and raise any error the kernels recorded (timeouts,
         routing validation, weight mismatch)."""
@@ -335,6 +351,10 @@ def create_group(fabric, rank: int, config: EpConfig, hooks: Optional[Allocation
     ccfg = config.to_c(layout)
     info = _lib.WindowInfo()
     _lib.call("epb_window_geometry", ctypes.byref(ccfg), ctypes.byref(info))
+    if config.ht_expert_out and hooks is None:
+        # the expert-output region is handed out as a torch view of the window
+        hooks = AllocationHooks(allocate=lambda n, a: torch.empty(n, dtype=torch.uint8, device=torch.device(
+            "cuda", torch.cuda.current_device())), release=lambda b: None)
     buffer, wptr, wbytes = None, 0, 0
     if hooks is not None:
         buffer = hooks.allocate(int(info.physical_bytes), ALLOC_ALIGNMENT)
@@ -378,8 +398,10 @@ def create_group(fabric, rank: int, config: EpConfig, hooks: Optional[Allocation
             hooks.release(buffer)
         raise
     fabric.registered[rank] = int(info.physical_bytes)
-    return EpGroup(fabric, rank, config, layout, cg, int(info.logical_bytes), int(info.physical_bytes),
-                   hooks, buffer, strict)
+    grp = EpGroup(fabric, rank, config, layout, cg, int(info.logical_bytes), int(info.physical_bytes),
+                  hooks, buffer, strict)
+    grp._expert_out = (int(info.expert_out_offset), int(info.expert_out_rows))
+    return grp
 
 
 def destroy_group(group: EpGroup) -> None:
@@ -725,7 +747,8 @@ class EpHandle:
         a = _lib.HTCombineArgs(y.data_ptr(), y_dtype.code, res.origin.data_ptr(), res.recv_total,
                                self.routing.data_ptr(), w.data_ptr(), self._b, self._tok_rank.data_ptr(),
                                self._meta["offsets"].data_ptr(), o.data_ptr(), out.dtype.code,
-                               self._weights.data_ptr(), self._row_ptr_scratch().data_ptr())
+                               self._weights.data_ptr(), self._row_ptr_scratch().data_ptr(),
+                               int(g._in_expert_out(y)))
         if g._fused_ok() and g._marks is None:
             g._launch("epb_ht_combine", g._g, self._round, _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
         else:
@@ -739,6 +762,17 @@ class EpHandle:
             out.view().copy_(o)
         self._combine_stats = None
         self.state = HandleState.COMBINED
+
+    def expert_out_buffer(self) -> torch.Tensor:
+        """HT, EpConfig.ht_expert_out: a [recv_total, H] bf16 tensor in the
+        group's registered window for this round's expert outputs.  Passing
+        it (unchanged) as the combine input makes the combine zero-copy: each
+        home rank pulls its tokens' rows from the owners over NVLink.  Its
+        contents must stay until every rank's combine of the round is done
+        (the next round's metadata exchange orders that)."""
+        if self.config.algorithm is not Algorithm.HT:
+            raise EpError(ErrorCode.INVALID_ARGUMENT, "expert_out_buffer is an HT feature")
+        return self.group.expert_out_view(self._meta["recv_total"])
 
     def _row_ptr_scratch(self) -> torch.Tensor:
         n = max(1, self._b * self.config.top_k)

@@ -23,10 +23,15 @@ framework integration needs around it:
 
 Cached dispatch (a training backward pass): pass an existing handle; LL
 reuses its routing snapshot, HT opens a fresh metadata round for it.
+
+Zero-copy HT combine: get_expert_out_buffer(handle) hands out the expert
+output tensor inside the registered window; a combine on it is pulled by the
+token owners over NVLink instead of pushed.
 """
 
 from __future__ import annotations
 
+import dataclasses
 from typing import Optional
 
 import numpy as np
@@ -42,7 +47,11 @@ _TORCH_TO_DTYPE = {torch.float32: Dtype.F32, torch.bfloat16: Dtype.BF16, torch.f
 class Buffer:
     """One rank's EP communication buffer over an EpGroup."""
 
-    def __init__(self, fabric, rank: int, config: EpConfig, layout: str = "optimized", strict: bool = False):
+    def __init__(self, fabric, rank: int, config: EpConfig, layout: str = "optimized", strict: bool = False,
+                 zero_copy_combine: bool = True):
+        if config.algorithm is Algorithm.HT and zero_copy_combine and not config.ht_expert_out \
+                and config.hidden % 8 == 0:
+            config = dataclasses.replace(config, ht_expert_out=True)
         self.config = config
         self.rank = rank
         self._allocs: dict = {}
@@ -177,6 +186,11 @@ class Buffer:
         ev = self._leave(async_finish)
         self._last_event = ev
         return out, topk_weights, ev
+
+    def get_expert_out_buffer(self, handle: api.EpHandle) -> torch.Tensor:
+        """HT: [recv_total, H] bf16 tensor in the registered window for the
+        handle's expert outputs; combine(x=this tensor) is zero-copy."""
+        return handle.expert_out_buffer()
 
     # -- counts --------------------------------------------------------------------------
     def get_tokens_per_expert_list(self) -> list:

@@ -227,7 +227,9 @@ class NDTensor:
 
     def view(self) -> torch.Tensor:
         """The typed torch view (no copy)."""
-        return torch.as_strided(self.data, self.shape, self.strides, self.offset)
+        # storage_offset is absolute in the storage: a `data` that is itself a
+        # view (a slice of a larger tensor) contributes its own offset
+        return torch.as_strided(self.data, self.shape, self.strides, self.data.storage_offset() + self.offset)
 
     def is_contiguous_view(self) -> bool:
         return self.strides == _row_major_strides(self.shape)
@@ -381,6 +383,10 @@ class EpConfig:
     # extension: LL combine wire dtype (None = token_dtype, the reference's
     # ll.py:437-438); C2 "FP8 dispatch + bf16 combine" sets Dtype.BF16
     combine_dtype: "Dtype | None" = None
+    # extension: HT registered expert-output region in the window; a combine
+    # whose expert rows live there is pulled by the home ranks over NVLink
+    # (EpHandle.expert_out_buffer / Buffer.get_expert_out_buffer)
+    ht_expert_out: bool = False
 
     def __post_init__(self):
         n, e, k = self.num_ranks, self.num_experts, self.top_k
@@ -425,6 +431,8 @@ class EpConfig:
         fp = "|".join(str(p) for p in parts)
         if self.combine_dtype is not None:
             fp += "|c=" + self.combine_dtype.value
+        if self.ht_expert_out:
+            fp += "|yout"
         return fp.encode()
 
     @property
@@ -442,4 +450,5 @@ class EpConfig:
         c.layout = 0 if layout == "optimized" else 1
         c.ht_chunk_tokens, c.ht_fifo_depth = self.ht_chunk_tokens, self.ht_fifo_depth
         c.combine_dtype = -1 if self.combine_dtype is None else self.combine_dtype.code
+        c.ht_expert_out = int(self.ht_expert_out)
         return c

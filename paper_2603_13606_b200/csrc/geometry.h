@@ -8,6 +8,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "../../include/epb200.h"
 
 namespace epb {
@@ -51,6 +53,7 @@ struct HTGeom {
   int N, E, L, K, H, B, rpn, wire;
   int RB, RBp, WBp, HBp, rec_stride, crow_stride;
   uint64_t meta, meta_flag, dflag, cflag, stage, rec, crow;
+  uint64_t yout, yout_rows, yrow;  // registered expert-output region (ht_expert_out)
   uint64_t window_bytes, logical_bytes;
   uint64_t barrier;  // [N] u64 device-barrier flags
 };
@@ -116,7 +119,10 @@ inline void make_ht_geom(const epb_config& c, HTGeom& g) {
   g.stage = a256(g.cflag + g.N * 8);
   g.rec = a256(g.stage + (uint64_t)g.B * g.RBp);
   g.crow = a256(g.rec + (uint64_t)g.N * g.B * g.rec_stride);
-  g.barrier = a256(g.crow + (uint64_t)g.B * g.K * g.crow_stride);
+  g.yrow = a16(2 * (uint64_t)c.hidden);
+  g.yout_rows = c.ht_expert_out ? (uint64_t)g.N * g.B * (uint64_t)std::min(g.K, g.L) : 0;
+  g.yout = a256(g.crow + (uint64_t)g.B * g.K * g.crow_stride);
+  g.barrier = a256(g.yout + g.yout_rows * g.yrow);
   g.window_bytes = a256(g.barrier + (uint64_t)g.N * 8);
   // reference ht_regions (ht.py:78-174)
   const int nodes = c.num_ranks / c.ranks_per_node;

@@ -53,6 +53,8 @@ static int validate_config(const epb_config* c) {
     return fail(EPB_INVALID_ARGUMENT, "combine_dtype");
   if (c->layout != EPB_LAYOUT_OPTIMIZED && c->layout != EPB_LAYOUT_LEGACY)
     return fail(EPB_INVALID_ARGUMENT, "layout");
+  if (c->ht_expert_out && (c->algorithm != EPB_HT || c->hidden % 8))
+    return fail(EPB_INVALID_ARGUMENT, "ht_expert_out needs HT and hidden % 8 == 0");
   return EPB_OK;
 }
 
@@ -104,6 +106,8 @@ const char* epb_last_error(void) { return g_last_error.c_str(); }
 int epb_window_geometry(const epb_config* cfg, epb_window_info* out) {
   int rc = validate_config(cfg);
   if (rc) return rc;
+  out->expert_out_offset = 0;
+  out->expert_out_rows = 0;
   if (cfg->algorithm == EPB_LL) {
     LLGeom g;
     make_ll_geom(*cfg, g);
@@ -114,6 +118,8 @@ int epb_window_geometry(const epb_config* cfg, epb_window_info* out) {
     make_ht_geom(*cfg, g);
     out->physical_bytes = g.window_bytes;
     out->logical_bytes = g.logical_bytes;
+    out->expert_out_offset = g.yout;
+    out->expert_out_rows = g.yout_rows;
   }
   return EPB_OK;
 }

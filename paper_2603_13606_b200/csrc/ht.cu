@@ -400,6 +400,7 @@ struct HTCombSend {
   uint64_t* row_ptr;
   HTGeom g;
   int rows, rank, in_dtype, b;
+  int pull;  // expert rows are this rank's window region: homes pull them
   uint32_t tag;
 };
 
@@ -432,10 +433,22 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
     const int L = g.L;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.b * K; i += gridDim.x * blockDim.x) {
       const int e = (int)p.topk[i];
-      p.row_ptr[i] = e / L == me
-          ? reinterpret_cast<uint64_t>(p.y) + (uint64_t)(p.offsets[e * N + me] + p.tok_rank[i]) * bytes
-          : reinterpret_cast<uint64_t>(p.win + g.crow + (int64_t)i * g.crow_stride);
+      const uint64_t srow = (uint64_t)(p.offsets[e * N + me] + p.tok_rank[i]);  // row on owner(e)
+      if (p.pull)  // the owner's registered expert-output region, read over NVLink
+        p.row_ptr[i] = reinterpret_cast<uint64_t>(hpeer(p.peers, e / L) + g.yout) + srow * g.yrow;
+      else
+        p.row_ptr[i] = e / L == me ? reinterpret_cast<uint64_t>(p.y) + srow * bytes
+                                   : reinterpret_cast<uint64_t>(p.win + g.crow + (int64_t)i * g.crow_stride);
     }
+  }
+  if (p.pull) {
+    // nothing moves: announce that this rank's expert rows are complete
+    // (written by earlier kernels on this stream) to every home rank
+    if (blockIdx.x == 0 && (int)threadIdx.x < N && (int)threadIdx.x != me) {
+      fence_sys();
+      ht_publish_comb(p, threadIdx.x, 0);
+    }
+    return;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -518,7 +531,7 @@ EPB_DEV void ht_load8(const uint8_t* row, int c, float* y) {
 }
 
 template <int IT, int OT>
-__global__ void __launch_bounds__(kHTThreads, 2) ht_combine_recv_kernel(HTCombRecv p) {
+__global__ void __launch_bounds__(kHTThreads, 1) ht_combine_recv_kernel(HTCombRecv p) {
   __shared__ int s_fail;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H, L = g.L;
@@ -558,15 +571,15 @@ __global__ void __launch_bounds__(kHTThreads, 2) ht_combine_recv_kernel(HTCombRe
       if (lane < K) {
         const int64_t i = (int64_t)tk * K + lane;
         my_w = p.w[i];
-        if (p.row_ptr && one_node) {
-          my_row = p.row_ptr[i];
-        } else {
+        if (p.row_ptr) my_row = p.row_ptr[i];
+        if (!one_node || !p.row_ptr) {
           const int e = (int)p.topk[i];
           const int owner = e / L;
           my_node = owner / g.rpn;
-          my_row = owner == me
-              ? reinterpret_cast<uint64_t>(p.y_local) + (uint64_t)(p.offsets[e * N + me] + p.tok_rank[i]) * H * YB
-              : reinterpret_cast<uint64_t>(crow + i * g.crow_stride);
+          if (!p.row_ptr)
+            my_row = owner == me
+                ? reinterpret_cast<uint64_t>(p.y_local) + (uint64_t)(p.offsets[e * N + me] + p.tok_rank[i]) * H * YB
+                : reinterpret_cast<uint64_t>(crow + i * g.crow_stride);
         }
       }
     };
@@ -583,7 +596,7 @@ __global__ void __launch_bounds__(kHTThreads, 2) ht_combine_recv_kernel(HTCombRe
       if (one_node) {
         // single node: acc = p_0 + p_1 + ... (first present as init), then
         // out = 0 + acc; all KB rows of a batch are in flight at once
-        constexpr int KB = IT == EPB_F32 ? 2 : 4;
+        constexpr int KB = IT == EPB_F32 ? 4 : 8;  // rows in flight per lane
         constexpr int NV = IT == EPB_F32 ? 2 : 1;  // 16-B loads per 8-element chunk
         for (int k0 = 0; k0 < K; k0 += KB) {
           int4 v[KB][NV];
@@ -820,6 +833,11 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
   if (int rc = check_ht(g, phases)) return rc;
   if (a->in_dtype != EPB_F32 && a->in_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine input f32|bf16");
   if (a->recv_total > 0 && !a16(a->expert_rows)) return fail(EPB_INVALID_ARGUMENT, "expert rows must be 16-byte aligned");
+  if (a->expert_rows_in_window) {
+    if (a->in_dtype != EPB_BF16 || !a->row_ptr || g->ht.yout_rows < (uint64_t)std::max(a->recv_total, 0) ||
+        a->expert_rows != g->window + g->ht.yout)
+      return fail(EPB_INVALID_ARGUMENT, "pulled combine needs bf16 rows in the window's expert-output region");
+  }
   cudaStream_t s = as_stream(stream);
   if ((phases & 1) && a->dispatch_weights && a->num_tokens > 0) {
     // combine weights must equal the dispatched ones (ht.py:605-609)
@@ -838,7 +856,7 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
     p.peers = g->d_peers; p.done = g->d_done + g->cfg.num_ranks; p.g = g->ht; p.rows = a->recv_total;
     p.rank = g->rank; p.in_dtype = a->in_dtype; p.tag = ht_tag(round);
     p.topk = a->topk_idx; p.tok_rank = a->tok_rank; p.offsets = a->offsets; p.win = g->window;
-    p.row_ptr = a->row_ptr; p.b = a->num_tokens;
+    p.row_ptr = a->row_ptr; p.b = a->num_tokens; p.pull = a->expert_rows_in_window;
     const int grid = 2 * hsm_count();
     if (a->in_dtype == EPB_F32) ht_combine_send_kernel<EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
     else ht_combine_send_kernel<EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
@@ -853,7 +871,7 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
     p.offsets = a->offsets; p.out = a->out; p.win = g->window; p.err = g->d_err; p.g = g->ht;
     p.timeout_ns = g->timeout_ns; p.b = a->num_tokens; p.rank = g->rank; p.y_dtype = a->in_dtype;
     p.tag = ht_tag(round);
-    const int grid = 2 * hsm_count();
+    const int grid = hsm_count();
     if (a->in_dtype == EPB_F32) {
       if (a->out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_F32, EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
       else ht_combine_recv_kernel<EPB_F32, EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);

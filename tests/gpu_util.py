@@ -101,7 +101,7 @@ def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="referen
         fabric.shutdown()
 
 
-def run_ht(cfg, tokens, routing, weights, expert_fn, bf16_expert=False):
+def run_ht(cfg, tokens, routing, weights, expert_fn, bf16_expert=False, zero_copy=False):
     n = cfg.num_ranks
     h = cfg.hidden
     fabric = ep.Fabric(ep.NodeTopology(n, cfg.ranks_per_node))
@@ -120,8 +120,13 @@ def run_ht(cfg, tokens, routing, weights, expert_fn, bf16_expert=False):
             origin_w = res.origin_w.cpu().numpy()
             y = oht.apply_experts(rows, origin, expert_fn)
             ydt = ep.Dtype.BF16 if bf16_expert else ep.Dtype.F32
-            comb_in = [ep.tensor_from_f32(y, ydt, ep.TensorTag.TOKENS),
-                       ep.tensor_from_f32(weights[rank], ep.Dtype.F32, ep.TensorTag.TOPK_WEIGHTS)]
+            if zero_copy:  # expert rows written into the registered window region
+                yb = hd.expert_out_buffer()
+                yb.copy_(torch.from_numpy(y).to(yb.device).to(torch.bfloat16))
+                yin = ep.tensor_from_torch(yb, ep.TensorTag.TOKENS)
+            else:
+                yin = ep.tensor_from_f32(y, ydt, ep.TensorTag.TOKENS)
+            comb_in = [yin, ep.tensor_from_f32(weights[rank], ep.Dtype.F32, ep.TensorTag.TOPK_WEIGHTS)]
             comb_out = ep.tensor_create((routing[rank].shape[0], h), ep.Dtype.F32, ep.TensorTag.TOKENS)
             hd.combine(comb_in, [comb_out])
             out = dict(rows=rows, origin=origin, origin_w=origin_w, counts=out_cnt.read_f32(),

@@ -145,8 +145,8 @@ def buffer_ll(world, rank):
     buf.destroy()
 
 
-def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert):
-    cfg = ep.EpConfig(ep.Algorithm.HT, world, rpn, e, k, h, b, ep.Dtype.BF16)
+def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert, zero_copy=False):
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, rpn, e, k, h, b, ep.Dtype.BF16, ht_expert_out=zero_copy)
     fab = ep.ProcessFabric(ep.NodeTopology(world, rpn))
     g = ep.create_group(fab, rank, cfg)
     wl = owl.make_workload(e, world, b, k, h, seed)
@@ -166,7 +166,12 @@ def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert):
     np.testing.assert_array_equal(hd.dispatch_result.origin.cpu().numpy(), dd[rank]["origin"])
     ydt = ep.Dtype.BF16 if bf16_expert else ep.Dtype.F32
     co = ep.tensor_create((b, h), ep.Dtype.F32, T.TOKENS)
-    hd.combine([ep.tensor_from_f32(ys[rank], ydt, T.TOKENS), w], [co])
+    if zero_copy:
+        yb = hd.expert_out_buffer()
+        yb.copy_(torch.from_numpy(ys[rank]).cuda().to(torch.bfloat16))
+        hd.combine([ep.tensor_from_torch(yb, T.TOKENS), w], [co])
+    else:
+        hd.combine([ep.tensor_from_f32(ys[rank], ydt, T.TOKENS), w], [co])
     np.testing.assert_array_equal(co.read_f32(), want)
     hd.destroy()
     g.destroy()
@@ -191,6 +196,7 @@ def main():
                                                             None, 7, True, "ref", rounds=3, layout="legacy")),
         ("buffer wrapper ll c2 path", lambda: buffer_ll(world, rank)),
         ("ht bf16 single node", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 4, False)),
+        ("ht zero-copy combine (pull)", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 8, True, zero_copy=True)),
         ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
     ]
     failures = []

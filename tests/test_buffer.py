@@ -100,7 +100,8 @@ def test_buffer_ht_and_cached_dispatch(n):
             np.testing.assert_array_equal(rw.cpu().numpy(), dd[r]["weights"])
             ell = cfg.experts_per_rank
             assert buf.get_tokens_per_expert_list() == m[:, r * ell:(r + 1) * ell].sum(axis=0).tolist()
-            y = torch.from_numpy(ys[r]).to(dev).to(torch.bfloat16)
+            y = buf.get_expert_out_buffer(hd)  # zero-copy: expert rows written in the window
+            y.copy_(torch.from_numpy(ys[r]).to(dev).to(torch.bfloat16))
             out, _, _ = buf.combine(y, hd, w, out_dtype=torch.float32)
             outs.append(out.cpu().numpy())
         buf.destroy_handle(hd)

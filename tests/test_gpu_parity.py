@@ -286,6 +286,21 @@ def test_ht_dsv3_like_matches_oracle(n, rpn):
         np.testing.assert_array_equal(res[r]["out"], comb[r])
 
 
+@pytest.mark.parametrize("n,rpn", [(1, 1), (2, 2), (8, 8), (8, 2)])
+def test_ht_zero_copy_combine_pulls_from_window(n, rpn):
+    """EpConfig.ht_expert_out: expert rows written into the registered
+    window region; the home ranks pull them (no push pass), bit-exact."""
+    cfg = ep.EpConfig(ep.Algorithm.HT, n, rpn, 64, 8, 2048, 256, ep.Dtype.BF16, ht_expert_out=True)
+    wl = owl.make_workload(64, n, 256, 8, 2048, seed=17)
+    res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_affine, zero_copy=True)
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, 64, n, 2048, "bf16")
+    ys = [bf16_round(oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_affine)) for r in range(n)]
+    comb = oht.combine(ys, wl.routing, wl.weights, 64, n, rpn)
+    for r in range(n):
+        np.testing.assert_array_equal(res[r]["rows"], dd[r]["rows"])
+        np.testing.assert_array_equal(res[r]["out"], comb[r])
+
+
 def test_ht_bf16_expert_rows_are_exact():
     cfg = make_cfg("ht", 4, 4, 32, 64, 4, 512, "bf16")
     wl = owl.make_workload(32, 4, 64, 4, 512, seed=9)

@@ -152,3 +152,13 @@ def test_process_bootstrap_config_mismatch_gloo():
         p.join(60)
     assert [r[2] for r in res] == ["ConfigMismatch", "ConfigMismatch"]
     assert res[0][1] == ["hello-0", "hello-1"]
+
+
+def test_tensor_from_torch_keeps_the_view_offset():
+    """A slice of a larger tensor wraps zero-copy at its own address (the
+    Buffer's window views and user sub-tensors rely on it)."""
+    base = torch.arange(100, dtype=torch.float32)
+    v = base[10:30].view(4, 5)
+    t = ep.tensor_from_torch(v, ep.TensorTag.TOKENS)
+    assert t.view().data_ptr() == v.data_ptr()
+    np.testing.assert_array_equal(t.read_f32(), v.numpy())
