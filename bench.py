@@ -460,7 +460,9 @@ def run_ht(args, world, rank):
     import paper_2603_13606_b200 as ep
     from oracle import workload as owl
     b = args.ht_tokens
-    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, E, K, H, b, ep.Dtype.BF16)
+    # expert outputs are written into the group's registered window region
+    # (EpHandle.expert_out_buffer), so the combine is pulled, not pushed
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, E, K, H, b, ep.Dtype.BF16, ht_expert_out=True)
     g = make_group(world, rank, cfg, strict=False)
     wl = owl.make_workload(E, world, b, K, H, seed=7)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -484,12 +486,14 @@ def run_ht(args, world, rank):
             bufs[tot] = (torch.zeros((tot, H), dtype=torch.bfloat16, device=dev),
                          torch.randn((tot, H), device=dev).to(torch.bfloat16))
         rt, yt = bufs[tot]
+        yw = h.expert_out_buffer()
+        yw.copy_(yt)  # stand-in for the expert GEMM writing its output (untimed)
         flush.zero_()
         g.device_barrier()
         g.trace_phases(marks)
         h.dispatch([X, Wt], [ep.tensor_from_torch(rt, T.TOKENS), CNT])
         g.mark("dispatch:end")
-        h.combine([ep.tensor_from_torch(yt, T.TOKENS), Wt], [OUT])
+        h.combine([ep.tensor_from_torch(yw, T.TOKENS), Wt], [OUT])
         g.mark("combine:end")
         g.trace_phases(None)
         h.destroy()
@@ -537,6 +541,8 @@ def run_ht(args, world, rank):
         "per_rank_us": {"dispatch": [round(v * 1e3, 1) for v in per_d], "combine": [round(v * 1e3, 1) for v in per_c],
                         "dispatch_send": [round(v * 1e3, 1) for v in ph_send],
                         "dispatch_recv": [round(v * 1e3, 1) for v in ph_recv]},
+        "transport": "dispatch: pull (rows staged in the sender's window, read once per (token, rank) over "
+                     "NVLink); combine: pull (expert outputs in the registered window, read by the token's home)",
         "note": "payload = bf16 rows per (token, destination rank) for dispatch and per (token, k) "
                 "for combine, all destinations incl. self; nvlink = remote part only",
     }
