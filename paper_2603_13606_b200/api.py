@@ -623,11 +623,11 @@ class EpHandle:
         if g.strict:
             g.check()
         if back_t:
-            out_tokens.view().copy_(out_t)
+            out_tokens.view().copy_(out_t, non_blocking=not g.strict)
         if back_s:
-            out_scales.view().copy_(out_s)
+            out_scales.view().copy_(out_s, non_blocking=not g.strict)
         if back_c:
-            out_counts.view().copy_(cnt_f)
+            out_counts.view().copy_(cnt_f, non_blocking=not g.strict)
         self._dispatch_result = LLDispatchResult(out_t, self._counts_i32, self._src_info, out_s,
                                                  _stats_fn=self._ll_dispatch_stats)
         self._keep_alive = None
@@ -659,7 +659,7 @@ class EpHandle:
         if g.strict:
             g.check()
         if back_t:
-            out_tokens.view().copy_(out_t)
+            out_tokens.view().copy_(out_t, non_blocking=not g.strict)
         ell, n = cfg.experts_per_rank, cfg.num_ranks
         lo = g.rank * ell
         hi = min(lo + ell, cfg.num_experts)
@@ -732,7 +732,7 @@ class EpHandle:
         if g.strict:
             g.check()
         if back:
-            out.view().copy_(o)
+            out.view().copy_(o, non_blocking=not g.strict)
         self._combine_stats = None
         self.state = HandleState.COMBINED
 
@@ -759,7 +759,7 @@ class EpHandle:
         if g.strict:
             g.check()
         if back:
-            out.view().copy_(o)
+            out.view().copy_(o, non_blocking=not g.strict)
         self._combine_stats = None
         self.state = HandleState.COMBINED
 
