@@ -495,7 +495,7 @@ def run_ht(args, world, rank):
     b = args.ht_tokens
     # expert outputs are written into the group's registered window region
     # (EpHandle.expert_out_buffer), so the combine is pulled, not pushed
-    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, E, K, H, b, ep.Dtype.BF16, ht_expert_out=True)
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, E, K, H, b, ep.Dtype.BF16, expert_out_window=True)
     g = make_group(world, rank, cfg, strict=False)
     wl = owl.make_workload(E, world, b, K, H, seed=7)
     dev = torch.device("cuda", torch.cuda.current_device())

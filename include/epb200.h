@@ -86,16 +86,17 @@ typedef struct epb_config {
   int32_t ht_chunk_tokens;  /* kept for fingerprint parity */
   int32_t ht_fifo_depth;
   int32_t combine_dtype;    /* LL combine wire dtype; -1 = token_dtype (reference) */
-  int32_t ht_expert_out;    /* HT: reserve a registered expert-output region in
-                               the window (N*B*min(K,L) bf16 rows); a combine
-                               whose input IS that region is pulled by the
-                               token's home rank over NVLink (no push pass) */
+  int32_t expert_out_window; /* reserve a registered expert-output region in
+                               the window (HT: N*B*min(K,L) bf16 rows; LL:
+                               [L][N*B] bf16 rows, bf16 combine wire); a
+                               combine whose input IS that region is pulled
+                               by the token's home rank over NVLink */
 } epb_config;
 
 typedef struct epb_window_info {
   uint64_t physical_bytes;  /* bytes this library needs (16-B aligned slots) */
   uint64_t logical_bytes;   /* the reference's window_bytes (footprint parity) */
-  uint64_t expert_out_offset; /* HT with ht_expert_out: byte offset of the
+  uint64_t expert_out_offset; /* HT with expert_out_window: byte offset of the
                                  expert-output region in the window */
   uint64_t expert_out_rows;   /* its capacity in rows of hidden bf16 */
 } epb_window_info;
@@ -174,6 +175,9 @@ typedef struct epb_ll_dispatch_args {
   int32_t* self_row;        /* send: [b, K] output row of (t, k) when e_tk is
                                this rank's own expert (placed directly, no
                                window hop), else -1; combine input           */
+  int32_t* owner_row;       /* send, nullable: [b, K] row of (t, k) in the
+                               dispatch output of e_tk's owner (pulled
+                               combine input)                                */
 } epb_ll_dispatch_args;
 
 /* K2 + K3: LL dispatch (ll.py:227-400) */
@@ -193,6 +197,9 @@ typedef struct epb_ll_combine_args {
   const int64_t* topk;      /* [b, K] routing of the handle; required by the
                                legacy layout (combine slot e*B + t,
                                ll.py:433-436), unused by the optimized one  */
+  const int32_t* owner_row; /* [b, K] from the dispatch (pulled combine)      */
+  int32_t expert_out_in_window; /* 1: expert_out is the window's expert-output
+                               region; homes pull their rows over NVLink    */
 } epb_ll_combine_args;
 
 /* K4a + K4b: LL combine (ll.py:404-507) */

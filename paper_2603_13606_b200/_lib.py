@@ -25,7 +25,7 @@ class Config(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "algorithm", "num_ranks", "ranks_per_node", "num_experts", "top_k", "hidden",
         "max_tokens_per_rank", "token_dtype", "with_scales", "layout",
-        "ht_chunk_tokens", "ht_fifo_depth", "combine_dtype", "ht_expert_out")]
+        "ht_chunk_tokens", "ht_fifo_depth", "combine_dtype", "expert_out_window")]
 
 
 class WindowInfo(ctypes.Structure):
@@ -44,7 +44,7 @@ class LLDispatchArgs(ctypes.Structure):
                 ("topk_idx", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("out_scales", ctypes.c_void_p),
                 ("counts_f32", ctypes.c_void_p), ("counts_i32", ctypes.c_void_p),
-                ("src_info", ctypes.c_void_p), ("self_row", ctypes.c_void_p)]
+                ("src_info", ctypes.c_void_p), ("self_row", ctypes.c_void_p), ("owner_row", ctypes.c_void_p)]
 
 
 class LLCombineArgs(ctypes.Structure):
@@ -52,7 +52,8 @@ class LLCombineArgs(ctypes.Structure):
                 ("counts_i32", ctypes.c_void_p), ("src_info", ctypes.c_void_p),
                 ("weights", ctypes.c_void_p), ("num_tokens", ctypes.c_int32),
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("self_row", ctypes.c_void_p),
-                ("topk", ctypes.c_void_p)]
+                ("topk", ctypes.c_void_p), ("owner_row", ctypes.c_void_p),
+                ("expert_out_in_window", ctypes.c_int32)]
 
 
 class HTDispatchArgs(ctypes.Structure):

@@ -198,10 +198,10 @@ class EpGroup:
 
     def expert_out_view(self, rows: int) -> torch.Tensor:
         """[rows, H] bf16 view of the window's registered expert-output
-        region (config.ht_expert_out)."""
+        region (config.expert_out_window)."""
         off, cap = getattr(self, "_expert_out", (0, 0))
         if not cap or not isinstance(self._buffer, torch.Tensor):
-            raise EpError(ErrorCode.INVALID_ARGUMENT, "group has no expert-output region (EpConfig.ht_expert_out)")
+            raise EpError(ErrorCode.INVALID_ARGUMENT, "group has no expert-output region (EpConfig.expert_out_window)")
         if rows > cap:
             raise EpError(ErrorCode.CAPACITY_EXCEEDED, f"{rows} expert rows exceed the region ({cap})")
         h = self.config.hidden
@@ -351,7 +351,7 @@ def create_group(fabric, rank: int, config: EpConfig, hooks: Optional[Allocation
     ccfg = config.to_c(layout)
     info = _lib.WindowInfo()
     _lib.call("epb_window_geometry", ctypes.byref(ccfg), ctypes.byref(info))
-    if config.ht_expert_out and hooks is None:
+    if config.expert_out_window and hooks is None:
         # the expert-output region is handed out as a torch view of the window
         hooks = AllocationHooks(allocate=lambda n, a: torch.empty(n, dtype=torch.uint8, device=torch.device(
             "cuda", torch.cuda.current_device())), release=lambda b: None)
@@ -595,11 +595,13 @@ class EpHandle:
             self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
             self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
             self._self_row = torch.empty(max(b, 1) * cfg.top_k, dtype=torch.int32, device=dev)
+            self._owner_row = torch.empty(max(b, 1) * cfg.top_k, dtype=torch.int32, device=dev) \
+                if g._expert_out[1] else None
             a = _lib.LLDispatchArgs(x.data_ptr(), tokens.dtype.code, xs.data_ptr() if xs is not None else None,
                                     self.routing.data_ptr(), b, out_t.data_ptr(), out_tokens.dtype.code,
                                     out_s.data_ptr() if out_s is not None else None, cnt_f.data_ptr(),
                                     self._counts_i32.data_ptr(), self._src_info.data_ptr(),
-                                    self._self_row.data_ptr())
+                                    self._self_row.data_ptr(), _ptr(self._owner_row))
             self._ll_args = a
             self._keep_alive = (x, xs)
             self._staged = (out_tokens, out_counts, out_scales, out_t, out_s, cnt_f, back_t, back_s, back_c)
@@ -709,7 +711,8 @@ class EpHandle:
             o, back = self._dev_out(out, full=True)
             a = _lib.LLCombineArgs(y.data_ptr(), rows_in.dtype.code, self._counts_i32.data_ptr(),
                                    self._src_info.data_ptr(), w.data_ptr(), b, o.data_ptr(), out.dtype.code,
-                                   self._self_row.data_ptr(), self.routing.data_ptr() if b else None)
+                                   self._self_row.data_ptr(), self.routing.data_ptr() if b else None,
+                                   _ptr(self._owner_row), int(g._in_expert_out(y)))
             self._ll_cargs = a
             self._staged = (out, o, back, w, y)
             if send_only:
@@ -764,14 +767,18 @@ class EpHandle:
         self.state = HandleState.COMBINED
 
     def expert_out_buffer(self) -> torch.Tensor:
-        """HT, EpConfig.ht_expert_out: a [recv_total, H] bf16 tensor in the
-        group's registered window for this round's expert outputs.  Passing
-        it (unchanged) as the combine input makes the combine zero-copy: each
-        home rank pulls its tokens' rows from the owners over NVLink.  Its
-        contents must stay until every rank's combine of the round is done
-        (the next round's metadata exchange orders that)."""
-        if self.config.algorithm is not Algorithm.HT:
-            raise EpError(ErrorCode.INVALID_ARGUMENT, "expert_out_buffer is an HT feature")
+        """EpConfig.expert_out_window: a bf16 tensor in the group's
+        registered window for this round's expert outputs — HT [recv_total,
+        H], LL [L, N*B, H] (the dispatch output layout).  Passing it
+        (unchanged) as the combine input makes the combine zero-copy: each
+        home rank pulls its tokens' rows from the owners over NVLink.  One
+        region per group: its contents must stay until every rank's combine
+        of the round is done (the next round's dispatch orders that), so LL
+        rounds pipelined on two handles must not both use it."""
+        if self.config.algorithm is Algorithm.LL:
+            cfg = self.config
+            rows = cfg.experts_per_rank * cfg.num_ranks * cfg.max_tokens_per_rank
+            return self.group.expert_out_view(rows).view(cfg.experts_per_rank, -1, cfg.hidden)
         return self.group.expert_out_view(self._meta["recv_total"])
 
     def _row_ptr_scratch(self) -> torch.Tensor:

@@ -49,9 +49,9 @@ class Buffer:
 
     def __init__(self, fabric, rank: int, config: EpConfig, layout: str = "optimized", strict: bool = False,
                  zero_copy_combine: bool = True):
-        if config.algorithm is Algorithm.HT and zero_copy_combine and not config.ht_expert_out \
+        if config.algorithm is Algorithm.HT and zero_copy_combine and not config.expert_out_window \
                 and config.hidden % 8 == 0:
-            config = dataclasses.replace(config, ht_expert_out=True)
+            config = dataclasses.replace(config, expert_out_window=True)
         self.config = config
         self.rank = rank
         self._allocs: dict = {}

@@ -386,7 +386,7 @@ class EpConfig:
     # extension: HT registered expert-output region in the window; a combine
     # whose expert rows live there is pulled by the home ranks over NVLink
     # (EpHandle.expert_out_buffer / Buffer.get_expert_out_buffer)
-    ht_expert_out: bool = False
+    expert_out_window: bool = False
 
     def __post_init__(self):
         n, e, k = self.num_ranks, self.num_experts, self.top_k
@@ -431,7 +431,7 @@ class EpConfig:
         fp = "|".join(str(p) for p in parts)
         if self.combine_dtype is not None:
             fp += "|c=" + self.combine_dtype.value
-        if self.ht_expert_out:
+        if self.expert_out_window:
             fp += "|yout"
         return fp.encode()
 
@@ -450,5 +450,5 @@ class EpConfig:
         c.layout = 0 if layout == "optimized" else 1
         c.ht_chunk_tokens, c.ht_fifo_depth = self.ht_chunk_tokens, self.ht_fifo_depth
         c.combine_dtype = -1 if self.combine_dtype is None else self.combine_dtype.code
-        c.ht_expert_out = int(self.ht_expert_out)
+        c.expert_out_window = int(self.expert_out_window)
         return c

@@ -40,6 +40,7 @@ struct LLGeom {
   uint64_t Kmagic;  // ceil(2^32 / K): token of a routing item i / K (i * K < 2^32)
   uint64_t parity_bytes, window_bytes, logical_bytes;
   uint64_t barrier;  // [N] u64 device-barrier flags (after both parities)
+  uint64_t yout, yout_rows, yrow;  // registered expert-output region [L][N*B] bf16 rows (expert_out_window)
 };
 
 // HT:
@@ -53,7 +54,7 @@ struct HTGeom {
   int N, E, L, K, H, B, rpn, wire;
   int RB, RBp, WBp, HBp, rec_stride, crow_stride;
   uint64_t meta, meta_flag, dflag, cflag, stage, rec, crow;
-  uint64_t yout, yout_rows, yrow;  // registered expert-output region (ht_expert_out)
+  uint64_t yout, yout_rows, yrow;  // registered expert-output region (expert_out_window)
   uint64_t window_bytes, logical_bytes;
   uint64_t barrier;  // [N] u64 device-barrier flags
 };
@@ -93,7 +94,10 @@ inline void make_ll_geom(const epb_config& c, LLGeom& g) {
   g.disp_slot = a256(g.comb_flag + (uint64_t)g.N * g.grid * 8);
   g.comb_slot = a256(g.disp_slot + (uint64_t)g.n_disp * g.slot_stride);
   g.parity_bytes = a256(g.comb_slot + (uint64_t)g.n_comb * g.comb_stride);
-  g.barrier = 2 * g.parity_bytes;
+  g.yrow = a16(2 * (uint64_t)c.hidden);
+  g.yout_rows = c.expert_out_window ? (uint64_t)g.L * g.N * g.B : 0;
+  g.yout = 2 * g.parity_bytes;
+  g.barrier = a256(g.yout + g.yout_rows * g.yrow);
   g.window_bytes = a256(g.barrier + (uint64_t)g.N * 8);
   // reference ll_regions (ll.py:58-121)
   const uint64_t ref_slot = (uint64_t)(g.HB + g.RB + g.SB);
@@ -120,7 +124,7 @@ inline void make_ht_geom(const epb_config& c, HTGeom& g) {
   g.rec = a256(g.stage + (uint64_t)g.B * g.RBp);
   g.crow = a256(g.rec + (uint64_t)g.N * g.B * g.rec_stride);
   g.yrow = a16(2 * (uint64_t)c.hidden);
-  g.yout_rows = c.ht_expert_out ? (uint64_t)g.N * g.B * (uint64_t)std::min(g.K, g.L) : 0;
+  g.yout_rows = c.expert_out_window ? (uint64_t)g.N * g.B * (uint64_t)std::min(g.K, g.L) : 0;
   g.yout = a256(g.crow + (uint64_t)g.B * g.K * g.crow_stride);
   g.barrier = a256(g.yout + g.yout_rows * g.yrow);
   g.window_bytes = a256(g.barrier + (uint64_t)g.N * 8);

@@ -53,8 +53,11 @@ static int validate_config(const epb_config* c) {
     return fail(EPB_INVALID_ARGUMENT, "combine_dtype");
   if (c->layout != EPB_LAYOUT_OPTIMIZED && c->layout != EPB_LAYOUT_LEGACY)
     return fail(EPB_INVALID_ARGUMENT, "layout");
-  if (c->ht_expert_out && (c->algorithm != EPB_HT || c->hidden % 8))
-    return fail(EPB_INVALID_ARGUMENT, "ht_expert_out needs HT and hidden % 8 == 0");
+  if (c->expert_out_window && c->hidden % 8)
+    return fail(EPB_INVALID_ARGUMENT, "expert_out_window needs hidden % 8 == 0");
+  if (c->expert_out_window && c->algorithm == EPB_LL &&
+      (c->combine_dtype < 0 ? c->token_dtype : c->combine_dtype) != EPB_BF16)
+    return fail(EPB_INVALID_ARGUMENT, "LL expert_out_window needs a bf16 combine wire");
   return EPB_OK;
 }
 
@@ -113,6 +116,8 @@ int epb_window_geometry(const epb_config* cfg, epb_window_info* out) {
     make_ll_geom(*cfg, g);
     out->physical_bytes = g.window_bytes;
     out->logical_bytes = g.logical_bytes;
+    out->expert_out_offset = g.yout;
+    out->expert_out_rows = g.yout_rows;
   } else {
     HTGeom g;
     make_ht_geom(*cfg, g);

@@ -162,6 +162,7 @@ struct LLDisp {
   int32_t* counts_i32;
   int32_t* src_info;
   int32_t* self_row;     // [b*K] row of (t, k) in this rank's output if e_tk is local, else -1
+  int32_t* owner_row;    // [b*K] row of (t, k) in e_tk's owner's output (pulled combine), nullable
   const uint64_t* peers;
   const uint8_t* win;
   int* err;
@@ -530,6 +531,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           const int srow = mine ? (e - p.rank * L) * N * B + p.rank * B + ci : -1;
           s_self[lane] = srow;
           if (p.self_row) p.self_row[(int64_t)t * K + lane] = srow;
+          if (p.owner_row) p.owner_row[(int64_t)t * K + lane] = (e - d * L) * N * B + p.rank * B + ci;
           if (mine) p.src_info[srow] = t * K + lane;
           if (first) {
             const int pos = __popc(fm & ((1u << lane) - 1u));
@@ -727,6 +729,8 @@ struct LLComb {
   const int32_t* src_info;
   const int32_t* self_row;  // [b*K] from the dispatch: rows of own experts are read in place
   const int64_t* topk;      // [b*K] routing (legacy layout: slot e*B + t)
+  const int32_t* owner_row; // [b*K] from the dispatch: row of (t, k) on e_tk's owner
+  int pull;                 // expert outputs live in every rank's window: homes pull them
   const float* w;
   void* out;
   const uint32_t* hseq;
@@ -757,7 +761,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
   const bool vec = (H & 15) == 0;
   const int nch = vec ? H / EPC : 0;
   // rows of this rank's own source tokens never travel: only N > 1 sends
-  const bool send = (p.phases & kPhaseSend) && N > 1;
+  const bool send = (p.phases & kPhaseSend) && N > 1 && !p.pull;
   const int P = L * N;
   const int per = (P + blockDim.x - 1) / blockDim.x;
   const int i0 = threadIdx.x * per;
@@ -849,6 +853,15 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
       st_flag(flag, (uint64_t)tag, sys);
     }
     LL_STAMP(p, 3);
+  } else if ((p.phases & kPhaseSend) && N > 1 && p.pull) {
+    // pulled combine: nothing moves; announce that this rank's expert
+    // outputs (written by earlier kernels on this stream) are complete
+    if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
+      fence_scoped(sys);
+      uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.comb_flag) +
+                       (int64_t)p.rank * G + blockIdx.x;
+      st_flag(flag, (uint64_t)tag, sys);
+    }
   }
 
   if (p.phases & kPhaseRecv) {
@@ -866,12 +879,20 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // the first task's rows are resolved before the flag wait
     const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
     int my_self = -1, my_slot = 0;
+    uint64_t my_pull = 0;  // pulled combine: the row in its owner's window
     float my_w = 0.0f;
     auto fetch = [&](int tk) {  // lane k's row of token tk
       if (lane < K) {
-        my_self = p.self_row ? p.self_row[(int64_t)tk * K + lane] : -1;
-        my_w = p.w[(int64_t)tk * K + lane];
-        my_slot = legacy ? (int)p.topk[(int64_t)tk * K + lane] * B + tk : tk * K + lane;
+        const int64_t i = (int64_t)tk * K + lane;
+        my_w = p.w[i];
+        if (p.pull) {
+          const int e = (int)p.topk[i];
+          const int owner = (int)(((uint64_t)e * g.Lmagic) >> 32);
+          my_pull = reinterpret_cast<uint64_t>(peer_base(p.peers, owner) + g.yout) + (uint64_t)p.owner_row[i] * g.yrow;
+        } else {
+          my_self = p.self_row ? p.self_row[i] : -1;
+          my_slot = legacy ? (int)p.topk[i] * B + tk : tk * K + lane;
+        }
       }
     };
     if (vec && task < tasks) fetch(task / segs);
@@ -890,9 +911,10 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         const int cbase = sg * kSeg + lane;
         const bool ok0 = cbase < nch, ok1 = cbase + 32 < nch;
         const uint8_t* my_row =
-            my_self >= 0 ? reinterpret_cast<const uint8_t*>(p.y) + (int64_t)my_self * H * dtype_width(IT)
-                         : slots + (int64_t)my_slot * g.comb_stride;
-        const bool my_in_y = my_self >= 0;
+            p.pull ? reinterpret_cast<const uint8_t*>(my_pull)
+                   : (my_self >= 0 ? reinterpret_cast<const uint8_t*>(p.y) + (int64_t)my_self * H * dtype_width(IT)
+                                   : slots + (int64_t)my_slot * g.comb_stride);
+        const bool my_in_y = !p.pull && my_self >= 0;
         float acc0[EPC], acc1[EPC];
 #pragma unroll
         for (int i = 0; i < EPC; ++i) acc0[i] = acc1[i] = 0.0f;
@@ -960,9 +982,14 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         for (int el = threadIdx.x; el < H; el += blockDim.x) {
           float acc = 0.0f;
           for (int k = 0; k < K; ++k) {
-            const int sr = p.self_row ? p.self_row[(int64_t)t * K + k] : -1;
+            const int sr = p.self_row && !p.pull ? p.self_row[(int64_t)t * K + k] : -1;
             float y;
-            if (sr >= 0) {
+            if (p.pull) {
+              const int e = (int)p.topk[(int64_t)t * K + k];
+              const uint8_t* row = peer_base(p.peers, (int)(((uint64_t)e * g.Lmagic) >> 32)) + g.yout +
+                                   (uint64_t)p.owner_row[(int64_t)t * K + k] * g.yrow;
+              y = load_elem(row, WT, el);
+            } else if (sr >= 0) {
               uint32_t wire = 0;  // own expert row, rounded through the wire dtype
               store_elem(&wire, WT, 0,
                          load_elem(reinterpret_cast<const uint8_t*>(p.y) + (int64_t)sr * H * dtype_width(IT), IT, el));
@@ -1119,7 +1146,8 @@ int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases, const epb_ll_d
   LLDisp p;
   p.x = a->x; p.x_scales = a->x_scales; p.topk = a->topk_idx; p.hseq = hseq;
   p.out = a->out; p.out_scales = a->out_scales; p.counts_f32 = a->counts_f32; p.counts_i32 = a->counts_i32;
-  p.src_info = a->src_info; p.self_row = a->self_row; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err;
+  p.src_info = a->src_info; p.self_row = a->self_row; p.owner_row = a->owner_row;
+  p.peers = g->d_peers; p.win = g->window; p.err = g->d_err;
   p.dseq = reinterpret_cast<uint32_t*>(g->d_scratch); p.drd = g->d_scratch + 1; p.trace = g->trace;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;
@@ -1160,6 +1188,10 @@ int epb_ll_combine(epb_group* g, const uint32_t* hseq, int32_t phases, const epb
     return fail(EPB_INVALID_ARGUMENT, "legacy layout combine needs the routing (topk)");
   p.y = a->expert_out; p.counts = a->counts_i32; p.src_info = a->src_info; p.self_row = a->self_row;
   p.topk = a->topk; p.w = a->weights; p.out = a->out;
+  p.owner_row = a->owner_row; p.pull = a->expert_out_in_window;
+  if (p.pull && (a->in_dtype != EPB_BF16 || g->ll.cwire != EPB_BF16 || !a->topk || !a->owner_row ||
+                 g->ll.yout_rows == 0 || a->expert_out != g->window + g->ll.yout))
+    return fail(EPB_INVALID_ARGUMENT, "pulled combine needs bf16 rows in the window's expert-output region");
   p.hseq = hseq; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err; p.trace = g->trace;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;

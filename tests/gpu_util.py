@@ -46,7 +46,7 @@ def dispatch_inputs(cfg, tokens, weights, mode="reference"):
 
 
 def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="reference",
-           wire_out=False, bf16_expert=False, rounds=1, layout="optimized"):
+           wire_out=False, bf16_expert=False, rounds=1, layout="optimized", zero_copy=False):
     """Returns per rank dict(recv, counts, out, recv_total)."""
     n = cfg.num_ranks
     bmax, h = cfg.max_tokens_per_rank, cfg.hidden
@@ -81,8 +81,13 @@ def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="referen
                     recv = out_tok.read_f32()
                 rows = oll.apply_experts(recv, counts.astype(np.int64), rank, cfg.num_experts, n, bmax, expert_fn)
                 ydt = ep.Dtype.BF16 if bf16_expert else ep.Dtype.F32
-                comb_in = [ep.tensor_from_f32(rows, ydt, ep.TensorTag.TOKENS),
-                           ep.tensor_from_f32(weights[rank], ep.Dtype.F32, ep.TensorTag.TOPK_WEIGHTS)]
+                if zero_copy:  # expert outputs written into the registered window region
+                    yb = hd.expert_out_buffer()
+                    yb.copy_(torch.from_numpy(rows).to(yb.device).to(torch.bfloat16))
+                    yin = ep.tensor_from_torch(yb, ep.TensorTag.TOKENS)
+                else:
+                    yin = ep.tensor_from_f32(rows, ydt, ep.TensorTag.TOKENS)
+                comb_in = [yin, ep.tensor_from_f32(weights[rank], ep.Dtype.F32, ep.TensorTag.TOPK_WEIGHTS)]
                 comb_out = ep.tensor_create((routing[rank].shape[0], h), ep.Dtype.F32, ep.TensorTag.TOKENS)
                 hd.combine(comb_in, [comb_out], send_only=staged)
                 if staged:

@@ -31,8 +31,9 @@ def bf16r(x):
 
 
 def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, staged, mode, rounds=1,
-            layout="optimized"):
-    cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, bmax, dtype, scales, combine_dtype=combine_dtype)
+            layout="optimized", zero_copy=False):
+    cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, bmax, dtype, scales, combine_dtype=combine_dtype,
+                      expert_out_window=zero_copy)
     fab = ep.ProcessFabric(ep.NodeTopology(world, world))
     g = ep.create_group(fab, rank, cfg, layout=layout)
     ell = cfg.experts_per_rank
@@ -69,8 +70,13 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
             idx = (plan[:, 0], plan[:, 1] * bmax + plan[:, 2])
             np.testing.assert_array_equal(recv[idx], d[rank]["recv"][idx])
         y = ys[rank]
-        comb_in = [ep.tensor_from_f32(y, ep.Dtype.BF16, T.TOKENS),
-                   ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)]
+        if zero_copy:
+            yb = hd.expert_out_buffer()
+            yb.copy_(torch.from_numpy(y).cuda().to(torch.bfloat16))
+            yin = ep.tensor_from_torch(yb, T.TOKENS)
+        else:
+            yin = ep.tensor_from_f32(y, ep.Dtype.BF16, T.TOKENS)
+        comb_in = [yin, ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)]
         comb_out = ep.tensor_create((bmax, h), ep.Dtype.F32, T.TOKENS)
         hd.combine(comb_in, [comb_out], send_only=staged)
         if staged:
@@ -146,7 +152,7 @@ def buffer_ll(world, rank):
 
 
 def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert, zero_copy=False):
-    cfg = ep.EpConfig(ep.Algorithm.HT, world, rpn, e, k, h, b, ep.Dtype.BF16, ht_expert_out=zero_copy)
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, rpn, e, k, h, b, ep.Dtype.BF16, expert_out_window=zero_copy)
     fab = ep.ProcessFabric(ep.NodeTopology(world, rpn))
     g = ep.create_group(fab, rank, cfg)
     wl = owl.make_workload(e, world, b, k, h, seed)
@@ -190,6 +196,8 @@ def main():
         ("ll staged bf16 uneven", lambda: ll_case(world, rank, 3 * world + 1, 3, 256, 12, ep.Dtype.BF16, False, None,
                                                   3, True, "ref", rounds=3)),
         ("ll pipelined parities", lambda: ll_pipelined(world, rank)),
+        ("ll zero-copy combine (pull) c2", lambda: ll_case(world, rank, 256, 8, 7168, 128, ep.Dtype.FP8, True,
+                                                            ep.Dtype.BF16, 9, False, "bf16", rounds=3, zero_copy=True)),
         ("ll legacy layout c2 hot path", lambda: ll_case(world, rank, 256, 8, 7168, 64, ep.Dtype.FP8, True,
                                                           ep.Dtype.BF16, 6, False, "bf16", rounds=2, layout="legacy")),
         ("ll legacy layout staged uneven", lambda: ll_case(world, rank, 3 * world + 1, 3, 256, 12, ep.Dtype.BF16, False,

@@ -249,6 +249,21 @@ def test_ll_legacy_layout_c2_hot_path(n):
         _check_ll(cfg, [res[r][rnd] for r in range(n)], d, comb)
 
 
+@pytest.mark.parametrize("n,layout", [(1, "optimized"), (4, "optimized"), (4, "legacy")])
+def test_ll_zero_copy_combine_pulls_from_window(n, layout):
+    """EpConfig.expert_out_window (LL): expert outputs written into the
+    registered [L, N*B, H] bf16 region; each home pulls its tokens' rows."""
+    cfg = ep.EpConfig(ep.Algorithm.LL, n, n, 64, 8, 2048, 32, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16,
+                      expert_out_window=True)
+    wl = owl.make_workload(64, n, 32, 8, 2048, seed=60 + n)
+    wl.tokens = [bf16_round(t) for t in wl.tokens]
+    res = run_ll(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale, mode="bf16", wire_out=True,
+                 bf16_expert=True, layout=layout, zero_copy=True, rounds=3)
+    d, comb = _ll_oracle(cfg, wl, owl.expert_scale, bf16_expert=True)
+    for rnd in range(3):
+        _check_ll(cfg, [res[r][rnd] for r in range(n)], d, comb)
+
+
 def test_ll_legacy_window_is_the_reference_footprint():
     from oracle import layout as olay
     cfg = ep.EpConfig(ep.Algorithm.LL, 2, 2, 64, 8, 1024, 16, ep.Dtype.FP8, True)
@@ -288,9 +303,9 @@ def test_ht_dsv3_like_matches_oracle(n, rpn):
 
 @pytest.mark.parametrize("n,rpn", [(1, 1), (2, 2), (8, 8), (8, 2)])
 def test_ht_zero_copy_combine_pulls_from_window(n, rpn):
-    """EpConfig.ht_expert_out: expert rows written into the registered
+    """EpConfig.expert_out_window: expert rows written into the registered
     window region; the home ranks pull them (no push pass), bit-exact."""
-    cfg = ep.EpConfig(ep.Algorithm.HT, n, rpn, 64, 8, 2048, 256, ep.Dtype.BF16, ht_expert_out=True)
+    cfg = ep.EpConfig(ep.Algorithm.HT, n, rpn, 64, 8, 2048, 256, ep.Dtype.BF16, expert_out_window=True)
     wl = owl.make_workload(64, n, 256, 8, 2048, seed=17)
     res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_affine, zero_copy=True)
     dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, 64, n, 2048, "bf16")
