@@ -61,6 +61,8 @@ struct HTGeom {
 
 inline int experts_per_rank(int e, int n) { return (e + n - 1) / n; }
 
+constexpr int kLayChunk = 128;  // tokens per CTA of the multi-CTA routing layout (K1)
+
 inline void make_ll_geom(const epb_config& c, LLGeom& g) {
   g.N = c.num_ranks; g.E = c.num_experts; g.L = experts_per_rank(c.num_experts, c.num_ranks);
   g.K = c.top_k; g.H = c.hidden; g.B = c.max_tokens_per_rank; g.wire = c.token_dtype;

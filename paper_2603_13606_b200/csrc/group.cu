@@ -148,6 +148,7 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
     if (g->d_err) cudaFree(g->d_err);
     if (g->d_done) cudaFree(g->d_done);
     if (g->d_scratch) cudaFree(g->d_scratch);
+    if (g->d_lay) cudaFree(g->d_lay);
     delete g;
     return code;
   };
@@ -170,6 +171,9 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
   if (e == cudaSuccess) e = cudaMalloc(&g->d_err, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&g->d_done, sizeof(int) * 4 * n);
   if (e == cudaSuccess) e = cudaMalloc(&g->d_scratch, sizeof(int) * (8 * n + 2 * l * n + 64));
+  if (e == cudaSuccess)
+    e = cudaMalloc(&g->d_lay, sizeof(int) * (size_t)((cfg->max_tokens_per_rank + kLayChunk - 1) / kLayChunk) *
+                                  (cfg->num_experts + n));
   if (e == cudaSuccess) e = cudaMemsetAsync(g->window, 0, g->window_bytes, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->d_err, 0, sizeof(int) * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->d_done, 0, sizeof(int) * 4 * n, s);
@@ -286,6 +290,7 @@ int epb_group_destroy(epb_group* g) {
   cudaFree(g->d_err);
   cudaFree(g->d_done);
   cudaFree(g->d_scratch);
+  cudaFree(g->d_lay);
   delete g;
   return EPB_OK;
 }

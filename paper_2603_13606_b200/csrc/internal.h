@@ -21,6 +21,7 @@ struct epb_group {
   int* d_err = nullptr;         // device error word
   int* d_done = nullptr;        // [2*N] arrival counters (dispatch, combine)
   int* d_scratch = nullptr;     // [4*N + 2*L*N + 64] small per-call state
+  int* d_lay = nullptr;         // [ceil(B / kLayChunk)][E+N] per-chunk routing histograms (K1)
   epb::LLGeom ll;
   epb::HTGeom ht;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;

@@ -316,6 +316,25 @@ def test_ht_zero_copy_combine_pulls_from_window(n, rpn):
         np.testing.assert_array_equal(res[r]["out"], comb[r])
 
 
+@pytest.mark.parametrize("b", [1500, 4096])
+def test_ht_multi_cta_routing_layout(b):
+    """Batches above 512 tokens take the multi-CTA routing layout (per-chunk
+    histograms, column prefix, rebase): same receive order and rows."""
+    n = 2
+    cfg = make_cfg("ht", n, n, 32, b, 4, 256, "bf16")
+    wl = owl.make_workload(32, n, b, 4, 256, seed=21)
+    res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale)
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, 32, n, 256, "bf16")
+    ys = [oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_scale) for r in range(n)]
+    comb = oht.combine(ys, wl.routing, wl.weights, 32, n, n)
+    for r in range(n):
+        np.testing.assert_array_equal(res[r]["m"], m)
+        np.testing.assert_array_equal(res[r]["q"], q)
+        np.testing.assert_array_equal(res[r]["origin"], dd[r]["origin"])
+        np.testing.assert_array_equal(res[r]["rows"], dd[r]["rows"])
+        np.testing.assert_array_equal(res[r]["out"], comb[r])
+
+
 def test_ht_bf16_expert_rows_are_exact():
     cfg = make_cfg("ht", 4, 4, 32, 64, 4, 512, "bf16")
     wl = owl.make_workload(32, 4, 64, 4, 512, seed=9)
@@ -343,6 +362,24 @@ def test_bad_routing_rejected_at_create_handle(routing):
     cfg, fab, g = _solo()
     with pytest.raises(ep.EpError) as ei:
         g.create_handle(np.array(routing))
+    assert ei.value.code == ep.ErrorCode.INVALID_ARGUMENT
+    g.destroy()
+
+
+@pytest.mark.parametrize("bad", [-1, 99, "dup"])
+def test_bad_routing_rejected_by_multi_cta_layout(bad):
+    """HT create_handle with > 512 tokens (multi-CTA layout): an invalid
+    row anywhere raises InvalidArgument, no fault."""
+    cfg = make_cfg("ht", 1, 1, 16, 1000, 2, 16)
+    fab = ep.Fabric(ep.NodeTopology(1, 1))
+    g = ep.create_group(fab, 0, cfg)
+    r = np.tile(np.array([[0, 1]], np.int64), (1000, 1))
+    if bad == "dup":
+        r[777] = [5, 5]
+    else:
+        r[901, 1] = bad
+    with pytest.raises(ep.EpError) as ei:
+        g.create_handle(r)
     assert ei.value.code == ep.ErrorCode.INVALID_ARGUMENT
     g.destroy()
 
