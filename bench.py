@@ -512,8 +512,14 @@ def run_ht(args, world, rank):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     bufs = {}
 
+    t_handle = []
+
     def step(marks):
-        h = g.create_handle(topk)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        h = g.create_handle(topk)  # routing layout + metadata all-gather (ht.py open_round); host-synchronous
+        t_handle.append(time.perf_counter() - t0)
         tot = h.get_num_recv_tokens()
         if tot not in bufs:
             bufs[tot] = (torch.zeros((tot, H), dtype=torch.bfloat16, device=dev),
@@ -550,6 +556,7 @@ def run_ht(args, world, rank):
         tc.append(ev["epb_ht_combine"].elapsed_time(ev["combine:end"]))
     g.check()
     barrier(world)
+    t_h = allreduce_max(statistics.median(t_handle[-args.ht_steps:]), world)
     per_d = allgather_f(statistics.median(td), world)
     per_c = allgather_f(statistics.median(tc), world)
     ph_send = allgather_f(tphase.get("epb_ht_dispatch", 0.0) / args.ht_steps, world)
@@ -566,6 +573,9 @@ def run_ht(args, world, rank):
     return {
         "tokens_per_rank": b, "dtype": "bf16", "recv_rows": tot,
         "dispatch_us": round(t_d * 1e6, 1), "combine_us": round(t_c * 1e6, 1),
+        "create_handle_us": round(t_h * 1e6, 1),
+        "create_handle_timing": "host wall clock of EpGroup.create_handle (routing layout + metadata "
+                                "all-gather, receive count on the host on return; ht.py open_round)",
         "dispatch_payload_GBps": round(d_all / t_d / 1e9, 1),
         "combine_payload_GBps": round(c_all / t_c / 1e9, 1),
         "dispatch_nvlink_GBps": round(d_remote / t_d / 1e9, 1) if world > 1 else None,
