@@ -139,6 +139,10 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
   g->rank = rank;
   make_ll_geom(*cfg, g->ll);
   make_ht_geom(*cfg, g->ht);
+  {
+    const char* f = getenv("EPB_SYS_FENCE");
+    g->ll.sys_fence = g->ht.sys_fence = (f && atoi(f) != 0) ? 1 : 0;
+  }
   const uint64_t need = cfg->algorithm == EPB_LL ? g->ll.window_bytes : g->ht.window_bytes;
   cudaGetDevice(&g->device);
   cudaStream_t s = as_stream(stream);

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
   }
   __syncthreads();
   if ((int)threadIdx.x < g.N) {
-    fence_sys();
+    fence_release(p.g.sys_fence);
     uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, threadIdx.x) + g.meta_flag) +
                      p.parity * g.N + p.rank;
     st_relaxed_sys_u64(flag, (uint64_t)p.tag);
@@ -251,10 +251,10 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) 
   __syncthreads();
   if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
     const int d = threadIdx.x;
-    fence_sys();
+    fence_release(p.g.sys_fence);
     if (atomicAdd(&p.done[d], 1) == (int)gridDim.x - 1) {
       p.done[d] = 0;
-      fence_sys();
+      fence_release(p.g.sys_fence);
       ht_publish_records(p, d);
     }
   }
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
     // nothing moves: announce that this rank's expert rows are complete
     // (written by earlier kernels on this stream) to every home rank
     if (blockIdx.x == 0 && (int)threadIdx.x < N && (int)threadIdx.x != me) {
-      fence_sys();
+      fence_release(p.g.sys_fence);
       ht_publish_comb(p, threadIdx.x, 0);
     }
     return;
@@ -490,11 +490,11 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
     const int c = s_cnt[s];
     const int want = ht_rows_to(p, s);
     if (c > 0) {
-      fence_sys();
+      fence_release(p.g.sys_fence);
       const int old = atomicAdd(&p.done[s], c);
       if (old + c == want) {
         p.done[s] = 0;
-        fence_sys();
+        fence_release(p.g.sys_fence);
         ht_publish_comb(p, s, want);
       }
     } else if (blockIdx.x == 0 && want == 0) {

@@ -55,10 +55,7 @@ EPB_DEV uint32_t ld_round_u32(const uint32_t* p) {
 }
 EPB_DEV uint8_t* peer_base(const uint64_t* peers, int r) { return reinterpret_cast<uint8_t*>(peers[r]); }
 
-EPB_DEV void fence_scoped(bool sys) {
-  if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
-  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
+// (the release fence itself: fence_release in common.cuh)
 EPB_DEV void st_flag(uint64_t* p, uint64_t v, bool sys) {
   if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -610,7 +607,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     // (no flags to self: own rows went straight to the output and the fused
     // receive reads its own counts from shared memory)
     if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
-      fence_scoped(sys);
+      fence_release(g.sys_fence);
       uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.disp_flag) +
                        (int64_t)p.rank * G + blockIdx.x;
       st_flag(flag, (uint64_t)tag, sys);
@@ -847,7 +844,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     __syncthreads();
     LL_STAMP(p, 2);
     if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
-      fence_scoped(sys);
+      fence_release(g.sys_fence);
       uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.comb_flag) +
                        (int64_t)p.rank * G + blockIdx.x;
       st_flag(flag, (uint64_t)tag, sys);
@@ -857,7 +854,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // pulled combine: nothing moves; announce that this rank's expert
     // outputs (written by earlier kernels on this stream) are complete
     if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
-      fence_scoped(sys);
+      fence_release(g.sys_fence);
       uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.comb_flag) +
                        (int64_t)p.rank * G + blockIdx.x;
       st_flag(flag, (uint64_t)tag, sys);
