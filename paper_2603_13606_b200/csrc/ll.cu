@@ -696,22 +696,85 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       s_pre[N] = run;
     }
     __syncthreads();
-    const int items = s_pre[N] * K;
-    // items = (slot, k, half row); CTA-major order spreads them over every SM
-    for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * items; f2 += gridDim.x * nw) {
-      const int f = f2 >> 1, half = f2 & 1;
-      const int sl = f / K, k = f - sl * K;
+    // warp tasks (slot, half row): the header is read once, the row loaded
+    // once and stored to every local expert the slot names (the fan-out of
+    // ll.py:378-400); CTA-major order spreads the tasks over every SM
+    const int nslots = s_pre[N];
+    const bool fan = (H & 15) == 0;
+    constexpr int EPC = Elems<WT>::n;
+    for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * nslots; f2 += gridDim.x * nw) {
+      const int sl = f2 >> 1, half = f2 & 1;
       int s = 0;
       while (s_pre[s + 1] <= sl) ++s;
       const int j = sl - s_pre[s];
       const uint8_t* slot = p.win + parity_off + g.disp_slot + ((int64_t)s * B + j) * g.slot_stride;
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
-      const int e = (int)hdr[2 + k];
-      if (e < lo || e >= lo + nloc) continue;
-      const int64_t row = (int64_t)(e - lo) * N * B + (int64_t)s * B + hdr[2 + K + k];
-      if (lane == 0 && half == 0) p.src_info[row] = (int32_t)(hdr[0] * K + k);
-      ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + row * orow_bytes,
-                              SC ? p.out_scales + row * (H / 128) : nullptr, lane, half, 2);
+      int e = -1, ci = 0;
+      if (lane < K) {
+        e = (int)hdr[2 + lane];
+        ci = (int)hdr[2 + K + lane];
+      }
+      const bool loc = lane < K && e >= lo && e < lo + nloc;
+      const int my_orow = (e - lo) * N * B + s * B + ci;
+      const unsigned lm = __ballot_sync(0xffffffffu, loc);
+      if (half == 0 && loc) p.src_info[my_orow] = (int32_t)(hdr[0] * K + lane);
+      if (!fan) {
+        for (unsigned mm = lm; mm; mm &= mm - 1) {
+          const int64_t row = __shfl_sync(0xffffffffu, my_orow, __ffs(mm) - 1);
+          ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + row * orow_bytes,
+                                  SC ? p.out_scales + row * (H / 128) : nullptr, lane, half, 2);
+        }
+        continue;
+      }
+      const int nch = H / EPC;
+      const int per = (nch + 1) / 2;
+      const int c0 = half * per, c1 = min(nch, c0 + per);
+      for (int base = c0; base < c1; base += 32 * kUnroll) {
+        int4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int c = base + u * 32 + lane;
+          if (c < c1) v[u] = ld_weak_v4(slot + (int64_t)c * 16);
+        }
+        float sc_c[kUnroll];
+        if constexpr (SC && OT != WT) {
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int c = base + u * 32 + lane;
+            sc_c[u] = c < c1 ? reinterpret_cast<const float*>(slot + g.RBp)[(c * EPC) >> 7] : 0.0f;
+          }
+        }
+        for (unsigned mm = lm; mm; mm &= mm - 1) {
+          const int64_t row = __shfl_sync(0xffffffffu, my_orow, __ffs(mm) - 1);
+          uint8_t* o = reinterpret_cast<uint8_t*>(p.out) + row * orow_bytes;
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int c = base + u * 32 + lane;
+            if (c < c1) {
+              if constexpr (OT == WT) {
+                st_weak_v4(o + (int64_t)c * 16, v[u]);
+              } else {
+                float f[EPC];
+                unpack16<WT>(v[u], f);
+                if constexpr (SC) {
+#pragma unroll
+                  for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], sc_c[u]);
+                }
+                store_f32_chunk<EPB_F32, EPC>(o, (int64_t)c * EPC, f);
+              }
+            }
+          }
+        }
+      }
+      if constexpr (SC && OT == WT) {
+        if (half == 0) {
+          for (unsigned mm = lm; mm; mm &= mm - 1) {
+            const int64_t row = __shfl_sync(0xffffffffu, my_orow, __ffs(mm) - 1);
+            for (int i = lane; i < H / 128; i += 32)
+              p.out_scales[row * (H / 128) + i] = reinterpret_cast<const float*>(slot + g.RBp)[i];
+          }
+        }
+      }
     }
     LL_STAMP(p, 7);
   }
