@@ -211,9 +211,12 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) 
         store_elem(p.stage + (int64_t)t * g.RBp, WT, el, load_elem(xrow, XT, el));
     }
   }
-  // (2) records: lane k holds (e_k, w_k, pos_k); lane d < N (and d + 32)
-  // the token's slot at rank d
-  const int words = K + 2 + 2 * K;
+  // (2) records: lane k holds (e_k, w_k, pos_k), lane d < N (and d + 32)
+  // the token's slot at rank d.  The record image [K f32 weights | t, K,
+  // e[K], pos[K]] is the same for every destination: lane l builds its
+  // 16-B piece once, then one vector store per lane per destination.
+  const int nvec = g.rec_stride / 16;  // <= 25 (K <= 32)
+  const int wq = g.WBp / 4;            // header word offset
   const int64_t rec0 = (int64_t)me * g.B;
   for (int t = blockIdx.x * nw + warp; t < p.b; t += gridDim.x * nw) {
     int e = 0, pos = 0;
@@ -226,24 +229,29 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) 
     }
     const int slot_lo = lane < N ? p.tok_slot[(int64_t)t * N + lane] : -1;
     const int slot_hi = lane + 32 < N ? p.tok_slot[(int64_t)t * N + lane + 32] : -1;
+    uint32_t img[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int wi = 4 * lane + u;
+      const int h = wi - wq;
+      const int src = wi < wq ? wi : (h >= 2 && h < 2 + K ? h - 2 : (h >= 2 + K ? h - 2 - K : 0));
+      const float wv = __shfl_sync(0xffffffffu, wk, src & 31);
+      const int ev = __shfl_sync(0xffffffffu, e, src & 31);
+      const int pv = __shfl_sync(0xffffffffu, pos, src & 31);
+      uint32_t v = 0;
+      if (wi < wq) v = wi < K ? __float_as_uint(wv) : 0u;
+      else if (h == 0) v = (uint32_t)t;
+      else if (h == 1) v = (uint32_t)K;
+      else if (h < 2 + K) v = (uint32_t)ev;
+      else if (h < 2 + 2 * K) v = (uint32_t)pv;
+      img[u] = v;
+    }
+    const int4 piece = make_int4((int)img[0], (int)img[1], (int)img[2], (int)img[3]);
     for (int d = 0; d < N; ++d) {
       const int j = __shfl_sync(0xffffffffu, d < 32 ? slot_lo : slot_hi, d & 31);
       if (j < 0) continue;
       uint8_t* rec = hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride;
-      for (int w0 = 0; w0 < words; w0 += 32) {
-        const int wd = w0 + lane;
-        const int h = wd - K;
-        const int src = wd < K ? wd : (h >= 2 && h < 2 + K ? h - 2 : (h >= 2 + K ? h - 2 - K : 0));
-        const float wv = __shfl_sync(0xffffffffu, wk, src & 31);
-        const int ev = __shfl_sync(0xffffffffu, e, src & 31);
-        const int pv = __shfl_sync(0xffffffffu, pos, src & 31);
-        if (wd < K) {
-          reinterpret_cast<float*>(rec)[wd] = wv;
-        } else if (wd < words) {
-          const uint32_t v = h == 0 ? (uint32_t)t : h == 1 ? (uint32_t)K : h < 2 + K ? (uint32_t)ev : (uint32_t)pv;
-          reinterpret_cast<uint32_t*>(rec + g.WBp)[h] = v;
-        }
-      }
+      if (lane < nvec) st_plain_v4(rec + 16 * lane, piece);
     }
   }
   (void)L;
