@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
 }
 
 struct HTCombRecv {
+  int rows_local;            // every row is in this GPU's memory (push mode, or one rank)
   const int64_t* topk;
   const uint64_t* row_ptr;   // [b*K] from the send phase, or null
   const float* w;
@@ -526,6 +527,88 @@ struct HTCombRecv {
   int b, rank, y_dtype;
   uint32_t tag;
 };
+
+// Single-node bf16 reduce with the row loads in flight through cp.async
+// (shared memory, not registers): each warp keeps kCS tasks (token, 32
+// chunks of 8 elements; K <= 8 rows of 512 B) in flight, so an SM has
+// 16 warps x kCS x 4 KB of peer / local loads outstanding.  Each lane only
+// consumes the chunks it copied itself: wait_group, no warp barrier.
+// Order: acc = p_0, acc = fl(acc + p_k) ascending k, out = fl(0 + acc).
+constexpr int kCS = 3;  // pipeline depth (tasks per warp in flight)
+
+EPB_DEV void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+EPB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+EPB_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int OT>
+EPB_DEV void ht_combine_reduce_async(const HTCombRecv& p, int K, int H, int warp, int lane, int nw) {
+  extern __shared__ int4 s_stage[];  // [nw][kCS][8 rows][32 lanes]
+  constexpr int OW = OT == EPB_F32 ? 4 : 2;
+  int4* my = s_stage + (int64_t)warp * kCS * 8 * 32;
+  const int nch = H / 8;
+  const int segs = (nch + 31) / 32;
+  const int tasks = p.b * segs;
+  const int tstride = gridDim.x * nw;
+  const int first = warp * gridDim.x + blockIdx.x;
+  // per stage: lane k's weight, the task's token/chunk
+  float sw[kCS];
+  int st[kCS], sc[kCS];
+  auto issue = [&](int task, int stg) {
+    if (task < tasks) {
+      const int t = task / segs, c = (task - t * segs) * 32 + lane;
+      uint64_t row = 0;
+      float w = 0.0f;
+      if (lane < K) {
+        row = p.row_ptr[(int64_t)t * K + lane];
+        w = p.w[(int64_t)t * K + lane];
+      }
+      sw[stg] = w;
+      st[stg] = t;
+      sc[stg] = c;
+      for (int k = 0; k < K; ++k) {
+        const uint64_t rk = __shfl_sync(0xffffffffu, row, k);
+        if (c < nch) cp_async16(&my[(stg * 8 + k) * 32 + lane], reinterpret_cast<const uint8_t*>(rk) + (int64_t)c * 16);
+      }
+    }
+    cp_async_commit();  // (an empty group keeps the wait_group arithmetic uniform)
+  };
+#pragma unroll
+  for (int i = 0; i < kCS - 1; ++i) issue(first + i * tstride, i);
+  // stages rotate with the unrolled q, so every stage index is a constant
+  for (int task0 = first; task0 < tasks; task0 += kCS * tstride) {
+#pragma unroll
+    for (int q = 0; q < kCS; ++q) {
+      const int task = task0 + q * tstride;
+      issue(task + (kCS - 1) * tstride, (q + kCS - 1) % kCS);
+      cp_async_wait<kCS - 1>();  // this task's copies (this lane's) are in
+      if (task < tasks) {
+        const int t = st[q], c = sc[q];
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        for (int k = 0; k < K; ++k) {
+          const float wk = __shfl_sync(0xffffffffu, sw[q], k);
+          float y[8];
+          unpack16<EPB_BF16>(my[(q * 8 + k) * 32 + lane], y);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float pk = __fmul_rn(wk, y[i]);
+            acc[i] = k == 0 ? pk : __fadd_rn(acc[i], pk);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(0.0f, acc[i]);
+        if (c < nch)
+          store_f32_chunk<OT, 8>(reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * OW, (int64_t)c * 8, acc);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
 
 // 8 consecutive elements (chunk c) of a row in dtype IT, as f32
 template <int IT>
@@ -562,6 +645,14 @@ __global__ void __launch_bounds__(kHTThreads, 1) ht_combine_recv_kernel(HTCombRe
   const uint8_t* crow = p.win + g.crow;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const bool one_node = g.rpn == N;
+  if constexpr (IT == EPB_BF16) {
+    // (cp.async from peer memory measured ~2.4x slower than register loads:
+    // the async path only runs when every row is local)
+    if (one_node && p.rows_local && p.row_ptr && K <= 8 && (H & 7) == 0) {
+      ht_combine_reduce_async<OT>(p, K, H, warp, lane, nw);
+      return;
+    }
+  }
   if ((H & 7) == 0 && K <= 32) {
     // warp tasks: (token, 32-chunk segment of 8 elements); lane = one chunk.
     // Lane k first resolves row k of the token (own expert rows are read in
@@ -874,6 +965,7 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
     if (a->out_dtype != EPB_F32 && a->out_dtype != EPB_BF16) return fail(EPB_TAG_MISMATCH, "combine output f32|bf16");
     if (!a16(a->out)) return fail(EPB_INVALID_ARGUMENT, "out must be 16-byte aligned");
     HTCombRecv p;
+    p.rows_local = g->cfg.num_ranks == 1 || !a->expert_rows_in_window;
     p.topk = a->topk_idx; p.row_ptr = a->row_ptr; p.w = a->weights; p.y_local = a->expert_rows;
     p.tok_rank = a->tok_rank;
     p.offsets = a->offsets; p.out = a->out; p.win = g->window; p.err = g->d_err; p.g = g->ht;
@@ -884,8 +976,17 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
       if (a->out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_F32, EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
       else ht_combine_recv_kernel<EPB_F32, EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
     } else {
-      if (a->out_dtype == EPB_F32) ht_combine_recv_kernel<EPB_BF16, EPB_F32><<<grid, kHTThreads, 0, s>>>(p);
-      else ht_combine_recv_kernel<EPB_BF16, EPB_BF16><<<grid, kHTThreads, 0, s>>>(p);
+      // cp.async staging of the bf16 reduce: [warps][kCS][8][32] x 16 B
+      const int csm = (kHTThreads / 32) * kCS * 8 * 32 * 16;
+      if (a->out_dtype == EPB_F32) {
+        EPB_CUDA(cudaFuncSetAttribute(ht_combine_recv_kernel<EPB_BF16, EPB_F32>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, csm));
+        ht_combine_recv_kernel<EPB_BF16, EPB_F32><<<grid, kHTThreads, csm, s>>>(p);
+      } else {
+        EPB_CUDA(cudaFuncSetAttribute(ht_combine_recv_kernel<EPB_BF16, EPB_BF16>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, csm));
+        ht_combine_recv_kernel<EPB_BF16, EPB_BF16><<<grid, kHTThreads, csm, s>>>(p);
+      }
     }
     EPB_LAUNCH_CHECK();
   }
