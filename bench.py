@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--no-ht", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-extra", action="store_true", help="skip the C4/C5 configs (extra_configs key)")
     p.add_argument("--cpu-sample-steps", type=int, default=3)
     p.add_argument("--sweep", action="store_true", help="LL token sweep 1..128 (extra key)")
     return p.parse_args()
@@ -174,17 +175,19 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 class LLStep:
-    def __init__(self, world, rank, b, seed=0):
+    def __init__(self, world, rank, b, seed=0, shape=None, zipf=False):
         import torch
 
         import paper_2603_13606_b200 as ep
         from oracle import workload as owl
         self.ep, self.torch = ep, torch
         self.world, self.rank, self.b = world, rank, b
+        E, K, H = shape or (globals()["E"], globals()["K"], globals()["H"])
+        self.E, self.K, self.H = E, K, H
         self.cfg = ep.EpConfig(ep.Algorithm.LL, world, world, E, K, H, b, ep.Dtype.FP8, True,
                                combine_dtype=ep.Dtype.BF16)
         self.g = make_group(world, rank, self.cfg, strict=False)
-        wl = owl.make_workload(E, world, b, K, H, seed)
+        wl = (owl.make_zipf_workload if zipf else owl.make_workload)(E, world, b, K, H, seed)
         dev = torch.device("cuda", torch.cuda.current_device())
         L = self.cfg.experts_per_rank
         self.x = torch.from_numpy(wl.tokens[rank]).to(dev).to(torch.bfloat16)
@@ -221,6 +224,7 @@ class LLStep:
 
     # algorithmic bytes per kernel launch (this rank), headers not credited
     def algo_bytes(self):
+        E, K, H = self.E, self.K, self.H
         L = self.cfg.experts_per_rank
         owner = self.routing_h // L
         dst_per_tok = np.array([len(set(r)) for r in owner]) if self.b else np.zeros(0)
@@ -360,9 +364,9 @@ def steps_per_graph(steps):
     return max(d for d in range(1, min(steps, 10) + 1) if steps % d == 0)
 
 
-def run_ll(args, world, rank):
+def run_ll(args, world, rank, shape=None, zipf=False):
     import torch
-    st = LLStep(world, rank, args.tokens)
+    st = LLStep(world, rank, args.tokens, shape=shape, zipf=zipf)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     S = steps_per_graph(args.steps)
     graph, per_step = capture_steps(st, st.g, S, flush, phases=False)
@@ -487,17 +491,18 @@ def run_e2e(args, world, rank, st):
 # HT prefill (configs[2]) — eager, phase events
 # ---------------------------------------------------------------------------
 
-def run_ht(args, world, rank):
+def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
     import torch
 
     import paper_2603_13606_b200 as ep
     from oracle import workload as owl
     b = args.ht_tokens
+    E, K, H = shape or (globals()["E"], globals()["K"], globals()["H"])
     # expert outputs are written into the group's registered window region
     # (EpHandle.expert_out_buffer), so the combine is pulled, not pushed
     cfg = ep.EpConfig(ep.Algorithm.HT, world, world, E, K, H, b, ep.Dtype.BF16, expert_out_window=True)
     g = make_group(world, rank, cfg, strict=False)
-    wl = owl.make_workload(E, world, b, K, H, seed=7)
+    wl = (owl.make_zipf_workload if zipf else owl.make_workload)(E, world, b, K, H, seed)
     dev = torch.device("cuda", torch.cuda.current_device())
     x = torch.from_numpy(wl.tokens[rank]).to(dev).to(torch.bfloat16)
     topk = torch.from_numpy(wl.routing[rank]).to(dev)
@@ -677,6 +682,21 @@ def main():
         result["e2e"] = run_e2e(args, world, rank, st)
     if not args.no_ht:
         result["ht"] = run_ht(args, world, rank)
+    if not args.no_ht and not args.no_extra:
+        # the other BASELINE configs at this N (parity for them: tests/test_gpu_parity.py)
+        extra = {}
+        a2 = argparse.Namespace(**vars(args))
+        a2.ht_steps = 3
+        extra["C4 HT Mixtral E=8 K=2 H=4096, 4096 tok"] = run_ht(a2, world, rank, shape=(8, 2, 4096))
+        extra["C5 HT Qwen3 E=128 K=8 H=4096, 4096 tok, Zipf routing"] = run_ht(
+            a2, world, rank, shape=(128, 8, 4096), zipf=True)
+        a3 = argparse.Namespace(**vars(args))
+        a3.steps, a3.warmup = 50, 10
+        s3, ms3, _, _, _, _, k3 = run_ll(a3, world, rank, shape=(128, 8, 4096), zipf=True)
+        extra["C5 LL Qwen3 E=128 K=8 H=4096, 128 tok, Zipf routing, fp8 dispatch / bf16 combine"] = {
+            "step_us": round(ms3 * 1000, 2), "kernel_us": {k: round(v, 2) for k, v in k3.items()}}
+        s3.g.destroy()
+        result["extra_configs"] = extra
     if args.sweep:
         sweep = {}
         for bb in (1, 2, 4, 8, 16, 32, 64, 128):

@@ -335,6 +335,46 @@ def test_ht_multi_cta_routing_layout(b):
         np.testing.assert_array_equal(res[r]["out"], comb[r])
 
 
+# BASELINE configs[3] / [4] shapes: Mixtral (E=8, K=2, H=4096, one expert per
+# rank at N=8) and Qwen3-MoE (E=128, K=8, H=4096, Zipf routing)
+@pytest.mark.parametrize("n", [2, 8])
+def test_ht_mixtral_shape(n):
+    cfg = make_cfg("ht", n, n, 8, 256, 2, 4096, "bf16")
+    wl = owl.make_workload(8, n, 256, 2, 4096, seed=31)
+    res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_affine)
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, 8, n, 4096, "bf16")
+    ys = [oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_affine) for r in range(n)]
+    comb = oht.combine(ys, wl.routing, wl.weights, 8, n, n)
+    for r in range(n):
+        np.testing.assert_array_equal(res[r]["rows"], dd[r]["rows"])
+        np.testing.assert_array_equal(res[r]["out"], comb[r])
+
+
+def test_ht_qwen3_shape_zipf():
+    n = 2
+    cfg = make_cfg("ht", n, n, 128, 256, 8, 4096, "bf16")
+    wl = owl.make_zipf_workload(128, n, 256, 8, 4096, seed=32)
+    res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale)
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, 128, n, 4096, "bf16")
+    ys = [oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_scale) for r in range(n)]
+    comb = oht.combine(ys, wl.routing, wl.weights, 128, n, n)
+    for r in range(n):
+        np.testing.assert_array_equal(res[r]["m"], m)
+        np.testing.assert_array_equal(res[r]["rows"], dd[r]["rows"])
+        np.testing.assert_array_equal(res[r]["out"], comb[r])
+
+
+def test_ll_qwen3_shape_zipf_fp8_bf16():
+    n = 2
+    cfg = ep.EpConfig(ep.Algorithm.LL, n, n, 128, 8, 4096, 64, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
+    wl = owl.make_zipf_workload(128, n, 64, 8, 4096, seed=33)
+    wl.tokens = [bf16_round(t) for t in wl.tokens]
+    res = run_ll(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale, mode="bf16", wire_out=True,
+                 bf16_expert=True)
+    d, comb = _ll_oracle(cfg, wl, owl.expert_scale, bf16_expert=True)
+    _check_ll(cfg, res, d, comb)
+
+
 def test_ht_bf16_expert_rows_are_exact():
     cfg = make_cfg("ht", 4, 4, 32, 64, 4, 512, "bf16")
     wl = owl.make_workload(32, 4, 64, 4, 512, seed=9)
