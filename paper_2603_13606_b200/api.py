@@ -212,10 +212,17 @@ class EpGroup:
         return bool(cap) and isinstance(self._buffer, torch.Tensor) and t.dtype == torch.bfloat16 and \
             t.data_ptr() == self._buffer.data_ptr() + off
 
+    def _pinned_i32(self, n: int) -> torch.Tensor:
+        buf = getattr(self, "_pinned_buf", None)
+        if buf is None or buf.numel() < n:
+            buf = self._pinned_buf = torch.empty(max(n, 1024), dtype=torch.int32).pin_memory()
+        return buf[:n]
+
     def check(self) -> None:
         """Synchronise and raise any error the kernels recorded (timeouts,
         routing validation, weight mismatch)."""
         code = ctypes.c_int32(0)
+        self.stream.synchronize()  # the group's stream may be a non-blocking one
         _lib.call("epb_group_poll_error", self._g, 1, ctypes.byref(code))
         if code.value:
             raise_status(code.value, "device-side failure recorded by the EP kernels")
@@ -470,22 +477,27 @@ class EpHandle:
         n, e = cfg.num_ranks, cfg.num_experts
         dev = g.device
         self._round = rnd
-        meta = torch.empty((n, e + n), dtype=torch.int32, device=dev)
+        nm = n * (e + n)
+        mt = torch.empty(nm + 1, dtype=torch.int32, device=dev)  # meta rows | receive total
+        meta, total = mt[:nm].view(n, e + n), mt[nm:]
         offsets = torch.empty((e, n), dtype=torch.int32, device=dev)
-        total = torch.empty(1, dtype=torch.int32, device=dev)
         g._launch("epb_ht_meta_send", g._g, rnd, ctypes.byref(self._lay), self._sp())
         g.fabric.phase(g.rank)
         g._launch("epb_ht_meta_recv", g._g, rnd, _ptr(meta), _ptr(offsets), _ptr(total), self._sp())
-        g.check()  # synchronises: receive shapes are host-known on return (api.py:235-237)
-        meta_h = meta.cpu().numpy()
         ell = cfg.experts_per_rank
         lo = g.rank * ell
         hi = min(lo + ell, e)
-        counts = np.zeros((ell, n), dtype=np.float32)  # TOKENS_PER_EXPERTS (api.py:437-441)
+        counts_dev = torch.zeros((ell, n), dtype=torch.float32, device=dev)  # TOKENS_PER_EXPERTS
+        counts_dev[:hi - lo] = meta[:, lo:hi].t().float()
+        host = g._pinned_i32(nm + 1)
+        host.copy_(mt, non_blocking=True)
+        g.check()  # one synchronisation: receive shapes are host-known on return (api.py:235-237)
+        meta_h = host[:nm].numpy().reshape(n, e + n).copy()
+        counts = np.zeros((ell, n), dtype=np.float32)  # (api.py:437-441)
         counts[:hi - lo] = meta_h[:, lo:hi].T
         self._meta = dict(m=meta_h[:, :e].astype(np.int64), q=meta_h[:, e:].astype(np.int64),
-                          recv_total=int(total.item()), offsets=offsets,
-                          counts_host=counts, counts_dev=torch.from_numpy(counts).to(dev))
+                          recv_total=int(host[nm]), offsets=offsets,
+                          counts_host=counts, counts_dev=counts_dev)
         self._round_open = True
 
     # -- staging helpers ----------------------------------------------------------
