@@ -306,10 +306,16 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
   }
   __syncthreads();
   if (s_fail) return;
+  // remote records interleaved over the sources in chunks of kRC: chunk c
+  // reads source me+1+(c % (N-1)), its chunk c / (N-1), so every source's
+  // stage is read by all receivers at an even rate for the whole phase
+  constexpr int kRC = 32;
+  __shared__ int s_maxq;
   if (threadIdx.x == 0) {
-    int run = 0;
-    for (int i = 0; i < N - 1; ++i) { s_pre[i] = run; run += s_q[(me + 1 + i) % N]; }
-    s_pre[N - 1] = run;
+    int mx = 0;
+    for (int s2 = 0; s2 < N; ++s2)
+      if (s2 != me) mx = max(mx, s_q[s2]);
+    s_maxq = mx;
   }
   __syncthreads();
   const int lo = me * L, hi = min(lo + L, g.E);
@@ -317,7 +323,9 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
   // warps [0, sw) take this rank's own records, the rest the remote ones
   const int sw = N == 1 ? nw : max(1, nw / N);
   const bool self_warp = warp < sw;
-  const int items = self_warp ? 2 * s_q[me] : 2 * s_pre[N - 1];
+  const int nrs = max(1, N - 1);
+  const int rchunks = (s_maxq + kRC - 1) / kRC;
+  const int items = self_warp ? 2 * s_q[me] : 2 * rchunks * nrs * kRC;
   const int wi = self_warp ? warp : warp - sw;
   const int wn = self_warp ? sw : nw - sw;
   constexpr int OW = OT == EPB_F32 ? 4 : 2;
@@ -329,10 +337,10 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
       s = me;
       j = rj;
     } else {
-      int si = 0;
-      while (s_pre[si + 1] <= rj) ++si;
-      j = rj - s_pre[si];
-      s = (me + 1 + si) % N;
+      const int c = rj / kRC, w = rj - c * kRC;
+      s = (me + 1 + c % nrs) % N;
+      j = (c / nrs) * kRC + w;
+      if (j >= s_q[s]) continue;  // that source has fewer records
     }
     const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.WBp);
