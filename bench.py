@@ -214,6 +214,13 @@ class LLStep:
         """One LL step; `upto` truncates it ("dispatch", "handle") for the
         marginal per-kernel timing in run_ll."""
         h = self.g.create_handle(self.topk)
+        if upto == "staged":  # send / complete split (api.py:445-451, :521-540)
+            h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT], send_only=True)
+            h.complete()
+            h.combine([self.Y, self.W], [self.OUT], send_only=True)
+            h.complete()
+            h.destroy()
+            return
         if upto != "handle":
             h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT])
         if upto == "combine":
@@ -344,8 +351,9 @@ def capture_steps(step_obj, group, nsteps, flush, phases, upto="combine"):
     return graph, per_step
 
 
-def replay_steps(graph, per_step, replays):
-    """Replay; returns (sum of step times ms, {phase: summed ms}, steps)."""
+def replay_steps(graph, per_step, replays, samples=None):
+    """Replay; returns (sum of step times ms, {phase: summed ms}, steps);
+    `samples` (a list) collects every step's time."""
     import torch
     total, phase, n = 0.0, {}, 0
     for _ in range(replays):
@@ -353,7 +361,10 @@ def replay_steps(graph, per_step, replays):
         torch.cuda.synchronize()
         for marks in per_step:
             evs = [m[1] for m in marks]
-            total += evs[0].elapsed_time(evs[-1])
+            dt = evs[0].elapsed_time(evs[-1])
+            total += dt
+            if samples is not None:
+                samples.append(dt)
             for i in range(len(marks) - 1):
                 phase[marks[i][0]] = phase.get(marks[i][0], 0.0) + evs[i].elapsed_time(evs[i + 1])
             n += 1
@@ -377,9 +388,13 @@ def run_ll(args, world, rank, shape=None, zipf=False):
     barrier(world)
     with ClockSampler(torch.cuda.current_device()) as clk:
         barrier(world)
-        total, _, n = replay_steps(graph, per_step, args.steps // S)
+        samples = []
+        total, _, n = replay_steps(graph, per_step, args.steps // S, samples)
         barrier(world)
     assert n == args.steps
+    srt = sorted(samples)
+    pct = {"median_us": allreduce_max(srt[len(srt) // 2], world) * 1000.0,
+           "p99_us": allreduce_max(srt[min(len(srt) - 1, int(0.99 * len(srt)))], world) * 1000.0}
     # per-kernel breakdown from the instrumented graph (events between launches)
     barrier(world)
     nb = max(10, min(args.steps, 100))
@@ -395,6 +410,16 @@ def run_ll(args, world, rank, shape=None, zipf=False):
         marg[upto] = allreduce_max(t2 / n2, world) * 1000.0
         del g2
     marg["combine"] = allreduce_max(total / n, world) * 1000.0
+    # staged (send_only + complete) steps: step time and the per-launch split
+    gs, pss = capture_steps(st, st.g, S, flush, phases=True, upto="staged")
+    gs.replay()
+    barrier(world)
+    ts, phs, ns = replay_steps(gs, pss, -(-nb // S))
+    st.staged = {"step_us_with_event_nodes": round(allreduce_max(ts / ns, world) * 1000.0, 2),
+                 "launch_us": {k: round(v / ns * 1000.0, 2) for k, v in phs.items()},
+                 "note": "dispatch(send_only) -> complete() -> combine(send_only) -> complete(); an event node "
+                         "before every launch (send phase, then receive phase of each op)"}
+    del gs
     # the same step as its own graph launch per step (graph launch included)
     graph1, marks1 = capture(st, st.g, phases=False)
     for _ in range(3):
@@ -410,6 +435,7 @@ def run_ll(args, world, rank, shape=None, zipf=False):
     launches = sum(1 for n_, _ in per_step_b[0] if n_.startswith("epb_"))
     kernel_us = {"epb_ll_dispatch": marg["dispatch"] - marg["handle"],
                  "epb_ll_combine": marg["combine"] - marg["dispatch"]}
+    st.pct = pct
     return (st, total_max / args.steps, per_phase, launches * args.steps, clk.report(),
             t1_max / args.steps * 1000.0, kernel_us)
 
@@ -666,6 +692,8 @@ def main():
                    "graph": (f"{steps_per_graph(args.steps)} steps per CUDA graph (create_handle+dispatch+combine "
                              "each, bracketed by in-graph events; flush + barrier between, untimed)")},
         "step_us_own_graph_launch": round(own_graph_us, 2),
+        "ll_staged": st.staged,
+        "step_us_median": round(st.pct["median_us"], 2), "step_us_p99": round(st.pct["p99_us"], 2),
         "kernel_us": {k: round(v, 2) for k, v in kernel_us.items()},
         "phase_us_event_nodes": {k: round(v, 2) for k, v in phases.items()},
         "gpu_launches": launches,

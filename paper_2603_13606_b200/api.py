@@ -626,7 +626,7 @@ class EpHandle:
             else:
                 g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_dispatch:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
             self._ll_recv()
 
     def _ll_recv(self) -> None:
@@ -736,7 +736,7 @@ class EpHandle:
             else:
                 g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_combine:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
             self._ll_combine_recv()
 
     def _ll_combine_recv(self) -> None:
@@ -806,14 +806,14 @@ class EpHandle:
         if self.state is HandleState.DISPATCH_STAGED:
             with torch.cuda.stream(g.stream):
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
+                g._launch("epb_ll_dispatch:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
                           ctypes.byref(self._ll_args), self._sp())
                 self._ll_recv()
             return
         if self.state is HandleState.COMBINE_STAGED:
             with torch.cuda.stream(g.stream):
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
+                g._launch("epb_ll_combine:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
                           ctypes.byref(self._ll_cargs), self._sp())
                 self._ll_combine_recv()
             return
