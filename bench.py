@@ -545,7 +545,7 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
 
     t_handle = []
 
-    def step(marks):
+    def step(marks, zero_copy=True):
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
@@ -563,7 +563,7 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         g.trace_phases(marks)
         h.dispatch([X, Wt], [ep.tensor_from_torch(rt, T.TOKENS), CNT])
         g.mark("dispatch:end")
-        h.combine([ep.tensor_from_torch(yw, T.TOKENS), Wt], [OUT])
+        h.combine([ep.tensor_from_torch(yw if zero_copy else yt, T.TOKENS), Wt], [OUT])
         g.mark("combine:end")
         g.trace_phases(None)
         h.destroy()
@@ -585,6 +585,18 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
             tphase[names[i]] = tphase.get(names[i], 0.0) + marks[i][1].elapsed_time(marks[i + 1][1])
         td.append(ev["epb_ht_dispatch"].elapsed_time(ev["dispatch:end"]))
         tc.append(ev["epb_ht_combine"].elapsed_time(ev["combine:end"]))
+    # the same combine with the expert rows in an ordinary tensor (pushed
+    # into the homes' slots, then reduced there)
+    tpush = []
+    for _ in range(2):
+        marks = []
+        step(marks, zero_copy=False)
+        torch.cuda.synchronize()
+        ev = {}
+        for n_, e_ in marks:
+            ev.setdefault(n_, e_)
+        tpush.append(ev["epb_ht_combine"].elapsed_time(ev["combine:end"]))
+    t_push = allreduce_max(min(tpush), world) / 1e3
     g.check()
     barrier(world)
     t_h = allreduce_max(statistics.median(t_handle[-args.ht_steps:]), world)
@@ -605,6 +617,8 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         "tokens_per_rank": b, "dtype": "bf16", "recv_rows": tot,
         "dispatch_us": round(t_d * 1e6, 1), "combine_us": round(t_c * 1e6, 1),
         "create_handle_us": round(t_h * 1e6, 1),
+        "combine_push_us": round(t_push * 1e6, 1),
+        "combine_push_note": "combine input in an ordinary tensor: rows pushed to the homes' slots, then reduced",
         "create_handle_timing": "host wall clock of EpGroup.create_handle (routing layout + metadata "
                                 "all-gather, receive count on the host on return; ht.py open_round)",
         "dispatch_payload_GBps": round(d_all / t_d / 1e9, 1),
