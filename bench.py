@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-extra", action="store_true", help="skip the C4/C5 configs (extra_configs key)")
     p.add_argument("--cpu-sample-steps", type=int, default=3)
-    p.add_argument("--sweep", action="store_true", help="LL token sweep 1..128 (extra key)")
+    p.add_argument("--no-sweep", action="store_true", help="skip the LL token sweep 1..128 (ll_sweep_us key)")
     return p.parse_args()
 
 
@@ -375,13 +375,15 @@ def steps_per_graph(steps):
     return max(d for d in range(1, min(steps, 10) + 1) if steps % d == 0)
 
 
-def run_ll(args, world, rank, shape=None, zipf=False):
+def run_ll(args, world, rank, shape=None, zipf=False, light=False):
+    """`light`: only the timed step graph (returns step ms; the sweep)."""
     import torch
     st = LLStep(world, rank, args.tokens, shape=shape, zipf=zipf)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     S = steps_per_graph(args.steps)
     graph, per_step = capture_steps(st, st.g, S, flush, phases=False)
-    graph_b, per_step_b = capture_steps(st, st.g, S, flush, phases=True)
+    if not light:
+        graph_b, per_step_b = capture_steps(st, st.g, S, flush, phases=True)
     for _ in range(max(1, -(-args.warmup // S))):
         graph.replay()
     torch.cuda.synchronize()
@@ -395,6 +397,9 @@ def run_ll(args, world, rank, shape=None, zipf=False):
     srt = sorted(samples)
     pct = {"median_us": allreduce_max(srt[len(srt) // 2], world) * 1000.0,
            "p99_us": allreduce_max(srt[min(len(srt) - 1, int(0.99 * len(srt)))], world) * 1000.0}
+    if light:
+        st.pct = pct
+        return st, allreduce_max(total, world) / args.steps
     # per-kernel breakdown from the instrumented graph (events between launches)
     barrier(world)
     nb = max(10, min(args.steps, 100))
@@ -739,12 +744,13 @@ def main():
             "step_us": round(ms3 * 1000, 2), "kernel_us": {k: round(v, 2) for k, v in k3.items()}}
         s3.g.destroy()
         result["extra_configs"] = extra
-    if args.sweep:
+    if not args.no_sweep:
+        # configs[1]'s 1-128 tokens/rank sweep (step time only)
         sweep = {}
         for bb in (1, 2, 4, 8, 16, 32, 64, 128):
             a2 = argparse.Namespace(**vars(args))
-            a2.tokens, a2.steps, a2.warmup = bb, max(20, args.steps // 4), 5
-            s2, ms2, _, _, _, _, _ = run_ll(a2, world, rank)
+            a2.tokens, a2.steps, a2.warmup = bb, 20, 10
+            s2, ms2 = run_ll(a2, world, rank, light=True)
             sweep[bb] = round(ms2 * 1000, 2)
             s2.g.destroy()
         result["ll_sweep_us"] = sweep
