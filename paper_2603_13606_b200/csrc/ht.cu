@@ -399,6 +399,149 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
 }
 
 // ---------------------------------------------------------------------------
+// Dispatch receive through the bulk-copy (TMA) engine: per warp, record
+// half-rows are pulled with cp.async.bulk global->shared (completion on an
+// mbarrier) into a 2-stage ring and written to every local expert's row with
+// cp.async.bulk shared->global — no registers hold payload, so an SM keeps
+// 2 x 8 half-rows (~112 KB at H=7168 bf16) in flight.  Same items and
+// outputs as ht_dispatch_recv_kernel (wire-dtype output only).
+// ---------------------------------------------------------------------------
+constexpr int kBulkWarps = 8;
+
+EPB_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+EPB_DEV void mbar_init(uint64_t* m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+EPB_DEV void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+EPB_DEV bool mbar_try_wait(uint64_t* m, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(m)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+EPB_DEV void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+EPB_DEV void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+}
+EPB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+EPB_DEV void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+EPB_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(HTRecv p) {
+  extern __shared__ __align__(128) uint8_t s_buf[];  // [warps][2][hb] then [warps][2] mbarriers
+  __shared__ int s_q[kMaxRanks];
+  __shared__ int s_fail, s_maxq;
+  const HTGeom& g = p.g;
+  const int N = g.N, K = g.K, L = g.L;
+  const int me = p.rank;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const uint32_t hb = (uint32_t)g.RBp / 2;
+  uint8_t* buf = s_buf + (size_t)warp * 2 * hb;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_buf + (size_t)nw * 2 * hb) + warp * 2;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
+  for (int s = threadIdx.x; s < N; s += blockDim.x) {
+    uint64_t v = 0;
+    if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    s_q[s] = s == me ? p.q[me] : (int)(v & 0xFFFFFFFFu);
+  }
+  __syncthreads();
+  if (s_fail) return;
+  // the staged rows were acquired through generic loads; the bulk copies
+  // read them through the async proxy
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (threadIdx.x == 0) {
+    int mx = 0;
+    for (int s = 0; s < N; ++s) mx = max(mx, s_q[s]);
+    s_maxq = mx;
+  }
+  __syncthreads();
+  // items: (chunk of kRC records, round-robin over the sources me+1, ...,
+  // me+N-1, me) x half rows
+  constexpr int kRC = 32;
+  const int rchunks = (s_maxq + kRC - 1) / kRC;
+  const int items = 2 * rchunks * N * kRC;
+  const int lo = me * L, hi = min(lo + L, g.E);
+  auto resolve = [&](int f2, int& s, int& j) {
+    const int rj = f2 >> 1, c = rj / kRC, w = rj - c * kRC;
+    s = (me + 1 + c % N) % N;
+    j = (c / N) * kRC + w;
+    return j < s_q[s];
+  };
+  auto next_item = [&](int f2) {
+    int s, j;
+    for (; f2 < items; f2 += gridDim.x * nw)
+      if (resolve(f2, s, j)) return f2;
+    return items;
+  };
+  uint32_t phase[2] = {0u, 0u};
+  int cur = next_item(warp * gridDim.x + blockIdx.x);
+  auto issue = [&](int f2, int stg) {
+    int s, j;
+    resolve(f2, s, j);
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride + g.WBp);
+    if (lane == 0) {
+      const uint8_t* row = hpeer(p.peers, s) + g.stage + (int64_t)hdr[0] * g.RBp + (f2 & 1) * hb;
+      mbar_expect_tx(&bar[stg], hb);
+      bulk_load(buf + stg * hb, row, hb, &bar[stg]);
+    }
+  };
+  if (cur < items) issue(cur, 0);
+  for (int q = 0; cur < items; ++q) {
+    const int stg = q & 1;
+    const int nxt = next_item(cur + gridDim.x * nw);
+    // the other buffer's stores (task q-1) must have read it before reuse
+    bulk_wait_read_all();
+    __syncwarp();
+    if (nxt < items) issue(nxt, stg ^ 1);
+    int s, j;
+    resolve(cur, s, j);
+    const int half = cur & 1;
+    const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.WBp);
+    int e = -1, pos = 0;
+    if (lane < K) {
+      e = (int)hdr[2 + lane];
+      pos = (int)hdr[2 + K + lane];
+    }
+    const bool loc = lane < K && e >= lo && e < hi;
+    if (half == 0 && loc) {
+      p.origin[(int64_t)pos * 4 + 0] = e;
+      p.origin[(int64_t)pos * 4 + 1] = s;
+      p.origin[(int64_t)pos * 4 + 2] = (int32_t)hdr[0];
+      p.origin[(int64_t)pos * 4 + 3] = lane;
+      p.origin_w[pos] = reinterpret_cast<const float*>(rec)[lane];
+    }
+    while (!mbar_try_wait(&bar[stg], phase[stg])) {
+    }
+    phase[stg] ^= 1u;
+    if (loc) {
+      bulk_store(reinterpret_cast<uint8_t*>(p.out) + (int64_t)pos * g.RBp + half * hb, buf + stg * hb, hb);
+      bulk_commit();
+    }
+    cur = nxt;
+  }
+  bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // K6: combine
 // ---------------------------------------------------------------------------
 struct HTCombSend {
@@ -858,6 +1001,17 @@ cudaError_t launch_hsend_x(const HTSend& p, int out_dtype, cudaStream_t s) {
 
 template <int WT, int OT>
 cudaError_t launch_hrecv(const HTRecv& p, cudaStream_t s) {
+  // wire-dtype output, half rows of 16-B multiples: the bulk-copy receive
+  static const int bulk = [] { const char* v = getenv("EPB_HT_BULK"); return v ? atoi(v) : 1; }();
+  const size_t hb = (size_t)p.g.RBp / 2;
+  const size_t bsm = (size_t)kBulkWarps * 2 * hb + (size_t)kBulkWarps * 2 * 8;
+  if (bulk && OT == WT && p.g.RB == p.g.RBp && (p.g.RBp % 32) == 0 && bsm <= 200 * 1024 && p.g.K <= 32) {
+    cudaError_t e = cudaFuncSetAttribute(ht_dispatch_recv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bsm);
+    if (e != cudaSuccess) return e;
+    ht_dispatch_recv_bulk_kernel<<<hsm_count(), kBulkWarps * 32, bsm, s>>>(p);
+    return cudaGetLastError();
+  }
   ht_dispatch_recv_kernel<WT, OT><<<2 * hsm_count(), kHTThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
