@@ -522,6 +522,9 @@ def run_e2e(args, world, rank, st):
 # HT prefill (configs[2]) — eager, phase events
 # ---------------------------------------------------------------------------
 
+HT_A2A_PULL_GBPS = 650.0  # measured all-to-all NVLink pull, remote bytes per GPU
+
+
 def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
     import torch
 
@@ -630,6 +633,10 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         "combine_payload_GBps": round(c_all / t_c / 1e9, 1),
         "dispatch_nvlink_GBps": round(d_remote / t_d / 1e9, 1) if world > 1 else None,
         "combine_nvlink_GBps": round(c_remote / t_c / 1e9, 1) if world > 1 else None,
+        # every GPU pulling from every peer at once (tools/a2a_micro.cu, N=2/4)
+        "nvlink_a2a_pull_bound_GBps": HT_A2A_PULL_GBPS if world > 1 else None,
+        "dispatch_frac_of_a2a": round(d_remote / t_d / 1e9 / HT_A2A_PULL_GBPS, 3) if world > 1 else None,
+        "combine_frac_of_a2a": round(c_remote / t_c / 1e9 / HT_A2A_PULL_GBPS, 3) if world > 1 else None,
         "phase_us": {k: round(v / args.ht_steps * 1e3, 1) for k, v in tphase.items()},
         "per_rank_us": {"dispatch": [round(v * 1e3, 1) for v in per_d], "combine": [round(v * 1e3, 1) for v in per_c],
                         "dispatch_send": [round(v * 1e3, 1) for v in ph_send],
