@@ -1009,7 +1009,7 @@ cudaError_t launch_hrecv(const HTRecv& p, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(ht_dispatch_recv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bsm);
     if (e != cudaSuccess) return e;
-    ht_dispatch_recv_bulk_kernel<<<hsm_count(), kBulkWarps * 32, bsm, s>>>(p);
+    ht_dispatch_recv_bulk_kernel<<<bulk * hsm_count(), kBulkWarps * 32, bsm, s>>>(p);
     return cudaGetLastError();
   }
   ht_dispatch_recv_kernel<WT, OT><<<2 * hsm_count(), kHTThreads, 0, s>>>(p);
