@@ -530,3 +530,51 @@ def test_host_buffers_round_trip():
     np.testing.assert_array_equal(comb_ref, _ll_oracle(cfg, wl, owl.expert_identity)[1][0])
     h.destroy()
     g.destroy()
+
+
+@pytest.mark.parametrize("strict,mapped_in", [(True, False), (False, False), (True, True), (False, True)])
+def test_ll_pinned_host_tokens_and_output_are_mapped(strict, mapped_in, monkeypatch):
+    """C2 path with pinned host tokens and a pinned host combine output: the
+    combine kernel writes the output in place over PCIe (api._HOST_MAPPED);
+    with `mapped_in` the dispatch kernel also reads the tokens in place.
+    Outputs are bit-identical to the all-device call."""
+    from paper_2603_13606_b200 import api as _api
+    monkeypatch.setattr(_api, "_HOST_MAPPED", True)
+    monkeypatch.setattr(_api, "_HOST_MAPPED_IN", mapped_in)
+    E, K, H, b = 256, 8, 7168, 128
+    cfg = ep.EpConfig(ep.Algorithm.LL, 1, 1, E, K, H, b, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
+    g = ep.create_group(ep.Fabric(ep.NodeTopology(1, 1)), 0, cfg, strict=strict)
+    wl = owl.make_workload(E, 1, b, K, H, seed=31)
+    dev = torch.device("cuda", 0)
+    T = ep.TensorTag
+    x_d = torch.from_numpy(wl.tokens[0]).to(dev).to(torch.bfloat16)
+    w_d = torch.from_numpy(wl.weights[0]).to(dev)
+    topk = torch.from_numpy(wl.routing[0]).to(dev)
+    y = torch.randn((E, b, H), device=dev).to(torch.bfloat16)
+    outs = {}
+    for where in ("device", "host"):
+        x = x_d if where == "device" else x_d.cpu().pin_memory()
+        out = torch.zeros((b, H), dtype=torch.bfloat16, device=dev)
+        if where == "host":
+            out = out.cpu().pin_memory()
+        recv = torch.zeros((E, b, H), dtype=torch.uint8, device=dev)
+        sc = torch.zeros((E, b, H // 128), dtype=torch.float32, device=dev)
+        cnt = torch.zeros((E, 1), dtype=torch.float32, device=dev)
+        h = g.create_handle(topk)
+        h.dispatch([ep.tensor_from_torch(x, T.TOKENS)],
+                   [ep.tensor_from_torch(recv, T.TOKENS), ep.tensor_from_torch(sc, T.SCALES),
+                    ep.tensor_from_torch(cnt, T.RECV_EXPERT_COUNTER_DEVICE)])
+        h.combine([ep.tensor_from_torch(y, T.TOKENS), ep.tensor_from_torch(w_d, T.TOPK_WEIGHTS)],
+                  [ep.tensor_from_torch(out, T.TOKENS)])
+        torch.cuda.synchronize()
+        g.check()
+        h.destroy()
+        valid = cnt.cpu().numpy().astype(np.int64)[:, 0]
+        rows = [recv[e, :valid[e]].cpu() for e in range(E)]
+        scs = [sc[e, :valid[e]].cpu() for e in range(E)]
+        outs[where] = (rows, scs, out.cpu())
+    g.destroy()
+    for a, c in zip(outs["device"][0] + outs["device"][1], outs["host"][0] + outs["host"][1]):
+        assert torch.equal(a, c)
+    assert torch.equal(outs["device"][2], outs["host"][2])
+    assert outs["host"][2].abs().sum() > 0
