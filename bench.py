@@ -21,7 +21,8 @@ Extra keys: `ht` (configs[2]: 4096 tokens/rank HT dispatch/combine, GB/s),
 
 `--impl reference` times the reference algorithm's CPU restatement
 (oracle/, the only executable form of the Python reference on the GPU box)
-on the same config and prints the same line with "impl": "reference".
+on the same config and prints the same line with "impl": "reference",
+using every usable host core (concurrent oracle rounds in forked processes).
 """
 
 from __future__ import annotations
