@@ -18,6 +18,7 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_13606_b200 as ep  # noqa: E402
+from paper_2603_13606_b200 import api as _api  # noqa: E402
 from oracle import codecs as oc  # noqa: E402
 from oracle import ht as oht  # noqa: E402
 from oracle import ll as oll  # noqa: E402
@@ -31,7 +32,7 @@ def bf16r(x):
 
 
 def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, staged, mode, rounds=1,
-            layout="optimized", zero_copy=False):
+            layout="optimized", zero_copy=False, host_io=False):
     cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, bmax, dtype, scales, combine_dtype=combine_dtype,
                       expert_out_window=zero_copy)
     fab = ep.ProcessFabric(ep.NodeTopology(world, world))
@@ -46,7 +47,11 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
               for r in range(world)]
         want = oll.combine(ys, wl.routing, wl.weights, e, world, bmax, h, cfg.combine_wire.value)[rank]
         hd = g.create_handle(wl.routing[rank])
-        if mode == "bf16":
+        if mode == "bf16" and host_io:  # pinned host tokens: staged H2D (even rounds), read in place (odd)
+            _api._HOST_MAPPED_IN = rnd % 2 == 1
+            xh = torch.from_numpy(wl.tokens[rank]).to(torch.bfloat16).pin_memory()
+            inputs = [ep.tensor_from_torch(xh, T.TOKENS)]
+        elif mode == "bf16":
             inputs = [ep.tensor_from_f32(wl.tokens[rank], ep.Dtype.BF16, T.TOKENS)]
         elif scales:
             c, s = oc.quantize_block(wl.tokens[rank])
@@ -62,6 +67,8 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
         hd.dispatch(inputs, [out, cnt], send_only=staged)
         if staged:
             hd.complete()
+        if host_io:
+            _api._HOST_MAPPED_IN = False
         counts = cnt.read_f32()
         np.testing.assert_array_equal(counts, d[rank]["counts"])
         recv = out.read_f32()
@@ -77,7 +84,10 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
         else:
             yin = ep.tensor_from_f32(y, ep.Dtype.BF16, T.TOKENS)
         comb_in = [yin, ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)]
-        comb_out = ep.tensor_create((bmax, h), ep.Dtype.F32, T.TOKENS)
+        if host_io:  # pinned host output: written by the combine kernel in place over PCIe
+            comb_out = ep.tensor_from_torch(torch.zeros((bmax, h), dtype=torch.float32).pin_memory(), T.TOKENS)
+        else:
+            comb_out = ep.tensor_create((bmax, h), ep.Dtype.F32, T.TOKENS)
         hd.combine(comb_in, [comb_out], send_only=staged)
         if staged:
             hd.complete()
@@ -202,6 +212,11 @@ def main():
                                                           ep.Dtype.BF16, 6, False, "bf16", rounds=2, layout="legacy")),
         ("ll legacy layout staged uneven", lambda: ll_case(world, rank, 3 * world + 1, 3, 256, 12, ep.Dtype.BF16, False,
                                                             None, 7, True, "ref", rounds=3, layout="legacy")),
+        ("ll c2 pinned host tokens + in-place host output", lambda: ll_case(
+            world, rank, 256, 8, 7168, 128, ep.Dtype.FP8, True, ep.Dtype.BF16, 11, False, "bf16", rounds=2,
+            host_io=True)),
+        ("ll staged, pinned host output", lambda: ll_case(world, rank, 256, 8, 7168, 32, ep.Dtype.FP8, True,
+                                                           ep.Dtype.BF16, 12, True, "bf16", rounds=2, host_io=True)),
         ("buffer wrapper ll c2 path", lambda: buffer_ll(world, rank)),
         ("ht bf16 single node", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 4, False)),
         ("ht zero-copy combine (pull)", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 8, True, zero_copy=True)),
