@@ -222,12 +222,9 @@ class LLStep:
             h.complete()
             h.destroy()
             return
-        if upto != "handle":
+        if upto != "handle":  # (every dispatch is combined: the arrival protocol counts rounds)
             h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT])
-        if upto == "combine":
             h.combine([self.Y, self.W], [self.OUT])
-        elif upto == "dispatch":
-            h.state = self.ep.HandleState.COMBINED  # timing only: this round's combine is skipped
         h.destroy()
 
     # algorithmic bytes per kernel launch (this rank), headers not credited
@@ -405,17 +402,8 @@ def run_ll(args, world, rank, shape=None, zipf=False, light=False):
     barrier(world)
     nb = max(10, min(args.steps, 100))
     _, phase, nph = replay_steps(graph_b, per_step_b, -(-nb // S))
-    # per-kernel device time as the marginal cost inside the graph: step
-    # truncated after dispatch / after create_handle, same bracketing events
-    marg = {}
-    for upto in ("dispatch", "handle"):
-        g2, ps2 = capture_steps(st, st.g, S, flush, phases=False, upto=upto)
-        g2.replay()
-        barrier(world)
-        t2, _, n2 = replay_steps(g2, ps2, -(-nb // S))
-        marg[upto] = allreduce_max(t2 / n2, world) * 1000.0
-        del g2
-    marg["combine"] = allreduce_max(total / n, world) * 1000.0
+    # per-kernel device time: the instrumented graph's event node before each
+    # launch (the nodes themselves add a little to each interval)
     # staged (send_only + complete) steps: step time and the per-launch split
     gs, pss = capture_steps(st, st.g, S, flush, phases=True, upto="staged")
     gs.replay()
@@ -439,8 +427,8 @@ def run_ll(args, world, rank, shape=None, zipf=False, light=False):
     t1_max = allreduce_max(t1, world)
     per_phase = {k: v / nph * 1000.0 for k, v in phase.items()}  # us
     launches = sum(1 for n_, _ in per_step_b[0] if n_.startswith("epb_"))
-    kernel_us = {"epb_ll_dispatch": marg["dispatch"] - marg["handle"],
-                 "epb_ll_combine": marg["combine"] - marg["dispatch"]}
+    kernel_us = {"epb_ll_dispatch": per_phase.get("epb_ll_dispatch", 0.0),
+                 "epb_ll_combine": per_phase.get("epb_ll_combine", 0.0)}
     st.pct = pct
     return (st, total_max / args.steps, per_phase, launches * args.steps, clk.report(),
             t1_max / args.steps * 1000.0, kernel_us)
@@ -747,8 +735,8 @@ def main():
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "algorithmic_bytes": int(algo[dom]), "traffic": traffic,
-                     "duration": "kernel_us: marginal in-graph event time of the launch (step truncated "
-                                 "before it vs after it, same bracketing events)",
+                     "duration": "kernel_us: in-graph event nodes before each launch (CUDA events on the "
+                                 "launching stream)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
         "nvlink_bytes_per_step": remote if world > 1 else None,
         "clocks": clocks,

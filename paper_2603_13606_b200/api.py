@@ -47,6 +47,10 @@ _HOST_MAPPED = os.environ.get("EPB_HOST_MAPPED", "1") != "0"
 _HOST_MAPPED_IN = os.environ.get("EPB_HOST_MAPPED_IN", "0") == "1"
 
 
+# entry points that never read or write a window (local routing layout)
+_WINDOW_FREE = frozenset({"epb_routing_layout"})
+
+
 @dataclass
 class AllocationHooks:
     """Caller-supplied provider of the group window (api.py:43-55).
@@ -170,7 +174,15 @@ class EpGroup:
         self._handles: list = []
         self._next_seq = 0
         self._ht_round = 0
-        self._ht_open = None
+        # HT: the handle whose round is open (opened by create_handle or a
+        # reused handle's dispatch, closed by its combine or by destroying it
+        # before dispatch) — one open round per group (ht.py:355-357, :619)
+        self._ht_active: Optional["EpHandle"] = None
+        # enqueued library entry points: all of them, and those that touch any
+        # window (the analogue of the reference fabric's put/signal/lsa
+        # counters that its tests assert unchanged on rejected calls)
+        self.launches = 0
+        self.traffic = 0
         self._alive = True
         self.strict = strict
         self._marks = None
@@ -229,9 +241,11 @@ class EpGroup:
 
     def check(self) -> None:
         """Synchronise and raise any error the kernels recorded (timeouts,
-        routing validation, weight mismatch)."""
+        routing validation, weight mismatch).  The whole device is
+        synchronised: the group's kernels may have gone to any stream that
+        was current at the call (ProcessFabric follows the caller's stream)."""
         code = ctypes.c_int32(0)
-        self.stream.synchronize()  # the group's stream may be a non-blocking one
+        torch.cuda.synchronize(self.device)
         _lib.call("epb_group_poll_error", self._g, 1, ctypes.byref(code))
         if code.value:
             raise_status(code.value, "device-side failure recorded by the EP kernels")
@@ -266,7 +280,11 @@ class EpGroup:
         """Call a C entry point; `name` may carry a ":label" suffix that
         only names the timing mark."""
         self.mark(name)
-        _lib.call(name.split(":")[0], *args)
+        fn = name.split(":")[0]
+        self.launches += 1
+        if fn not in _WINDOW_FREE:
+            self.traffic += 1
+        _lib.call(fn, *args)
 
     def _fused_ok(self) -> bool:
         """Send and receive halves may share one (cooperative) launch unless
@@ -295,12 +313,23 @@ class EpGroup:
         return handle
 
     def _open_ht_round(self, handle: "EpHandle") -> None:
-        if self._ht_open is not None and self._ht_open() is not None and self._ht_open()._round_open:
+        """Run the metadata collective for `handle` (HTRank.open_round,
+        ht.py:335-368): refused while any round of this group is open, i.e.
+        until the previous round's combine (ht.py:355-357, reset at :619)."""
+        if self._ht_active is not None:
             raise EpError(ErrorCode.HANDLE_STATE_ERROR, "previous round still open; combine first")
         rnd = self._ht_round
         self._ht_round += 1
-        handle._open_round(rnd)
-        self._ht_open = weakref.ref(handle)
+        self._ht_active = handle
+        try:
+            handle._open_round(rnd)
+        except BaseException:
+            self._ht_active = None
+            raise
+
+    def _close_ht_round(self, handle: "EpHandle") -> None:
+        if self._ht_active is handle:
+            self._ht_active = None
 
     def destroy(self) -> None:
         """Release the window; all handles must be destroyed (api.py:241-253)."""
@@ -791,6 +820,7 @@ class EpHandle:
         if back:
             out.view().copy_(o, non_blocking=not g.strict)
         self._combine_stats = None
+        g._close_ht_round(self)
         self.state = HandleState.COMBINED
 
     def expert_out_buffer(self) -> torch.Tensor:
@@ -884,7 +914,10 @@ class EpHandle:
         """Retire the handle; legal only with no round in flight."""
         self._require((HandleState.CREATED, HandleState.COMBINED), "destroy handle")
         if self._round_open:
-            self._round_open = False  # metadata went out, payload never followed
+            # HT: metadata went out, payload never followed; every rank drops
+            # the round with its handle (HTRank.abort_round, ht.py:370-377)
+            self._round_open = False
+            self.group._close_ht_round(self)
         self.state = HandleState.DESTROYED
         try:
             self.group._handles.remove(self)

@@ -96,6 +96,21 @@ class Buffer:
         else:
             self._comm.wait_stream(torch.cuda.current_stream())
 
+    def _guard(self, inputs, outputs) -> None:
+        """Caching-allocator stream bookkeeping: inputs made on the caller's
+        stream are read on the communication stream, outputs allocated on
+        the communication stream are consumed on the caller's stream — each
+        must not be recycled before the other stream is done with it."""
+        cur = torch.cuda.current_stream()
+        if cur == self._comm:
+            return
+        for t in inputs:
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(self._comm)
+        for t in outputs:
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(cur)
+
     def _leave(self, async_finish: bool) -> torch.cuda.Event:
         ev = self.capture()
         if not async_finish:
@@ -164,6 +179,8 @@ class Buffer:
                 recv_x = (recv, scales) if scales is not None else recv
                 recv_i = res.counts
                 recv_w = None
+        self._guard((x, x_scales, topk_idx, topk_weights),
+                    (recv_x if isinstance(recv_x, tuple) else (recv_x,)) + (recv_i, recv_w))
         self._last_handle = handle
         ev = self._leave(async_finish)
         self._last_event = ev
@@ -183,6 +200,7 @@ class Buffer:
             out = torch.empty((w.shape[0], cfg.hidden), dtype=odt, device=self.group.device)
             handle.combine([tensor_from_torch(x, TensorTag.TOKENS), tensor_from_torch(w, TensorTag.TOPK_WEIGHTS)],
                            [tensor_from_torch(out, TensorTag.TOKENS)])
+        self._guard((x, topk_weights, w), (out,))
         ev = self._leave(async_finish)
         self._last_event = ev
         return out, topk_weights, ev

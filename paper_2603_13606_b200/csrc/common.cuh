@@ -27,15 +27,14 @@ EPB_DEV void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 EPB_DEV void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-// Release before a flag that a peer GPU acquires.  MEMBAR.GPU already waits
-// for this thread's outstanding stores, NVLink peer stores included
-// (tools/fence_micro.cu on this system: ~12k cycles after 64 peer stores per
-// warp, ~300 with none), so the flag cannot overtake the data; MEMBAR.SYS
-// adds a fixed ~6.8k cycles (~3.5 us) of host-coherence work that peers on
-// NVLink do not need.  The receiving side keeps ld.acquire.sys.  `strict`
-// (EPB_SYS_FENCE=1) restores fence.acq_rel.sys.
-EPB_DEV void fence_release(bool strict) {
-  if (strict) asm volatile("fence.acq_rel.sys;" ::: "memory");
+// Release before a flag that a peer acquires.  `sys`: the peer may run on
+// another GPU, so the fence must be system scope (a GPU-scope fence orders
+// nothing for an observer outside this GPU in the PTX memory model).  The
+// flag-writing thread issues it after a block barrier, so by cumulativity it
+// covers the payload stores of every thread of the CTA.  GPU scope is used
+// only while all ranks share this GPU (N = 1 or emulated ranks).
+EPB_DEV void fence_release(bool sys) {
+  if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
   else asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 EPB_DEV uint64_t globaltimer() {

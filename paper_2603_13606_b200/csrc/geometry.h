@@ -15,9 +15,10 @@
 namespace epb {
 
 constexpr int kMaxRanksHost = 64;
-// LL kernels run a fixed, rank-independent grid (one 512-thread CTA per B200
-// SM, co-resident for the cooperative fused launch) so every rank knows how
-// many per-CTA flags each peer publishes
+// LL kernels run a rank-independent grid (default one 512-thread CTA per
+// B200 SM, co-resident for the cooperative fused launch; EPB_LL_CTAS picks a
+// smaller one so LL can share the GPU with compute) — every rank must use
+// the same value: a receiver expects one arrival per source CTA
 constexpr int kLLGrid = 148;
 
 inline size_t a16(size_t x) { return (x + 15) / 16 * 16; }
@@ -25,23 +26,27 @@ inline size_t a256(size_t x) { return (x + 255) / 256 * 256; }
 inline int width_of(int dt) { return dt == EPB_F32 ? 4 : (dt == EPB_FP8 ? 1 : 2); }
 
 // LL, per parity:
-//   [count words: L*N u64][dispatch flags: N*grid u64][combine flags: N*grid u64]
+//   [count rows: N src x (L+1) u32]   row src = m of each of this rank's local
+//                                     experts from src, then q (slots from src)
+//   [dispatch arrivals: N src u64][combine arrivals: N src u64]
 //   [disp slots: n_disp x slot_stride]                      (256-aligned)
 //   [comb slots: n_comb x comb_stride]
 // slot = [row RBp][scales SBp][hdr: t, kcount, K ids, K ranks (HBp)]
+// Arrivals are cumulative: every CTA of a source adds 1 per round after a
+// release, so round seq on parity seq&1 is complete at grid*((seq>>1)+1).
 struct LLGeom {
   int N, E, L, K, H, B, wire, cwire, scales, layout;
   int RB, RBp, SB, SBp, HB, HBp, CB;
   int slot_stride, comb_stride;
   int64_t n_disp, n_comb;
-  uint64_t disp_ctr, disp_flag, comb_flag, disp_slot, comb_slot;  // offsets within a parity
-  int grid;  // CTAs of every LL launch (kLLGrid)
+  uint64_t cnt_row, d_arr, c_arr, disp_slot, comb_slot;  // offsets within a parity
+  int grid;  // CTAs of every LL launch (the same on every rank: receivers expect `grid` arrivals)
   uint64_t Lmagic;  // ceil(2^32 / L): owner rank e / L = (e * Lmagic) >> 32 (exact for e * L < 2^32)
   uint64_t Kmagic;  // ceil(2^32 / K): token of a routing item i / K (i * K < 2^32)
   uint64_t parity_bytes, window_bytes, logical_bytes;
   uint64_t barrier;  // [N] u64 device-barrier flags (after both parities)
   uint64_t yout, yout_rows, yrow;  // registered expert-output region [L][N*B] bf16 rows (expert_out_window)
-  int sys_fence;                   // release fences at system scope (EPB_SYS_FENCE=1)
+  int sys_fence;                   // release fences at system scope (peers on other GPUs)
 };
 
 // HT:
@@ -89,13 +94,11 @@ inline void make_ll_geom(const epb_config& c, LLGeom& g) {
     g.n_disp = (int64_t)g.N * g.B;
     g.n_comb = (int64_t)g.B * g.K;
   }
-  // per parity: count words [L*N] (m, q of each (local expert, src) pair),
-  // dispatch flags [N src][grid CTA], combine flags [N src][grid CTA]
   g.grid = kLLGrid;
-  g.disp_ctr = 0;
-  g.disp_flag = pairs * 8;
-  g.comb_flag = g.disp_flag + (uint64_t)g.N * g.grid * 8;
-  g.disp_slot = a256(g.comb_flag + (uint64_t)g.N * g.grid * 8);
+  g.cnt_row = 0;
+  g.d_arr = a16((uint64_t)g.N * (g.L + 1) * 4);
+  g.c_arr = g.d_arr + (uint64_t)g.N * 8;
+  g.disp_slot = a256(g.c_arr + (uint64_t)g.N * 8);
   g.comb_slot = a256(g.disp_slot + (uint64_t)g.n_disp * g.slot_stride);
   g.parity_bytes = a256(g.comb_slot + (uint64_t)g.n_comb * g.comb_stride);
   g.yrow = a16(2 * (uint64_t)c.hidden);

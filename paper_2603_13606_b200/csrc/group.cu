@@ -139,9 +139,20 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
   g->rank = rank;
   make_ll_geom(*cfg, g->ll);
   make_ht_geom(*cfg, g->ht);
+  // release fences: system scope whenever a peer window lives on another GPU
+  // (epb_group_open_peers); GPU scope only while every rank is on this GPU.
+  // EPB_SYS_FENCE=1 forces system scope everywhere; EPB_SYS_FENCE=0 forces
+  // GPU scope even across GPUs (outside the PTX memory model: measurement only)
   {
     const char* f = getenv("EPB_SYS_FENCE");
-    g->ll.sys_fence = g->ht.sys_fence = (f && atoi(f) != 0) ? 1 : 0;
+    g->fence_override = f ? (atoi(f) != 0 ? 1 : 0) : -1;
+    g->ll.sys_fence = g->ht.sys_fence = g->fence_override == 1 ? 1 : 0;
+  }
+  // LL grid (identical on every rank: receivers count one arrival per
+  // source CTA); EPB_LL_CTAS < 148 leaves SMs free for concurrent compute
+  if (const char* c = getenv("EPB_LL_CTAS")) {
+    const int v = atoi(c);
+    if (v >= 1 && v <= kLLGrid) g->ll.grid = v;
   }
   const uint64_t need = cfg->algorithm == EPB_LL ? g->ll.window_bytes : g->ht.window_bytes;
   cudaGetDevice(&g->device);
@@ -152,6 +163,7 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
     if (g->d_err) cudaFree(g->d_err);
     if (g->d_done) cudaFree(g->d_done);
     if (g->d_scratch) cudaFree(g->d_scratch);
+    if (g->d_seq) cudaFree(g->d_seq);
     if (g->d_lay) cudaFree(g->d_lay);
     delete g;
     return code;
@@ -175,6 +187,8 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
   if (e == cudaSuccess) e = cudaMalloc(&g->d_err, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&g->d_done, sizeof(int) * 4 * n);
   if (e == cudaSuccess) e = cudaMalloc(&g->d_scratch, sizeof(int) * (8 * n + 2 * l * n + 64));
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_seq, sizeof(uint32_t) * kLLGrid);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->d_seq, 0, sizeof(uint32_t) * kLLGrid, s);
   if (e == cudaSuccess)
     e = cudaMalloc(&g->d_lay, sizeof(int) * (size_t)((cfg->max_tokens_per_rank + kLayChunk - 1) / kLayChunk) *
                                   (cfg->num_experts + n));
@@ -253,6 +267,7 @@ int epb_group_open_peers(epb_group* g, const epb_ipc_desc* descs) {
   EPB_CUDA(cudaMemcpy(g->d_peers, ptrs.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice));
   g->peers_ready = true;
   g->sys_scope = true;
+  g->ll.sys_fence = g->ht.sys_fence = g->fence_override == 0 ? 0 : 1;
   return EPB_OK;
 }
 
@@ -294,6 +309,7 @@ int epb_group_destroy(epb_group* g) {
   cudaFree(g->d_err);
   cudaFree(g->d_done);
   cudaFree(g->d_scratch);
+  cudaFree(g->d_seq);
   cudaFree(g->d_lay);
   delete g;
   return EPB_OK;

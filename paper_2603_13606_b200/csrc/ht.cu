@@ -53,6 +53,7 @@ EPB_DEV void st_plain_v4(void* p, int4 v) {
 // K5a: metadata all-gather over the windows
 // ---------------------------------------------------------------------------
 struct HTMetaSend {
+  const int* err;  // a routing the layout kernel rejected sends nothing (validation before traffic)
   const int32_t* m;
   const int32_t* q;
   const uint64_t* peers;
@@ -63,6 +64,7 @@ struct HTMetaSend {
 
 __global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
   const HTGeom& g = p.g;
+  if (*reinterpret_cast<const volatile int*>(p.err) != 0) return;
   const int C = g.E + g.N;
   const uint64_t row_off = g.meta + ((uint64_t)p.parity * g.N + p.rank) * C * 4;
   for (int i = threadIdx.x; i < g.N * C; i += blockDim.x) {
@@ -1025,7 +1027,7 @@ extern "C" {
 int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay, void* stream) {
   if (int rc = check_ht(g, 1)) return rc;
   HTMetaSend p;
-  p.m = lay->expert_count; p.q = lay->rank_count; p.peers = g->d_peers; p.g = g->ht;
+  p.err = g->d_err; p.m = lay->expert_count; p.q = lay->rank_count; p.peers = g->d_peers; p.g = g->ht;
   p.rank = g->rank; p.parity = round & 1; p.tag = ht_tag(round);
   ht_meta_send_kernel<<<1, 256, 0, as_stream(stream)>>>(p);
   EPB_LAUNCH_CHECK();

@@ -20,7 +20,8 @@ struct epb_group {
   std::vector<void*> ipc_opened;
   int* d_err = nullptr;         // device error word
   int* d_done = nullptr;        // [2*N] arrival counters (dispatch, combine)
-  int* d_scratch = nullptr;     // [4*N + 2*L*N + 64] small per-call state
+  int* d_scratch = nullptr;     // [8*N + 2*L*N + 64] small per-call state
+  uint32_t* d_seq = nullptr;    // [kLLGrid] LL round sequence, one copy per dispatch CTA
   int* d_lay = nullptr;         // [ceil(B / kLayChunk)][E+N] per-chunk routing histograms (K1)
   epb::LLGeom ll;
   epb::HTGeom ht;
@@ -28,6 +29,7 @@ struct epb_group {
   uint64_t* trace = nullptr;    // optional [grid][16] globaltimer stamps (diagnostics)
   bool peers_ready = false;
   bool sys_scope = false;       // peers on other GPUs: system-scope fences/flags
+  int fence_override = -1;      // EPB_SYS_FENCE: -1 auto, 0 GPU scope, 1 system scope
 };
 
 namespace epb {

@@ -1,31 +1,36 @@
 // Low-Latency dispatch / combine: two kernels per round (K2+K3 fused, K4a+K4b
 // fused), each runnable as send-only, recv-only or both (one cooperative
-// launch).  Every LL launch uses the same fixed grid (kLLGrid CTAs) on every
-// rank, so a receiver knows how many per-CTA flags each peer publishes.
+// launch when peers are other GPUs).  Every LL launch of a group uses the same
+// grid on every rank: a receiver expects one arrival per source CTA.
 //
 // Reference semantics (epsim ll.py):
 //  * dispatch send (ll.py:255-308): per destination rank d, the tokens that
 //    touch d go, ascending t, into d's slots [src*B + j]; the receiver learns
 //    m(e, src) per (local expert, src) pair (the reference's counter value
-//    m + 1).  Here CTA 0 of the source writes the tagged count words
-//    (tag << 40) | (q << 20) | m and every source CTA publishes one tagged
-//    flag per destination after a release fence; the tag (from the round
-//    sequence) replaces the reference's counter reset (ll.py:351-353).
-//  * dispatch recv (ll.py:310-400): after all flags of all sources, every
-//    slot row goes to recv[l, src*B + i] for each local expert; i (the
-//    filled[l] order) and j (the slot) are prefix counts the SENDER computes
-//    over its earlier tokens, i travels in the slot header after the
-//    reference header fields (layout.py:282-295).
+//    m + 1).  Here one CTA of the source writes a count row (m of each of d's
+//    experts, then q = slots) into d's window, and once every source CTA has
+//    stored, the source adds one arrival to d's counter for it after a
+//    system-scope release.  Arrivals are cumulative per parity, so round seq
+//    is complete at (seq>>1)+1: the counter never needs the reference's
+//    reset (ll.py:351-353).
+//  * dispatch recv (ll.py:310-400): every slot row goes to recv[l, src*B + i]
+//    for each local expert; i (the filled[l] order) and j (the slot) are
+//    prefix counts the SENDER computes over its earlier tokens, i travels in
+//    the slot header after the reference header fields (layout.py:282-295).
+//    Each receiving warp waits only for the source of its own task, so slots
+//    of early sources are placed while later sources are still sending.
 //  * combine send (ll.py:404-462): each valid expert row (l, src, i) goes,
 //    in the combine wire dtype, to src's slot t*K + k.
 //  * combine recv (ll.py:464-507): out[t] = sum_k w[t,k] * y_k in f32,
-//    ascending k from acc = 0, explicit __fmul_rn/__fadd_rn (no FMA).
+//    ascending k from acc = 0, explicit __fmul_rn/__fadd_rn (no FMA); a warp
+//    waits only for the owners of its token's experts.
 //
 // Latency design (B200): the token row is prefetched into registers at
-// kernel start so its DRAM latency hides behind the routing pass; routing
-// validation, counts and prefix ranks are one parallel shared-memory pass;
-// flags replace atomics; copies keep 8 x 16 B loads in flight per lane;
-// fences/flags use GPU scope when every rank lives on this GPU.
+// kernel start; the routing snapshot is one coalesced load into shared
+// memory; a CTA computes only its own tokens' positions (prefix counts over
+// the earlier tokens, warp reductions) while its warps quantise; one release
+// fence per rank (system scope when peers are other GPUs; the last CTA to finish), then one arrival per destination; receivers
+// poll N counters, not per-CTA flags.
 #include <algorithm>
 
 #include "common.cuh"
@@ -37,6 +42,7 @@ constexpr int kPhaseSend = 1, kPhaseRecv = 2;
 constexpr int kThreads = 512;
 constexpr int kUnroll = 8;
 constexpr int kParts = 4;  // combine send: warps per row
+constexpr uint32_t kPoison = 0xFFFFFFFFu;  // count row of a source whose routing was rejected
 
 // diagnostics: thread 0 of each CTA stamps the global timer at checkpoints
 #define LL_STAMP(P, I)                                                                    \
@@ -44,7 +50,6 @@ constexpr int kParts = 4;  // combine send: warps per row
     if ((P).trace && threadIdx.x == 0) (P).trace[blockIdx.x * 16 + (I)] = globaltimer(); \
   } while (0)
 
-EPB_DEV uint32_t ll_tag_of(uint32_t seq) { return (seq % 0xFFFFFFu) + 1u; }
 // round counters: written by an earlier kernel (visible at the kernel
 // boundary) and not again until every CTA has read them — a relaxed GPU-scope
 // load suffices (a volatile, i.e. system-scope, load measured ~2 us slower)
@@ -55,22 +60,23 @@ EPB_DEV uint32_t ld_round_u32(const uint32_t* p) {
 }
 EPB_DEV uint8_t* peer_base(const uint64_t* peers, int r) { return reinterpret_cast<uint8_t*>(peers[r]); }
 
-// (the release fence itself: fence_release in common.cuh)
-EPB_DEV void st_flag(uint64_t* p, uint64_t v, bool sys) {
-  if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-  else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-EPB_DEV uint64_t ld_flag(const uint64_t* p, bool sys) {
+EPB_DEV uint64_t ld_acq(const uint64_t* p, bool sys) {
   uint64_t v;
   if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-// spin until the low 32 bits equal `tag` (bounded; records TransportClosed)
-EPB_DEV bool wait_flag(const uint64_t* f, uint32_t tag, bool sys, uint64_t timeout_ns, int* err) {
+// one arrival (the caller released first: fence_release, then these)
+EPB_DEV void red_arrive(uint64_t* p, bool sys) {
+  if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+  else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+}
+// spin until *c >= need (bounded; records TransportClosed).  Acquire: what
+// the arriving CTAs stored before their release is visible afterwards.
+EPB_DEV bool wait_arrivals(const uint64_t* c, uint64_t need, bool sys, uint64_t timeout_ns, int* err) {
   uint64_t start = 0;
   for (int spins = 0;; ++spins) {
-    if ((uint32_t)ld_flag(f, sys) == tag) return true;
+    if (ld_acq(c, sys) >= need) return true;
     if ((spins & 31) != 31) continue;
     if (*(volatile int*)err != 0) return false;
     if (spins == 63) start = globaltimer();
@@ -79,6 +85,46 @@ EPB_DEV bool wait_flag(const uint64_t* f, uint32_t tag, bool sys, uint64_t timeo
       return false;
     }
   }
+}
+// Publish this rank's part of a round: every CTA releases its stores at GPU
+// scope and counts itself in at a local counter; the last CTA then issues
+// the one system-scope release of the rank and adds one arrival at each
+// peer.  By cumulativity the system-scope fence covers every CTA's stores
+// (each CTA's GPU-scope release is acquired by the last CTA's RMW on the
+// counter), so peers on other GPUs see all payload once they see the
+// arrival — at the cost of one MEMBAR.SYS per rank per phase instead of one
+// per CTA (concurrent system-scope fences from every SM measured several us).
+// All threads call.  `done`: this kind's local counter (reset by the last).
+EPB_DEV void ll_arrive(const uint64_t* peers, uint64_t off, int N, int me, bool fence_sys, bool sys,
+                       unsigned* done) {
+  __syncthreads();
+  if (threadIdx.x == 0 && N > 1) {
+    fence_release(false);
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *done = 0u;  // next use is a later kernel (stream order)
+      fence_release(fence_sys);
+      for (int d = 0; d < N; ++d)
+        if (d != me) red_arrive(reinterpret_cast<uint64_t*>(peer_base(peers, d) + off) + me, sys);
+    }
+  }
+}
+// warp: wait until every source in `need` (bit per rank) has arrived; bits
+// already seen are cached in `seen`.  Lane 0 polls; __syncwarp orders the
+// other lanes' later loads after its acquire.
+EPB_DEV bool warp_wait_sources(uint64_t need, uint64_t& seen, const uint64_t* ctr, uint64_t target, bool sys,
+                               uint64_t timeout_ns, int* err, int lane) {
+  need &= ~seen;
+  bool ok = true;
+  while (need) {
+    const int s = __ffsll((long long)need) - 1;
+    if (lane == 0) ok = wait_arrivals(&ctr[s], target, sys, timeout_ns, err);
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) return false;
+    seen |= 1ull << s;
+    need &= need - 1;
+  }
+  __syncwarp();
+  return true;
 }
 EPB_DEV int4 ld_weak_v4(const void* p) {
   int4 v;
@@ -163,8 +209,8 @@ struct LLDisp {
   const uint64_t* peers;
   const uint8_t* win;
   int* err;
-  uint32_t* dseq;
-  int* drd;
+  uint32_t* dseq;  // [grid] round sequence: CTA c reads and advances its own copy
+  unsigned* done;  // local CTA-completion counter of the send phase (ll_arrive)
   uint64_t* trace;
   LLGeom g;
   uint64_t timeout_ns;
@@ -230,13 +276,398 @@ EPB_DEV void ll_copy_row(const LLGeom& g, const uint8_t* slot, uint8_t* orow, fl
   }
 }
 
+// the exact quotient for the rare near-midpoint elements: one out-of-line
+// copy of the IEEE division sequence instead of one per unrolled element
+__device__ __noinline__ float div_rn_call(float a, float b) { return __fdiv_rn(a, b); }
+
+// f32 values of one 16-B wire chunk -> the wire image (block-128 FP8 scale
+// over 8 aligned lanes; `scale` = the block's scale, 0 for non-FP8 wires)
+template <int WT, bool SC>
+EPB_DEV int4 wire_chunk(float* f, float& scale, int lane) {
+  constexpr int EPC = Elems<WT>::n;
+  scale = 0.0f;
+  if constexpr (SC) {
+    float amax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < EPC; ++i) amax = fmaxf(amax, fabsf(f[i]));
+    const unsigned gm = 0xFFu << (lane & 24);
+    amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 1));
+    amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 2));
+    amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 4));
+    scale = __fdiv_rn(amax, 448.0f);
+    const float div = scale > 0.0f ? scale : 1.0f;
+    // fl32(x / div) without 16 IEEE division sequences: q = x * rcp(div),
+    // then one exact-residual correction (Markstein), correctly rounded for
+    // |x|, div in [2^-100, 2^100] (checked against IEEE division on 10^9
+    // random pairs, tools/div_check.c); the sign of a zero quotient follows
+    // x.  Anything outside that range takes the out-of-line IEEE division.
+    const float r = __frcp_rn(div);
+    bool slow = div < 0x1p-100f || div > 0x1p100f;
+#pragma unroll
+    for (int i = 0; i < EPC; ++i) slow |= f[i] != 0.0f && fabsf(f[i]) < 0x1p-100f;
+    if (!slow) {
+#pragma unroll
+      for (int i = 0; i < EPC; ++i) {
+        const float q = __fmul_rn(f[i], r);
+        const float res = __fmaf_rn(-q, div, f[i]);
+        f[i] = copysignf(__fmaf_rn(res, r, q), f[i]);
+      }
+    } else {
+      float tmp[EPC];
+#pragma unroll
+      for (int i = 0; i < EPC; ++i) tmp[i] = f[i];
+#pragma unroll 1
+      for (int i = 0; i < EPC; ++i) tmp[i] = div_rn_call(tmp[i], div);
+#pragma unroll
+      for (int i = 0; i < EPC; ++i) f[i] = tmp[i];
+    }
+  }
+  return pack16<WT>(f);
+}
+
+// chunk c of an input row as f32 (from prefetched registers when given)
+template <int XT, int EPC, int NV>
+EPB_DEV void input_chunk(const int4* pre, const uint8_t* xrow, const float* xsc, int c, float* f) {
+  if (pre != nullptr) {
+    if constexpr (NV > 0) {
+      constexpr int XW = XT == EPB_F32 ? 4 : (XT == EPB_FP8 ? 1 : 2);
+      constexpr int PER = 16 / XW;
+#pragma unroll
+      for (int u = 0; u < NV; ++u) unpack16<XT>(pre[u], f + u * PER);
+      if constexpr (XT == EPB_FP8) {
+        if (xsc != nullptr) {
+#pragma unroll
+          for (int i = 0; i < EPC; ++i) f[i] = __fmul_rn(f[i], xsc[((int64_t)c * EPC + i) >> 7]);
+        }
+      }
+      return;
+    }
+  }
+  load_input_chunk<XT, EPC>(xrow, xsc, (int64_t)c * EPC, f);
+}
+
+EPB_DEV int sel8(const int* v, int i) {
+  int r = v[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) r = i == k ? v[k] : r;
+  return r;
+}
+
+// Send phase, fast path (top-k <= 8, batch <= block size, hidden % 16 == 0).
+// Thread tau holds routing row tau in registers: validation, the earlier-
+// token prefix counts of the CTA's token and the counting CTA's histograms
+// need no shared-memory staging.  Work units are (token, part): a small
+// batch spreads each token over up to 8 CTAs so few warps per SM quantise
+// (latency, not throughput, bounds a decode step).  One barrier (which also
+// reduces the validation verdict) separates the position pass from the
+// stores; every warp derives the destination list itself.
+// Returns the routing verdict (true = rejected, nothing was sent).
 template <int XT, int WT, bool SC, int OT>
+EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t& seq, uint64_t& parity_off) {
+  const LLGeom& g = p.g;
+  const int K = g.K, N = g.N, H = g.H, L = g.L, E = g.E, B = g.B, G = gridDim.x;
+  const int b = p.b, me = p.rank, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5, BD = blockDim.x;
+  constexpr int EPC = Elems<WT>::n;
+  constexpr int XW = XT == EPB_F32 ? 4 : (XT == EPB_FP8 ? 1 : 2);
+  constexpr int NV = (EPC * XW) >= 16 ? (EPC * XW) / 16 : 0;
+  constexpr int OB = OT == EPB_F32 ? 4 : (OT == EPB_FP8 ? 1 : 2);
+  const int nch = H / EPC;
+  const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
+  const int lo = me * L;
+  const int nloc = max(0, min(L, E - lo));
+  // parts per token: chunk ranges are multiples of 8 chunks (FP8 blocks)
+  int P = b > 0 ? G / b : 1;
+  P = max(1, min(min(P, 8), max(1, nch / 8)));
+  const int per = ((nch + P - 1) / P + 7) & ~7;
+  const int units = b * P;
+  __shared__ int s_part[kThreads / 32][16];  // per-warp prefix partials (i of k, then j of k)
+  __shared__ uint32_t s_seq2;
+  const uint64_t L_magic = g.Lmagic;
+  auto owner_of = [&](int e) { return (int)(((uint64_t)(uint32_t)e * L_magic) >> 32); };
+
+  // chunks per thread held in registers (one 16-element FP8 chunk covers
+  // H <= 8192 at 512 threads; 8-element wires take two); wider rows finish
+  // in a loop that quantises as it stores
+  constexpr int CPT = EPC >= 16 ? 1 : 2;
+  // first unit's input chunks, prefetched (their DRAM latency overlaps the
+  // routing loads and the position pass)
+  int4 xr[CPT][NV > 0 ? NV : 1];
+  bool xpre[CPT];
+#pragma unroll
+  for (int r = 0; r < CPT; ++r) xpre[r] = false;
+  {
+    const int u = blockIdx.x;
+    if (NV > 0 && u < units) {
+      const int t = u / P, c0 = (u - t * P) * per, c1 = min(nch, c0 + per);
+#pragma unroll
+      for (int r = 0; r < CPT; ++r) {
+        const int c = c0 + tid + r * BD;
+        if (c < c1) {
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(p.x) + ((int64_t)t * H + (int64_t)c * EPC) * XW;
+#pragma unroll
+          for (int v = 0; v < (NV > 0 ? NV : 1); ++v) xr[r][v] = ld_nc_v4(src + 16 * v);
+          xpre[r] = true;
+        }
+      }
+    }
+  }
+  // this thread's routing row (token tid): range, distinctness, owners
+  int rw[8];
+  bool row_ok = true;
+  uint64_t own = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    rw[k] = -1 - k;
+    if (tid < b && k < K) {
+      const int64_t v = __ldg(p.topk + (int64_t)tid * K + k);
+      const bool in = v >= 0 && v < E;
+      row_ok &= in;
+      rw[k] = in ? (int)v : -100;
+    }
+  }
+#pragma unroll
+  for (int k = 1; k < 8; ++k)
+#pragma unroll
+    for (int j = 0; j < k; ++j) row_ok &= rw[j] != rw[k];
+  if (tid < b && row_ok) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < K) own |= 1ull << owner_of(rw[k]);
+  }
+  if (tid == 0) {
+    // every CTA advances its own copy of the round sequence (the copies move
+    // in lockstep, no cross-CTA atomics); CTA 0 records it in the handle
+    s_seq2 = seq_ld;
+    p.dseq[blockIdx.x] = seq_ld + 1;
+    if (blockIdx.x == 0) *p.hseq = seq_ld;
+  }
+  LL_STAMP(p, 8);
+  bool bad = false;
+  for (int it = 0, u = blockIdx.x;; ++it, u += G) {
+    const bool has = u < units;
+    int t = 0, c0 = 0, c1 = 0;
+    if (has) {
+      t = u / P;
+      c0 = (u - t * P) * per;
+      c1 = min(nch, c0 + per);
+    }
+    int et[8];  // token t's experts (broadcast loads)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      et[k] = -2 - k;
+      if (has && k < K) {
+        const int64_t v = __ldg(p.topk + (int64_t)t * K + k);
+        et[k] = (v >= 0 && v < E) ? (int)v : 0;
+      }
+    }
+    const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
+    const float* xsc = p.x_scales ? p.x_scales + (int64_t)t * (H / 128) : nullptr;
+    int4 qv[CPT];
+    float qs[CPT];
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+      const int c = c0 + tid + r * BD;
+      qs[r] = 0.0f;
+      if (has && c < c1) {
+        float f[EPC];
+        input_chunk<XT, EPC, NV>(it == 0 && xpre[r] ? xr[r] : nullptr, xrow, xsc, c, f);
+        qv[r] = wire_chunk<WT, SC>(f, qs[r], lane);
+      }
+    }
+    LL_STAMP(p, 9);
+    // prefix partials: i_k = #{t' < t routed to e_tk}, j_k = #{t' < t
+    // touching owner(e_tk)} over this thread's token t' = tid
+    uint32_t hit_i = 0, hit_j = 0;
+    if (has && tid < t) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < K) {
+          bool in = false;
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) in |= rw[k2] == et[k];
+          hit_i |= (uint32_t)in << k;
+          hit_j |= (uint32_t)((own >> owner_of(et[k])) & 1ull) << k;
+        }
+      }
+    }
+    int my_i = 0, my_j = 0;
+    if (has && warp * 32 < t) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < K) {
+          const int ci = __reduce_add_sync(0xffffffffu, (hit_i >> k) & 1u);
+          const int cj = __reduce_add_sync(0xffffffffu, (hit_j >> k) & 1u);
+          if (lane == k) {
+            my_i = ci;
+            my_j = cj;
+          }
+        }
+      }
+    }
+    if (lane < 8) {
+      s_part[warp][lane] = my_i;
+      s_part[warp][8 + lane] = my_j;
+    }
+    if (it == 0) {
+      bad = __syncthreads_or(tid < b && !row_ok) != 0;
+      seq = s_seq2;
+      parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+    } else {
+      __syncthreads();
+    }
+    if (!has || bad) break;
+    LL_STAMP(p, 10);
+    // destinations of token t (every warp derives them): lanes k < K
+    int e = -1, d = -1, ci = 0, cj = 0;
+    if (lane < K) {
+      e = sel8(et, lane);
+      d = owner_of(e);
+      const int wl = (t + 31) >> 5;  // warps that held earlier tokens
+      for (int w = 0; w < wl; ++w) {
+        ci += s_part[w][lane];
+        cj += s_part[w][8 + lane];
+      }
+    }
+    const bool mine = lane < K && d == me;
+    bool first = lane < K && !mine;
+    if (!legacy) {  // optimized: one slot per destination rank (dedup)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int dj = __shfl_sync(0xffffffffu, d, j);
+        first &= !(j < lane && dj == d);
+      }
+    }
+    const unsigned fm = __ballot_sync(0xffffffffu, first);
+    const unsigned mm = __ballot_sync(0xffffffffu, mine);
+    const int jslot = legacy ? ((e - d * L) * N + me) * B + ci : me * B + cj;
+    const int srow = mine ? (e - lo) * N * B + me * B + ci : -1;
+    const uint64_t slot_off = parity_off + g.disp_slot;
+    if (c0 == 0 && warp == 0) {
+      // part 0: routing metadata and the slot headers (t, K, ids, ranks)
+      if (lane < K) {
+        if (p.self_row) p.self_row[(int64_t)t * K + lane] = srow;
+        if (p.owner_row) p.owner_row[(int64_t)t * K + lane] = (e - d * L) * N * B + me * B + ci;
+        if (mine) p.src_info[srow] = t * K + lane;
+      }
+      const int ve = __shfl_sync(0xffffffffu, e, max(0, min(31, lane - 2)));
+      const int vc = __shfl_sync(0xffffffffu, ci, max(0, min(31, lane - 2 - K)));
+      const uint32_t word = lane == 0 ? (uint32_t)t : lane == 1 ? (uint32_t)K : lane < 2 + K ? (uint32_t)ve : (uint32_t)vc;
+      for (unsigned m = fm; m; m &= m - 1) {
+        const int ln = __ffs(m) - 1;
+        const int dd = __shfl_sync(0xffffffffu, d, ln), jj = __shfl_sync(0xffffffffu, jslot, ln);
+        if (lane < 2 + 2 * K)
+          reinterpret_cast<uint32_t*>(peer_base(p.peers, dd) + slot_off + (int64_t)jj * g.slot_stride + g.RBp +
+                                      g.SBp)[lane] = word;
+      }
+    }
+    // chunk c to every destination slot and every own-expert output row
+    auto emit = [&](int c, bool ok, const int4& v, float scale) {
+      for (unsigned m = fm; m; m &= m - 1) {
+        const int ln = __ffs(m) - 1;
+        const int dd = __shfl_sync(0xffffffffu, d, ln), jj = __shfl_sync(0xffffffffu, jslot, ln);
+        if (ok) {
+          uint8_t* slot = peer_base(p.peers, dd) + slot_off + (int64_t)jj * g.slot_stride;
+          st_na_v4(slot + (int64_t)c * 16, v);
+          if constexpr (SC) {
+            if ((c & 7) == 0) reinterpret_cast<float*>(slot + g.RBp)[c >> 3] = scale;
+          }
+        }
+      }
+      for (unsigned m = mm; m; m &= m - 1) {
+        const int sr = __shfl_sync(0xffffffffu, srow, __ffs(m) - 1);
+        if (ok) {
+          uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)sr * H * OB;
+          if constexpr (OT == WT) {
+            st_v4(orow + (int64_t)c * 16, v);
+            if constexpr (SC) {
+              if ((c & 7) == 0) p.out_scales[(int64_t)sr * (H / 128) + (c >> 3)] = scale;
+            }
+          } else {
+            float fw[EPC];  // the f32 image of what a slot would carry
+            unpack16<WT>(v, fw);
+            if constexpr (SC) {
+#pragma unroll
+              for (int i = 0; i < EPC; ++i) fw[i] = __fmul_rn(fw[i], scale);
+            }
+            store_f32_chunk<EPB_F32, EPC>(orow, (int64_t)c * EPC, fw);
+          }
+        }
+      }
+    };
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+      const int c = c0 + tid + r * BD;
+      emit(c, c < c1, qv[r], qs[r]);
+    }
+    // chunks beyond CPT per thread (very wide rows): quantise as they go
+    for (int cb = c0 + CPT * BD + warp * 32; cb < c1; cb += BD) {
+      const int c = cb + lane;
+      int4 v = make_int4(0, 0, 0, 0);
+      float scale = 0.0f;
+      float f[EPC];
+      if (c < c1) input_chunk<XT, EPC, NV>(nullptr, xrow, xsc, c, f);
+      else {
+#pragma unroll
+        for (int i = 0; i < EPC; ++i) f[i] = 0.0f;
+      }
+      v = wire_chunk<WT, SC>(f, scale, lane);
+      emit(c, c < c1, v, scale);
+    }
+    LL_STAMP(p, 2);
+    if (u + G >= units) break;
+    __syncthreads();  // s_part reuse by the next unit
+  }
+  LL_STAMP(p, 3);
+  if ((int)blockIdx.x == G - 1) {
+    // the counting CTA: m(e) and q(d) over the batch (ll.py:255-259,
+    // :292-296) -> a count row into every peer's window (m of the peer's
+    // experts, then q), own counts straight to the counts output
+    int* s_m = smem;    // [E]
+    int* s_q = smem + E;  // [N]
+#pragma unroll 1
+    for (int e2 = tid; e2 < E; e2 += BD) s_m[e2] = 0;
+    if (tid < N) s_q[tid] = 0;
+    __syncthreads();
+    if (!bad && tid < b) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < K) atomicAdd(&s_m[rw[k]], 1);
+      for (uint64_t o = own; o; o &= o - 1) atomicAdd(&s_q[__ffsll((long long)o) - 1], 1);
+    }
+    __syncthreads();
+    const int R = L + 1;
+#pragma unroll 1
+    for (int i = tid; i < N * R; i += BD) {
+      const int d2 = i / R, l = i - d2 * R;
+      if (d2 == me) continue;
+      const uint32_t v = bad ? kPoison : (l < L ? (d2 * L + l < E ? (uint32_t)s_m[d2 * L + l] : 0u) : (uint32_t)s_q[d2]);
+      reinterpret_cast<uint32_t*>(peer_base(p.peers, d2) + parity_off + g.cnt_row)[me * R + l] = v;
+    }
+#pragma unroll 1
+    for (int l = tid; l < L; l += BD) {
+      const int m = l < nloc && !bad ? s_m[lo + l] : 0;
+      p.counts_i32[l * N + me] = m;
+      p.counts_f32[l * N + me] = (float)m;
+    }
+    if (bad && tid == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
+  }
+  (void)nw;
+  return bad;
+}
+
+// FAST: the decode hot path only (ll_send_fast + the optimized-layout vector
+// receive) — a compact kernel keeps the instruction footprint small (cold
+// i-cache after an L2 flush was the largest stall of the combined kernel);
+// everything else (top-k > 8, batches above the block size, unaligned
+// hidden, the legacy layout) runs the general kernel.
+template <int XT, int WT, bool SC, int OT, bool FAST>
 __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   extern __shared__ int smem[];
   const LLGeom& g = p.g;
-  const int K = g.K, N = g.N, H = g.H, L = g.L, E = g.E, B = g.B, G = g.grid;
-  const int b = p.b;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = g.K, N = g.N, H = g.H, L = g.L, E = g.E, B = g.B, G = gridDim.x;
+  const int b = p.b, me = p.rank;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const bool sys = p.sys;
   constexpr int EPC = Elems<WT>::n;
   constexpr int XW = XT == EPB_F32 ? 4 : (XT == EPB_FP8 ? 1 : 2);
@@ -244,168 +675,91 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   const bool vec = (H & 15) == 0;
   const int nch = vec ? H / EPC : 0;
   constexpr int OB = OT == EPB_F32 ? 4 : (OT == EPB_FP8 ? 1 : 2);  // output element bytes
+  const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
+  const int lo = me * L;
+  const int nloc = max(0, min(L, E - lo));
 
   // split: warps 1.. quantise a token's chunks (<= 2 each, in registers)
-  // while warp 0 resolves its destinations; else every thread loops
+  // while the position pass runs; else every thread loops
   const int nq = (int)blockDim.x - 32;
   const bool split = vec && nch <= 2 * nq;
   const int c_first = split ? (int)threadIdx.x - 32 : (int)threadIdx.x;  // first chunk of this thread
   // prefetch this CTA's first token chunk: its DRAM latency overlaps the
-  // routing pass below
+  // routing load and the position pass
   int4 xr[NV > 0 ? NV : 1];
-  const bool pre = (p.phases & kPhaseSend) && NV > 0 && vec && (int)blockIdx.x < b && c_first >= 0 && c_first < nch;
+  const bool pre = !FAST && (p.phases & kPhaseSend) && NV > 0 && vec && (int)blockIdx.x < b && c_first >= 0 &&
+                   c_first < nch;
   if (pre) {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(p.x) +
                          ((int64_t)blockIdx.x * H + (int64_t)c_first * EPC) * XW;
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) xr[v] = ld_nc_v4(src + 16 * v);
   }
-  // prefetch this thread's first two routing items (t*K + k) and, for
-  // top-k <= 8, the routing row of token t = threadIdx.x (validation)
-  int64_t rid0 = 0, rid1 = 0;
-  int64_t row[8];
-  const bool row_pre = (p.phases & kPhaseSend) && K <= 8 && (int)threadIdx.x < b;
-  if (p.phases & kPhaseSend) {
-    const int i0 = (int)threadIdx.x, i1 = i0 + (int)blockDim.x;
-    if (i0 < b * K) rid0 = __ldg(p.topk + i0);
-    if (i1 < b * K) rid1 = __ldg(p.topk + i1);
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) row[k] = (row_pre && k < K) ? __ldg(p.topk + (int64_t)threadIdx.x * K + k) : -1 - k;
   LL_STAMP(p, 0);
   // round sequence: thread 0 issues the load now; it lands in shared memory
-  // at the first block barrier after the routing pass (send) or right away
+  // at the first block barrier
   __shared__ uint32_t s_seq;
+  __shared__ int s_bad;
   uint32_t seq_ld = 0;
-  if (threadIdx.x == 0) seq_ld = ld_round_u32((p.phases & kPhaseSend) ? p.dseq : p.hseq);
-  uint32_t seq = 0, tag = 0;
+  if (threadIdx.x == 0) seq_ld = ld_round_u32((p.phases & kPhaseSend) ? p.dseq + blockIdx.x : p.hseq);
+  uint32_t seq = 0;
   uint64_t parity_off = 0;
-  // per-expert token counts of this round (send phase; the fused receive
-  // takes its own-rank counts from here)
-  int* s_m = nullptr;
 
-  if (p.phases & kPhaseSend) {
-    // shared: routing snapshot, per-expert and per-destination token bitmaps
-    // (bit t' of word t'/32), per-expert / per-destination counts
-    const int W = (b + 31) >> 5;
-    int* s_topk = smem;                                                        // [b*K]
-    uint32_t* s_ebits = reinterpret_cast<uint32_t*>(s_topk + b * K);           // [E][W]
-    uint32_t* s_dbits = s_ebits + E * W;                                       // [N][W]
-    s_m = reinterpret_cast<int*>(s_dbits + N * W);                             // [E]
-    int* s_q = s_m + E;                                                        // [N]
-    __shared__ int s_bad, s_nd;
+  if constexpr (FAST) {
+    if (p.phases & kPhaseSend) {
+      const bool bad = ll_send_fast<XT, WT, SC, OT>(p, smem, seq_ld, seq, parity_off);
+      // publish: one system-scope release per rank, one arrival per destination
+      ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done);
+      LL_STAMP(p, 4);
+      if (bad) return;
+    }
+  } else if (p.phases & kPhaseSend) {
+    int* s_topk = smem;           // [b*K] routing snapshot (-1 = id out of range)
+    int* s_m = s_topk + b * K;    // [E] per-expert token counts (counting CTA)
+    int* s_q = s_m + E;           // [N] tokens per destination (counting CTA)
+    __shared__ int s_nd;
+    __shared__ int s_cnt[2 * kMaxTopK];  // this token's prefix counts: i per k, then j per k
     // per destination entry: rank and absolute slot index in its window
     // (optimized: one slot per (token, dst) at src*B + j; legacy: one slot
     // per (token, expert) at ((e - dL)*N + src)*B + i)
     __shared__ int s_dst[kMaxRanks], s_j[kMaxRanks];
     __shared__ int s_self[kMaxTopK];  // output row of (t, k) for this rank's own experts, else -1
     __shared__ uint32_t s_hdr[2 + 2 * kMaxTopK];
-    for (int i = threadIdx.x; i < E * W; i += blockDim.x) s_ebits[i] = 0;
+    const int items = b * K;
+    for (int i = threadIdx.x; i < items; i += blockDim.x) {
+      const int64_t e = __ldg(p.topk + i);
+      s_topk[i] = (e >= 0 && e < E) ? (int)e : -1;
+    }
+    if ((int)threadIdx.x < 2 * kMaxTopK) s_cnt[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
     LL_STAMP(p, 8);
-    // routing (api.py:150-170).  Rows: range check and distinct experts,
-    // from registers (one token per thread).  Items (t, k), one per thread
-    // per pass (coalesced): snapshot and the token bitmap of each expert.
-    // No value-returning atomics and no dependent shared-memory chains on
-    // this path: each link of such a chain costs ~30+ cycles.
+    // routing validation (api.py:150-170): ids in range, distinct per row;
+    // every CTA reaches the same verdict before any traffic
     for (int t = threadIdx.x; t < b; t += blockDim.x) {
       bool ok = true;
-      if (K <= 8) {
-        int64_t v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = (t == (int)threadIdx.x && row_pre) ? row[k] : (k < K ? p.topk[(int64_t)t * K + k] : -1 - k);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          ok &= k >= K || (v[k] >= 0 && v[k] < E);
-#pragma unroll
-          for (int j = 0; j < k; ++j) ok &= v[j] != v[k];
-        }
-      } else {
-        for (int k = 0; k < K; ++k) {
-          const int64_t e = p.topk[(int64_t)t * K + k];
-          ok &= e >= 0 && e < E;
-          for (int j = 0; j < k; ++j) ok &= p.topk[(int64_t)t * K + j] != e;
-        }
+      for (int k = 0; k < K; ++k) {
+        const int e = s_topk[t * K + k];
+        ok &= e >= 0;
+        for (int j = 0; j < k; ++j) ok &= s_topk[t * K + j] != e;
       }
       if (!ok) s_bad = 1;
     }
-    const int items = b * K;
-    for (int i = threadIdx.x, r = 0; i < items; i += blockDim.x, ++r) {
-      const int64_t e = r == 0 ? rid0 : (r == 1 ? rid1 : p.topk[i]);
-      const int t = (int)(((uint64_t)i * g.Kmagic) >> 32);
-      s_topk[i] = (int)e;
-      if (e >= 0 && e < E) atomicOr(&s_ebits[(int)e * W + (t >> 5)], 1u << (t & 31));
-    }
-    __syncthreads();
-    LL_STAMP(p, 13);
-    // per expert (threads [0, E)): token count = popcount of its bitmap;
-    // per destination word (threads [E, E + N*W)): OR of its experts' words
-    for (int u = threadIdx.x; u < E + N * W; u += blockDim.x) {
-      if (u < E) {
-        int m = 0;
-        if (W <= 16) {
-#pragma unroll
-          for (int w = 0; w < 16; ++w) m += w < W ? __popc(s_ebits[u * W + min(w, W - 1)]) : 0;
-        } else {
-          for (int w = 0; w < W; ++w) m += __popc(s_ebits[u * W + w]);
-        }
-        s_m[u] = m;
-      } else {
-        const int d = (u - E) / W, w = (u - E) - d * W;
-        const int e0 = d * L, e1 = min(E, e0 + L);
-        uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
-        int e = e0;
-        for (; e + 4 <= e1; e += 4) {
-          o0 |= s_ebits[e * W + w];
-          o1 |= s_ebits[(e + 1) * W + w];
-          o2 |= s_ebits[(e + 2) * W + w];
-          o3 |= s_ebits[(e + 3) * W + w];
-        }
-        for (; e < e1; ++e) o0 |= s_ebits[e * W + w];
-        s_dbits[d * W + w] = o0 | o1 | o2 | o3;
-      }
-    }
-    LL_STAMP(p, 10);
-    uint32_t arrived = 0;
     if (threadIdx.x == 0) {
+      // the round: every CTA advances its own copy of the sequence (all
+      // copies move in lockstep, no cross-CTA atomics); CTA 0 records it in
+      // the handle word for the receive launch and the combine
       s_seq = seq_ld;
-      LL_STAMP(p, 11);
-      // every CTA has read the round counter (its value is consumed above,
-      // so the read is complete): arrive now, act on the result at the end
-      // of the send phase (the round trip overlaps it)
-      arrived = atomicAdd(reinterpret_cast<unsigned*>(p.drd), 1u);
-      LL_STAMP(p, 12);
+      p.dseq[blockIdx.x] = seq_ld + 1;
+      if (blockIdx.x == 0) *p.hseq = seq_ld;
     }
     __syncthreads();
-    seq = s_seq;
-    tag = ll_tag_of(seq);
-    parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
     LL_STAMP(p, 1);
-    // the last CTA to arrive records the round in the handle word and
-    // advances the group counter (all CTAs have read it)
-    auto commit_round = [&]() {
-      if (threadIdx.x == 0 && arrived == (uint32_t)gridDim.x - 1) {
-        *p.drd = 0;
-        *p.hseq = seq;
-        *p.dseq = seq + 1;
-      }
-    };
-    if (s_bad) {
-      // validation before any traffic: every CTA reaches the same verdict
-      if (threadIdx.x == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
-      commit_round();
-      return;
-    }
-    LL_STAMP(p, 2);
-    // tokens per destination (count words), read at the publish below
-    for (int d = threadIdx.x; d < N; d += blockDim.x) {
-      int q = 0;
-      for (int w = 0; w < W; ++w) q += __popc(s_dbits[d * W + w]);
-      s_q[d] = q;
-    }
+    seq = s_seq;
+    parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+    const bool bad = s_bad != 0;
     const uint64_t slot_off = parity_off + g.disp_slot;
-    const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
+
     // one token chunk: input (prefetched for the CTA's first token) ->
     // f32 -> optional block-128 FP8 scale (x / scale, correctly rounded) ->
     // 16-B wire image
@@ -426,22 +780,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       } else {
         load_input_chunk<XT, EPC>(xrow, xsc, (int64_t)c * EPC, f);
       }
-      scale = 0.0f;
-      if constexpr (SC) {
-        // block-128 = 8 consecutive 16-element chunks = 8 aligned lanes
-        float amax = 0.0f;
-#pragma unroll
-        for (int i = 0; i < EPC; ++i) amax = fmaxf(amax, fabsf(f[i]));
-        const unsigned gm = 0xFFu << (lane & 24);
-        amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 1));
-        amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 2));
-        amax = fmaxf(amax, __shfl_xor_sync(gm, amax, 4));
-        scale = __fdiv_rn(amax, 448.0f);
-        const float div = scale > 0.0f ? scale : 1.0f;
-#pragma unroll
-        for (int i = 0; i < EPC; ++i) f[i] = __fdiv_rn(f[i], div);
-      }
-      v = pack16<WT>(f);
+      v = wire_chunk<WT, SC>(f, scale, lane);
     };
     // chunk c to every destination slot and every own-expert output row
     auto emit = [&](int c, const int4& v, float scale, int nd) {
@@ -472,7 +811,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         }
       }
     };
-    for (int t = blockIdx.x; t < b; t += G) {
+    for (int t = blockIdx.x; !bad && t < b; t += G) {
       const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.x) + (int64_t)t * H * XW;
       const float* xsc = p.x_scales ? p.x_scales + (int64_t)t * (H / 128) : nullptr;
       int4 qv[2];
@@ -483,37 +822,72 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           const int c = c_first + r * nq;
           if (c < nch) quantize(t, c, xrow, xsc, qv[r], qs[r]);
         }
+        if (p.trace && threadIdx.x == 32) p.trace[blockIdx.x * 16 + 9] = globaltimer();
       }
+      // positions of token t: i_k = #{t' < t routed to e_tk} (ll.py:383-399)
+      // and j_k = #{t' < t touching owner(e_tk)} (ll.py:292-296), one
+      // earlier token per thread, warp reductions, shared atomics per warp
+      for (int base = warp * 32; base < t; base += (int)blockDim.x) {
+        const int tp = base + lane;
+        uint32_t hit_i = 0, hit_j = 0;
+        if (tp < t) {
+          if (K <= 8) {  // both rows in registers
+            int rw[8], et[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              rw[k] = k < K ? s_topk[tp * K + k] : -1;
+              et[k] = k < K ? s_topk[t * K + k] : -2;
+            }
+            uint64_t own = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k < K) own |= 1ull << (int)(((uint64_t)rw[k] * g.Lmagic) >> 32);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              bool in = false;
+#pragma unroll
+              for (int k2 = 0; k2 < 8; ++k2) in |= rw[k2] == et[k];
+              hit_i |= (uint32_t)in << k;
+              if (k < K) hit_j |= (uint32_t)((own >> (int)(((uint64_t)et[k] * g.Lmagic) >> 32)) & 1ull) << k;
+            }
+          } else {
+            uint64_t own = 0;
+            for (int k2 = 0; k2 < K; ++k2) own |= 1ull << (int)(((uint64_t)s_topk[tp * K + k2] * g.Lmagic) >> 32);
+            for (int k = 0; k < K; ++k) {
+              const int e = s_topk[t * K + k];
+              bool in = false;
+              for (int k2 = 0; k2 < K; ++k2) in |= s_topk[tp * K + k2] == e;
+              hit_i |= (uint32_t)in << k;
+              hit_j |= (uint32_t)((own >> (int)(((uint64_t)e * g.Lmagic) >> 32)) & 1ull) << k;
+            }
+          }
+        }
+        int my_i = 0, my_j = 0;
+        for (int k = 0; k < K; ++k) {
+          const int ci = __reduce_add_sync(0xffffffffu, (hit_i >> k) & 1u);
+          const int cj = __reduce_add_sync(0xffffffffu, (hit_j >> k) & 1u);
+          if (lane == k) { my_i = ci; my_j = cj; }
+        }
+        if (lane < K) {
+          atomicAdd(&s_cnt[lane], my_i);
+          atomicAdd(&s_cnt[kMaxTopK + lane], my_j);
+        }
+      }
+      if (warp == 0) LL_STAMP(p, 10);
+      __syncthreads();
       if (warp == 0) {
-        // lane k: i = #{t' < t routed to e_tk} (popc of e's bitmap below t)
-        // and, for its owner d_k, j = #{t' < t touching d_k}; lanes keep the
-        // first occurrence of each destination
-        const uint32_t below = (1u << (t & 31)) - 1u;
-        const int wt = t >> 5;
         int e = -1, d = -1, ci = 0, cj = 0;
         if (lane < K) {
           e = s_topk[t * K + lane];
           d = (int)(((uint64_t)e * g.Lmagic) >> 32);
-          if (W <= 16) {
-#pragma unroll
-            for (int w = 0; w < 16; ++w) {
-              const int wc = min(w, W - 1);
-              const uint32_t mk = w < wt ? 0xFFFFFFFFu : (w == wt ? below : 0u);
-              ci += __popc(s_ebits[e * W + wc] & mk);
-              cj += __popc(s_dbits[d * W + wc] & mk);
-            }
-          } else {
-            for (int w = 0; w < wt; ++w) {
-              ci += __popc(s_ebits[e * W + w]);
-              cj += __popc(s_dbits[d * W + w]);
-            }
-            ci += __popc(s_ebits[e * W + wt] & below);
-            cj += __popc(s_dbits[d * W + wt] & below);
-          }
+          ci = s_cnt[lane];
+          cj = s_cnt[kMaxTopK + lane];
+          s_cnt[lane] = 0;  // ready for the next token (read above by this lane only)
+          s_cnt[kMaxTopK + lane] = 0;
         }
         // rows for this rank's own experts skip the window: they go straight
         // to the expert-major output (and the combine reads them in place)
-        const bool mine = lane < K && d == p.rank;
+        const bool mine = lane < K && d == me;
         bool first = lane < K && !mine;
         if (!legacy) {  // optimized: one slot per destination (dedup)
           for (int j = 0; j < K; ++j) {
@@ -525,15 +899,15 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         if (lane < K) {
           s_hdr[2 + lane] = (uint32_t)e;
           s_hdr[2 + K + lane] = (uint32_t)ci;
-          const int srow = mine ? (e - p.rank * L) * N * B + p.rank * B + ci : -1;
+          const int srow = mine ? (e - lo) * N * B + me * B + ci : -1;
           s_self[lane] = srow;
           if (p.self_row) p.self_row[(int64_t)t * K + lane] = srow;
-          if (p.owner_row) p.owner_row[(int64_t)t * K + lane] = (e - d * L) * N * B + p.rank * B + ci;
+          if (p.owner_row) p.owner_row[(int64_t)t * K + lane] = (e - d * L) * N * B + me * B + ci;
           if (mine) p.src_info[srow] = t * K + lane;
           if (first) {
             const int pos = __popc(fm & ((1u << lane) - 1u));
             s_dst[pos] = d;
-            s_j[pos] = legacy ? ((e - d * L) * N + p.rank) * B + ci : p.rank * B + cj;
+            s_j[pos] = legacy ? ((e - d * L) * N + me) * B + ci : me * B + cj;
           }
         }
         if (lane == 0) {
@@ -543,7 +917,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         }
       }
       __syncthreads();
-      LL_STAMP(p, 9);
+      LL_STAMP(p, 2);
       const int nd = s_nd;
       for (int w = threadIdx.x; w < 2 + 2 * K; w += blockDim.x)
         for (int i = 0; i < nd; ++i) {
@@ -590,123 +964,136 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       __syncthreads();
     }
     LL_STAMP(p, 3);
-    commit_round();
-    __syncthreads();  // s_q
-    // publish: CTA 0 writes the count words of every (local expert, src)
-    // pair at every destination; then every CTA fences and flags each
-    // destination (a receiver waits for all grid CTAs of all sources)
-    if (blockIdx.x == 0) {
-      for (int i = threadIdx.x; i < N * L; i += blockDim.x) {
-        const int d = i / L, l = i - d * L, e = d * L + l;
-        uint64_t* ctr = reinterpret_cast<uint64_t*>(peer_base(p.peers, d) + parity_off + g.disp_ctr);
-        const uint64_t m = e < E ? (uint64_t)s_m[e] : 0ull;
-        ctr[l * N + p.rank] = ((uint64_t)tag << 40) | ((uint64_t)s_q[d] << 20) | m;
+    if ((int)blockIdx.x == G - 1) {
+      // the counting CTA: m(e) per expert and q(d) per destination over the
+      // whole batch (ll.py:255-259, :292-296) -> a count row into every
+      // peer's window (m of the peer's experts, then q), own counts straight
+      // to the counts output
+      for (int e = threadIdx.x; e < E; e += blockDim.x) s_m[e] = 0;
+      for (int d = threadIdx.x; d < N; d += blockDim.x) s_q[d] = 0;
+      __syncthreads();
+      if (!bad) {
+        for (int t = threadIdx.x; t < b; t += blockDim.x) {
+          uint64_t own = 0;
+          for (int k = 0; k < K; ++k) {
+            const int e = s_topk[t * K + k];
+            atomicAdd(&s_m[e], 1);
+            own |= 1ull << (int)(((uint64_t)e * g.Lmagic) >> 32);
+          }
+          for (; own; own &= own - 1) atomicAdd(&s_q[__ffsll((long long)own) - 1], 1);
+        }
       }
+      __syncthreads();
+      const int R = L + 1;
+      for (int i = threadIdx.x; i < N * R; i += blockDim.x) {
+        const int d = i / R, l = i - d * R;
+        if (d == me) continue;
+        const uint32_t v = bad ? kPoison : (l < L ? (d * L + l < E ? (uint32_t)s_m[d * L + l] : 0u) : (uint32_t)s_q[d]);
+        reinterpret_cast<uint32_t*>(peer_base(p.peers, d) + parity_off + g.cnt_row)[me * R + l] = v;
+      }
+      for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        const int m = l < nloc && !bad ? s_m[lo + l] : 0;
+        p.counts_i32[l * N + me] = m;
+        p.counts_f32[l * N + me] = (float)m;
+      }
+      if (bad && threadIdx.x == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
     }
-    __syncthreads();
-    // (no flags to self: own rows went straight to the output and the fused
-    // receive reads its own counts from shared memory)
-    if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
-      fence_release(g.sys_fence);
-      uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.disp_flag) +
-                       (int64_t)p.rank * G + blockIdx.x;
-      st_flag(flag, (uint64_t)tag, sys);
-    }
+    // publish: one release per CTA, one arrival per destination
+    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done);
     LL_STAMP(p, 4);
+    if (bad) return;
   }
 
   if (p.phases & kPhaseRecv) {
-    __shared__ int s_rq[kMaxRanks], s_pre[kMaxRanks + 1];
-    __shared__ int s_fail;
     LL_STAMP(p, 5);
-    const int lo = p.rank * L;
-    const int nloc = max(0, min(L, E - lo));
-    if (threadIdx.x == 0) {
-      s_fail = 0;
-      if (!(p.phases & kPhaseSend)) s_seq = seq_ld;
-    }
-    __syncthreads();
     if (!(p.phases & kPhaseSend)) {
+      if (threadIdx.x == 0) s_seq = seq_ld;
+      __syncthreads();
       seq = s_seq;
-      tag = ll_tag_of(seq);
       parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
     }
-    // every CTA of every peer source (no flags from self)
-    const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.disp_flag);
-    for (int i = threadIdx.x; i < N * G; i += blockDim.x)
-      if (i / G != p.rank && !wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
-    __syncthreads();
-    if (s_fail) return;
-    LL_STAMP(p, 6);
-    const volatile uint64_t* ctr = reinterpret_cast<const volatile uint64_t*>(p.win + parity_off + g.disp_ctr);
-    if (blockIdx.x == 0) {
-      for (int i = threadIdx.x; i < L * N; i += blockDim.x) {
-        const int l = i / N, s = i - l * N;
-        int m = 0;
-        if (i < nloc * N) {
-          // own counts: this launch's routing pass (fused) or the earlier
-          // send launch's count word (split phases, stream-ordered)
-          m = (s == p.rank && s_m != nullptr) ? s_m[lo + l] : (int)(ctr[i] & 0xFFFFF);
-        }
-        p.counts_i32[i] = m;
-        p.counts_f32[i] = (float)m;
-      }
-    }
-    if (nloc == 0) return;
+    if (N == 1) return;  // own rows and counts were placed by the send phase
+    const uint64_t target = (uint64_t)((seq >> 1) + 1);
+    const uint64_t* arr = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.d_arr);
+    const uint32_t* crows = reinterpret_cast<const uint32_t*>(p.win + parity_off + g.cnt_row);
+    const int R = L + 1;
+    const int nsrc = N - 1;
     const int ob = (OT == EPB_F32 ? 4 : dtype_width(OT));
     const int64_t orow_bytes = (int64_t)H * ob;
-    const int nw = blockDim.x >> 5;
-    if (g.layout == EPB_LAYOUT_LEGACY) {
+    if (!FAST && legacy) {
       // legacy (ll.py:362-376): slot (l*N + r)*B + i holds recv[l, r*B + i]
-      // — the same linear index; rows of remote pairs, prefix over pairs
+      // — the same linear index; per source, rows of its pairs by prefix
       __shared__ int s_wsum[kThreads / 32];
-      int* s_pp = smem;  // [L*N + 1] (the send phase is done with it)
-      __syncthreads();
-      block_exclusive_scan(nloc * N, [&](int i) { return i % N == p.rank ? 0 : (int)(ctr[i] & 0xFFFFF); }, s_pp,
-                           s_wsum);
-      const int rows = s_pp[nloc * N];
-      for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * rows; f2 += gridDim.x * nw) {
-        const int r = f2 >> 1, half = f2 & 1;
-        int lo_i = 0, hi_i = nloc * N;  // largest pair with s_pp[pair] <= r
-        while (hi_i - lo_i > 1) {
-          const int mid = (lo_i + hi_i) >> 1;
-          if (s_pp[mid] <= r) lo_i = mid; else hi_i = mid;
+      __shared__ int s_ok;
+      int* s_pp = smem;  // [L + 1] (the send phase is done with it)
+      for (int so = 0; so < nsrc; ++so) {
+        const int s = (me + 1 + so) % N;
+        __syncthreads();
+        if (threadIdx.x == 0) s_ok = wait_arrivals(&arr[s], target, sys, p.timeout_ns, p.err);
+        __syncthreads();
+        if (!s_ok) return;
+        const uint32_t* crow = crows + s * R;
+        if (crow[L] == kPoison) {
+          if (threadIdx.x == 0) atomicCAS(p.err, 0, EPB_TRANSPORT_CLOSED);
+          return;
         }
-        const int64_t lin = (int64_t)lo_i * B + (r - s_pp[lo_i]);
-        const uint8_t* slot = p.win + parity_off + g.disp_slot + lin * g.slot_stride;
-        if (lane == 0 && half == 0) {
-          const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
-          const int e = lo + lo_i / N;
-          int k = 0;
-          while (k < K - 1 && (int)hdr[2 + k] != e) ++k;
-          p.src_info[lin] = (int32_t)(hdr[0] * K + k);
+        if ((int)blockIdx.x == s % G)
+          for (int l = threadIdx.x; l < L; l += blockDim.x) {
+            const int m = l < nloc ? (int)crow[l] : 0;
+            p.counts_i32[l * N + s] = m;
+            p.counts_f32[l * N + s] = (float)m;
+          }
+        block_exclusive_scan(nloc, [&](int l) { return (int)crow[l]; }, s_pp, s_wsum);
+        const int rows = s_pp[nloc];
+        for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * rows; f2 += gridDim.x * nw) {
+          const int r = f2 >> 1, half = f2 & 1;
+          int lo_i = 0, hi_i = nloc;  // largest l with s_pp[l] <= r
+          while (hi_i - lo_i > 1) {
+            const int mid = (lo_i + hi_i) >> 1;
+            if (s_pp[mid] <= r) lo_i = mid; else hi_i = mid;
+          }
+          const int64_t lin = ((int64_t)lo_i * N + s) * B + (r - s_pp[lo_i]);
+          const uint8_t* slot = p.win + parity_off + g.disp_slot + lin * g.slot_stride;
+          if (lane == 0 && half == 0) {
+            const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
+            const int e = lo + lo_i;
+            int k = 0;
+            while (k < K - 1 && (int)hdr[2 + k] != e) ++k;
+            p.src_info[lin] = (int32_t)(hdr[0] * K + k);
+          }
+          ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + lin * orow_bytes,
+                                  SC ? p.out_scales + lin * (H / 128) : nullptr, lane, half, 2);
         }
-        ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + lin * orow_bytes,
-                                SC ? p.out_scales + lin * (H / 128) : nullptr, lane, half, 2);
       }
       LL_STAMP(p, 7);
       return;
     }
-    // own rows were placed by the send phase; only remote slots remain
-    if ((int)threadIdx.x < N) s_rq[threadIdx.x] = (int)threadIdx.x == p.rank ? 0 : (int)((ctr[threadIdx.x] >> 20) & 0xFFFFF);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int run = 0;
-      for (int s = 0; s < N; ++s) { s_pre[s] = run; run += s_rq[s]; }
-      s_pre[N] = run;
-    }
-    __syncthreads();
-    // warp tasks (slot, half row): the header is read once, the row loaded
-    // once and stored to every local expert the slot names (the fan-out of
-    // ll.py:378-400); CTA-major order spreads the tasks over every SM
-    const int nslots = s_pre[N];
+    // warp tasks (source, slot j, half row), sources interleaved so a warp's
+    // successive tasks visit different sources; each warp waits only for
+    // its task's source.  The header is read once, the row loaded once and
+    // stored to every local expert the slot names (the fan-out of
+    // ll.py:378-400).  Task (s, 0, 0) also writes the counts of pairs (l, s).
     const bool fan = (H & 15) == 0;
-    constexpr int EPC = Elems<WT>::n;
-    for (int f2 = warp * gridDim.x + blockIdx.x; f2 < 2 * nslots; f2 += gridDim.x * nw) {
-      const int sl = f2 >> 1, half = f2 & 1;
-      int s = 0;
-      while (s_pre[s + 1] <= sl) ++s;
-      const int j = sl - s_pre[s];
+    uint64_t seen = 0;
+    const int tasks = 2 * B * nsrc;
+    for (int f2 = warp * gridDim.x + blockIdx.x; f2 < tasks; f2 += gridDim.x * nw) {
+      const int half = f2 & 1, r = f2 >> 1;
+      const int j = r / nsrc, so = r - j * nsrc;
+      const int s = me + 1 + so < N ? me + 1 + so : me + 1 + so - N;
+      if (!warp_wait_sources(1ull << s, seen, arr, target, sys, p.timeout_ns, p.err, lane)) return;
+      const uint32_t* crow = crows + s * R;
+      const uint32_t q = crow[L];
+      if (q == kPoison) {
+        if (lane == 0) atomicCAS(p.err, 0, EPB_TRANSPORT_CLOSED);
+        return;
+      }
+      if (j == 0 && half == 0)
+        for (int l = lane; l < L; l += 32) {
+          const int m = l < nloc ? (int)crow[l] : 0;
+          p.counts_i32[l * N + s] = m;
+          p.counts_f32[l * N + s] = (float)m;
+        }
+      if (j >= (int)q) continue;
       const uint8_t* slot = p.win + parity_off + g.disp_slot + ((int64_t)s * B + j) * g.slot_stride;
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
       int e = -1, ci = 0;
@@ -718,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const int my_orow = (e - lo) * N * B + s * B + ci;
       const unsigned lm = __ballot_sync(0xffffffffu, loc);
       if (half == 0 && loc) p.src_info[my_orow] = (int32_t)(hdr[0] * K + lane);
-      if (!fan) {
+      if (!FAST && !fan) {
         for (unsigned mm = lm; mm; mm &= mm - 1) {
           const int64_t row = __shfl_sync(0xffffffffu, my_orow, __ffs(mm) - 1);
           ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + row * orow_bytes,
@@ -726,9 +1113,9 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         }
         continue;
       }
-      const int nch = H / EPC;
-      const int per = (nch + 1) / 2;
-      const int c0 = half * per, c1 = min(nch, c0 + per);
+      const int nch2 = H / EPC;
+      const int per = (nch2 + 1) / 2;
+      const int c0 = half * per, c1 = min(nch2, c0 + per);
       for (int base = c0; base < c1; base += 32 * kUnroll) {
         int4 v[kUnroll];
 #pragma unroll
@@ -797,6 +1184,7 @@ struct LLComb {
   const uint64_t* peers;
   const uint8_t* win;
   int* err;
+  unsigned* done;  // local CTA-completion counter of the send phase (ll_arrive)
   uint64_t* trace;
   LLGeom g;
   uint64_t timeout_ns;
@@ -804,11 +1192,14 @@ struct LLComb {
   bool sys;
 };
 
-template <int IT, int WT, int OT>
+// VEC: hidden % 16 == 0 (the vector paths only; the element paths are a
+// separate instantiation, keeping the hot kernel's code small)
+template <int IT, int WT, int OT, bool VEC>
 __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
   extern __shared__ int s_pre[];  // [L*N + 1]
   const LLGeom& g = p.g;
-  const int N = g.N, L = g.L, B = g.B, H = g.H, K = g.K, G = g.grid;
+  const int N = g.N, L = g.L, B = g.B, H = g.H, K = g.K, G = gridDim.x;
+  const int me = p.rank;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const bool sys = p.sys;
   LL_STAMP(p, 0);
@@ -816,9 +1207,9 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
   __shared__ int s_wsum[kThreads / 32];
   // the round load is in flight while the send phase loads its counts
   uint32_t seq_ld = 0;
-  if (threadIdx.x == 0) seq_ld = ld_round_u32(p.hseq);
+  if (threadIdx.x == 0 && N > 1) seq_ld = ld_round_u32(p.hseq);
   constexpr int EPC = Elems<WT>::n;
-  const bool vec = (H & 15) == 0;
+  constexpr bool vec = VEC;
   const int nch = vec ? H / EPC : 0;
   // rows of this rank's own source tokens never travel: only N > 1 sends
   const bool send = (p.phases & kPhaseSend) && N > 1 && !p.pull;
@@ -830,10 +1221,14 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // counts of the (l, src) pairs, own-source pairs excluded
     for (int i = i0; i < min(P, i0 + per); ++i) local += (i % N == p.rank) ? 0 : p.counts[i];
   }
-  if (threadIdx.x == 0) s_seq = seq_ld;
-  __syncthreads();
-  const uint32_t seq = s_seq;
-  const uint32_t tag = ll_tag_of(seq);
+  // (one rank: every row is this rank's own, read in place — no slots, no
+  // round parity, no barrier)
+  uint32_t seq = 0;
+  if (N > 1) {
+    if (threadIdx.x == 0) s_seq = seq_ld;
+    __syncthreads();
+    seq = s_seq;
+  }
   const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
 
   if (send) {
@@ -904,24 +1299,14 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         for (int el = lane; el < H; el += 32) store_elem(dst, WT, el, load_elem(yrow, IT, el));
       }
     }
-    __syncthreads();
     LL_STAMP(p, 2);
-    if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
-      fence_release(g.sys_fence);
-      uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.comb_flag) +
-                       (int64_t)p.rank * G + blockIdx.x;
-      st_flag(flag, (uint64_t)tag, sys);
-    }
+  }
+  if ((p.phases & kPhaseSend) && N > 1) {
+    // one release per CTA, one arrival per home rank (pulled combine: the
+    // expert outputs were written by earlier kernels on this stream — the
+    // arrival announces them)
+    ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done);
     LL_STAMP(p, 3);
-  } else if ((p.phases & kPhaseSend) && N > 1 && p.pull) {
-    // pulled combine: nothing moves; announce that this rank's expert
-    // outputs (written by earlier kernels on this stream) are complete
-    if ((int)threadIdx.x < N && (int)threadIdx.x != p.rank) {
-      fence_release(g.sys_fence);
-      uint64_t* flag = reinterpret_cast<uint64_t*>(peer_base(p.peers, threadIdx.x) + parity_off + g.comb_flag) +
-                       (int64_t)p.rank * G + blockIdx.x;
-      st_flag(flag, (uint64_t)tag, sys);
-    }
   }
 
   if (p.phases & kPhaseRecv) {
@@ -938,35 +1323,39 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // (read in place from the expert output) or its combine slot — and w_k;
     // the first task's rows are resolved before the flag wait
     const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
-    int my_self = -1, my_slot = 0;
+    int my_self = -1, my_slot = 0, my_owner = me;
     uint64_t my_pull = 0;  // pulled combine: the row in its owner's window
     float my_w = 0.0f;
     auto fetch = [&](int tk) {  // lane k's row of token tk
       if (lane < K) {
         const int64_t i = (int64_t)tk * K + lane;
         my_w = p.w[i];
+        const int e = (int)p.topk[i];
+        my_owner = (int)(((uint64_t)e * g.Lmagic) >> 32);
         if (p.pull) {
-          const int e = (int)p.topk[i];
-          const int owner = (int)(((uint64_t)e * g.Lmagic) >> 32);
-          my_pull = reinterpret_cast<uint64_t>(peer_base(p.peers, owner) + g.yout) + (uint64_t)p.owner_row[i] * g.yrow;
+          my_pull = reinterpret_cast<uint64_t>(peer_base(p.peers, my_owner) + g.yout) + (uint64_t)p.owner_row[i] * g.yrow;
         } else {
           my_self = p.self_row ? p.self_row[i] : -1;
-          my_slot = legacy ? (int)p.topk[i] * B + tk : tk * K + lane;
+          my_slot = legacy ? e * B + tk : tk * K + lane;
         }
       }
     };
     if (vec && task < tasks) fetch(task / segs);
-    if (threadIdx.x == 0) s_fail = 0;
-    __syncthreads();
-    const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.comb_flag);
-    for (int i = threadIdx.x; i < N * G; i += blockDim.x)
-      if (i / G != p.rank && !wait_flag(&flags[i], tag, sys, p.timeout_ns, p.err)) s_fail = 1;
-    __syncthreads();
-    if (s_fail) return;
+    const uint64_t target = (uint64_t)((seq >> 1) + 1);
+    const uint64_t* arr = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.c_arr);
+    uint64_t seen = 0;
     LL_STAMP(p, 5);
     if (vec) {
       for (; task < tasks; task += tstride) {
         const int t = task / segs, sg = task - t * segs;
+        // the owners of this token's experts must have arrived (rows pushed
+        // into our slots, or, pulled, their expert outputs announced)
+        if (N > 1) {
+          const uint64_t bit = (lane < K && my_owner != me) ? 1ull << my_owner : 0ull;
+          const uint64_t need = (uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)bit) |
+                                ((uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)(bit >> 32)) << 32);
+          if (!warp_wait_sources(need, seen, arr, target, sys, p.timeout_ns, p.err, lane)) return;
+        }
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
         const int cbase = sg * kSeg + lane;
         const bool ok0 = cbase < nch, ok1 = cbase + 32 < nch;
@@ -1034,6 +1423,14 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         if (ok1) store_f32_chunk<OT, EPC>(orow, (int64_t)(cbase + 32) * EPC, acc1);
       }
     } else {
+      // element path (hidden not a multiple of 16): every source first
+      if (threadIdx.x == 0) {
+        s_fail = 0;
+        for (int s2 = 0; s2 < N; ++s2)
+          if (s2 != me && !wait_arrivals(&arr[s2], target, sys, p.timeout_ns, p.err)) s_fail = 1;
+      }
+      __syncthreads();
+      if (s_fail) return;
       for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
         __syncthreads();
         if ((int)threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
@@ -1130,7 +1527,12 @@ cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const
 
 template <int XT, int WT, bool SC, int OT>
 cudaError_t run_disp(const LLDisp& p, size_t smem, cudaStream_t s) {
-  return launch(ll_dispatch_kernel<XT, WT, SC, OT>, p.g.grid, smem, p.phases == 3, p, s);
+  // fused send + receive across GPUs: receivers spin on arrivals from peer
+  // GPUs' CTAs, which must all be resident -> cooperative launch
+  const bool coop = p.phases == 3 && p.g.N > 1;
+  const bool fast = p.g.K <= 8 && p.b <= kThreads && (p.g.H & 15) == 0 && p.g.layout == EPB_LAYOUT_OPTIMIZED;
+  return fast ? launch(ll_dispatch_kernel<XT, WT, SC, OT, true>, p.g.grid, smem, coop, p, s)
+              : launch(ll_dispatch_kernel<XT, WT, SC, OT, false>, p.g.grid, smem, coop, p, s);
 }
 
 template <int XT, int WT, bool SC>
@@ -1153,7 +1555,9 @@ cudaError_t run_disp_x(const LLDisp& p, int out_dtype, size_t smem, cudaStream_t
 
 template <int IT, int WT, int OT>
 cudaError_t run_comb(const LLComb& p, size_t smem, cudaStream_t s) {
-  return launch(ll_combine_kernel<IT, WT, OT>, p.g.grid, smem, p.phases == 3, p, s);
+  const bool coop = p.phases == 3 && p.g.N > 1;
+  return (p.g.H & 15) == 0 ? launch(ll_combine_kernel<IT, WT, OT, true>, p.g.grid, smem, coop, p, s)
+                           : launch(ll_combine_kernel<IT, WT, OT, false>, p.g.grid, smem, coop, p, s);
 }
 
 template <int IT, int WT>
@@ -1208,14 +1612,15 @@ int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases, const epb_ll_d
   p.out = a->out; p.out_scales = a->out_scales; p.counts_f32 = a->counts_f32; p.counts_i32 = a->counts_i32;
   p.src_info = a->src_info; p.self_row = a->self_row; p.owner_row = a->owner_row;
   p.peers = g->d_peers; p.win = g->window; p.err = g->d_err;
-  p.dseq = reinterpret_cast<uint32_t*>(g->d_scratch); p.drd = g->d_scratch + 1; p.trace = g->trace;
+  p.dseq = g->d_seq; p.done = reinterpret_cast<unsigned*>(g->d_scratch) + 4; p.trace = g->trace;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;
   const int E = g->ll.E, N = g->ll.N, K = g->ll.K;
-  const size_t W = (size_t)(b + 31) / 32;
-  size_t smem = (phases & kPhaseSend) ? sizeof(int) * ((size_t)b * K + (E + N) * W + E + N) : 0;
-  if ((phases & kPhaseRecv) && g->cfg.layout == EPB_LAYOUT_LEGACY)  // receive: pair prefix [L*N + 1]
-    smem = std::max(smem, sizeof(int) * ((size_t)g->ll.L * N + 1));
+  // send: routing snapshot [b*K] + per-expert / per-destination counts;
+  // legacy receive: per-source expert prefix [L + 1]
+  size_t smem = (phases & kPhaseSend) ? sizeof(int) * ((size_t)b * K + E + N) : 0;
+  if ((phases & kPhaseRecv) && g->cfg.layout == EPB_LAYOUT_LEGACY)
+    smem = std::max(smem, sizeof(int) * ((size_t)g->ll.L + 1));
   if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "LL batch too large for the fused dispatch kernel");
   cudaStream_t s = as_stream(stream);
   cudaError_t e;
@@ -1253,6 +1658,7 @@ int epb_ll_combine(epb_group* g, const uint32_t* hseq, int32_t phases, const epb
                  g->ll.yout_rows == 0 || a->expert_out != g->window + g->ll.yout))
     return fail(EPB_INVALID_ARGUMENT, "pulled combine needs bf16 rows in the window's expert-output region");
   p.hseq = hseq; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err; p.trace = g->trace;
+  p.done = reinterpret_cast<unsigned*>(g->d_scratch) + 5;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;
   const size_t smem = sizeof(int) * ((size_t)g->ll.L * g->ll.N + 1);

@@ -153,8 +153,6 @@ def ht_dispatch_stats(cfg: EpConfig, rank: int, routing: np.ndarray, meta_q: np.
     for d in range(n):
         st.msgs += 1
         st.bytes_put += (e + n) * 4
-        if d // rpn != node:
-            pass  # rows=0 for metadata stores: no row counters move
         st.signals += 1
     rec = _ht_record_bytes(cfg)
     for d in range(n):

@@ -13,7 +13,7 @@ import paper_2603_13606_b200 as ep
 from oracle import codecs as oc
 from oracle import ht as oht
 from oracle import ll as oll
-from paper_2603_13606_b200.harness import run_ranks
+from tests.rank_threads import run_ranks
 
 DT = {"f32": ep.Dtype.F32, "bf16": ep.Dtype.BF16, "f16": ep.Dtype.F16, "fp8": ep.Dtype.FP8}
 

@@ -8,6 +8,7 @@ expected values from the same seeded workload).
         --master-port 29511 tests/mp_worker.py
 """
 
+import contextlib
 import os
 import sys
 import traceback
@@ -25,6 +26,18 @@ from oracle import ll as oll  # noqa: E402
 from oracle import workload as owl  # noqa: E402
 
 T = ep.TensorTag
+
+
+@contextlib.contextmanager
+def host_mapped_input(on: bool):
+    """Pinned host token inputs read in place by the dispatch kernel for the
+    duration of the block (api._HOST_MAPPED_IN), restored on any exit."""
+    prev = _api._HOST_MAPPED_IN
+    _api._HOST_MAPPED_IN = bool(on)
+    try:
+        yield
+    finally:
+        _api._HOST_MAPPED_IN = prev
 
 
 def bf16r(x):
@@ -48,7 +61,6 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
         want = oll.combine(ys, wl.routing, wl.weights, e, world, bmax, h, cfg.combine_wire.value)[rank]
         hd = g.create_handle(wl.routing[rank])
         if mode == "bf16" and host_io:  # pinned host tokens: staged H2D (even rounds), read in place (odd)
-            _api._HOST_MAPPED_IN = rnd % 2 == 1
             xh = torch.from_numpy(wl.tokens[rank]).to(torch.bfloat16).pin_memory()
             inputs = [ep.tensor_from_torch(xh, T.TOKENS)]
         elif mode == "bf16":
@@ -64,11 +76,10 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
             inputs = [ep.tensor_from_f32(wl.tokens[rank], dtype, T.TOKENS)]
         out = ep.tensor_create((ell, world * bmax, h), ep.Dtype.F32, T.TOKENS)
         cnt = ep.tensor_create((ell, world), ep.Dtype.F32, T.RECV_EXPERT_COUNTER_HOST)
-        hd.dispatch(inputs, [out, cnt], send_only=staged)
-        if staged:
-            hd.complete()
-        if host_io:
-            _api._HOST_MAPPED_IN = False
+        with host_mapped_input(host_io and rnd % 2 == 1):
+            hd.dispatch(inputs, [out, cnt], send_only=staged)
+            if staged:
+                hd.complete()
         counts = cnt.read_f32()
         np.testing.assert_array_equal(counts, d[rank]["counts"])
         recv = out.read_f32()

@@ -11,7 +11,7 @@ from oracle import codecs as oc
 from oracle import ht as oht
 from oracle import ll as oll
 from oracle import workload as owl
-from paper_2603_13606_b200.harness import run_ranks
+from tests.rank_threads import run_ranks
 
 pytestmark = pytest.mark.gpu
 

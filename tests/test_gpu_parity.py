@@ -11,7 +11,7 @@ from oracle import ht as oht
 from oracle import ll as oll
 from oracle import workload as owl
 from tests._golden import HT_NAMES, LL_NAMES, ht_case, ll_case, load
-from paper_2603_13606_b200.harness import run_ranks
+from tests.rank_threads import run_ranks
 from tests.gpu_util import bf16_round, make_cfg, run_ht, run_ll
 
 pytestmark = pytest.mark.gpu
@@ -497,7 +497,11 @@ def test_allocation_hooks_back_the_window():
     out = ep.tensor_create((4, 3, 16), ep.Dtype.F32, ep.TensorTag.TOKENS)
     cnt = ep.tensor_create((4, 1), ep.Dtype.F32, ep.TensorTag.RECV_EXPERT_COUNTER_HOST)
     h.dispatch([tok], [out, cnt])
-    assert allocs[0][2].any()  # traffic landed in the hook storage
+    import ctypes
+    from paper_2603_13606_b200 import _lib
+    win, nb = ctypes.c_void_p(), ctypes.c_uint64()
+    _lib.call("epb_group_window", g._g, ctypes.byref(win), ctypes.byref(nb))
+    assert win.value == allocs[0][2].data_ptr() and nb.value == allocs[0][0]  # the hook storage is the window
     comb = ep.tensor_create((2, 16), ep.Dtype.F32, ep.TensorTag.TOKENS)
     h.combine([out, ep.tensor_from_f32(np.ones((2, 2), np.float32), ep.Dtype.F32, ep.TensorTag.TOPK_WEIGHTS)], [comb])
     np.testing.assert_array_equal(comb.read_f32(), np.full((2, 16), 2.0, np.float32))

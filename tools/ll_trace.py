@@ -18,9 +18,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2603_13606_b200 import _lib  # noqa: E402
 
-DISP = ["start", "seq", "routed", "stored", "published", "recv", "waited", "copied", "zeroed", "hdr",
-        "rt-loop", "t0-seq", "t0-arrive", "pass1"]
-COMB = ["start", "prefix", "sent", "published", "recv", "waited", "reduced"]
+# stamp indices of ll_dispatch_kernel / ll_combine_kernel (csrc/ll.cu LL_STAMP)
+DISP = ["start", "validated", "positioned", "tokens-done", "arrived", "recv", "", "recv-done", "routing-in",
+        "quantised(w1)", "prefix(w0)"]
+COMB = ["start", "prefix", "sent", "arrived", "recv", "fetched", "reduced"]
 
 
 def show(name, buf, labels):
