@@ -52,33 +52,54 @@ def expert_offsets(m, rank, e, n):
     return off.reshape(hi - lo, n)
 
 
+def dispatch_plan(routing, weights, e, n, d):
+    """Where every (src, token, k) routed to rank d lands in d's sorted
+    output (ht.py:553-583 order, offsets of ht.py:185-193): arrays
+    pos, e, src, t, k, w over those entries, plus recv_total and counts."""
+    ell = experts_per_rank(e, n)
+    m, _ = meta(routing, e, n)
+    off = expert_offsets(m, d, e, n)
+    cols = [[], [], [], [], [], []]
+    for s in range(n):
+        rt = np.asarray(routing[s], dtype=np.int64)
+        if rt.shape[0] == 0:
+            continue
+        ranks = expert_ranks(rt, e)
+        tt, kk = np.nonzero(rt // ell == d)
+        ee = rt[tt, kk]
+        cols[0].append(off[ee - d * ell, s] + ranks[tt, kk])
+        cols[1].append(ee)
+        cols[2].append(np.full(len(tt), s, dtype=np.int64))
+        cols[3].append(tt)
+        cols[4].append(kk)
+        cols[5].append(np.asarray(weights[s], dtype=np.float32)[tt, kk])
+    pos, ee, src, tt, kk = (np.concatenate(c) if c else np.zeros(0, np.int64) for c in cols[:5])
+    w = np.concatenate(cols[5]) if cols[5] else np.zeros(0, np.float32)
+    counts = np.zeros((ell, n), dtype=np.int64)
+    lo, hi = d * ell, min(d * ell + ell, e)
+    counts[:hi - lo] = m[:, lo:hi].T
+    return dict(pos=pos, e=ee, src=src, t=tt, k=kk, w=w, recv_total=recv_total(m, d, e, n), counts=counts)
+
+
 def dispatch(tokens, routing, weights, e, n, h, dtype):
     """Per destination rank dict(rows [R, H], origin [R, 5] as
     (e, src, t, k) int64 + w f32 column separately, counts [L, N])."""
-    ell = experts_per_rank(e, n)
     m, q = meta(routing, e, n)
     out = []
     for d in range(n):
-        total = recv_total(m, d, e, n)
-        off = expert_offsets(m, d, e, n)
+        pl = dispatch_plan(routing, weights, e, n, d)
+        total = pl["recv_total"]
         rows = np.zeros((total, h), dtype=np.float32)
         origin = np.zeros((total, 4), dtype=np.int64)
         wts = np.zeros((total,), dtype=np.float32)
+        pos = pl["pos"]
         for s in range(n):
-            rt = np.asarray(routing[s], dtype=np.int64)
-            if rt.shape[0] == 0:
-                continue
-            ranks = expert_ranks(rt, e)
-            tt, kk = np.nonzero(rt // ell == d)
-            ee = rt[tt, kk]
-            pos = off[ee - d * ell, s] + ranks[tt, kk]
-            rows[pos] = wire_roundtrip(tokens[s][tt], dtype, False)
-            origin[pos, 0], origin[pos, 1], origin[pos, 2], origin[pos, 3] = ee, s, tt, kk
-            wts[pos] = np.asarray(weights[s], dtype=np.float32)[tt, kk]
-        counts = np.zeros((ell, n), dtype=np.int64)
-        lo, hi = d * ell, min(d * ell + ell, e)
-        counts[:hi - lo] = m[:, lo:hi].T
-        out.append(dict(rows=rows, origin=origin, weights=wts, counts=counts,
+            sel = pl["src"] == s
+            if np.any(sel):
+                rows[pos[sel]] = wire_roundtrip(tokens[s][pl["t"][sel]], dtype, False)
+        origin[pos, 0], origin[pos, 1], origin[pos, 2], origin[pos, 3] = pl["e"], pl["src"], pl["t"], pl["k"]
+        wts[pos] = pl["w"]
+        out.append(dict(rows=rows, origin=origin, weights=wts, counts=pl["counts"],
                         recv_total=total))
     return out, m, q
 

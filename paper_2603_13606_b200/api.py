@@ -239,6 +239,13 @@ class EpGroup:
             buf = self._pinned_buf = torch.empty(max(n, 1024), dtype=torch.int32).pin_memory()
         return buf[:n]
 
+    def _on_stream(self):
+        """Context for a call's device work: the group's stream, ordered after
+        the caller's current stream (inputs the caller just produced) and
+        followed by it (outputs the caller consumes next).  A no-op when they
+        are the same stream (ProcessFabric, one emulated rank)."""
+        return _StreamScope(self.stream)
+
     def check(self) -> None:
         """Synchronise and raise any error the kernels recorded (timeouts,
         routing validation, weight mismatch).  The whole device is
@@ -299,7 +306,7 @@ class EpGroup:
         self._check_alive()
         routing = _validated_routing(topk_idx, self.config, self.device, snapshot=self.strict)
         handle = EpHandle(self, routing)
-        with torch.cuda.stream(self.stream):
+        with self._on_stream():
             if self.config.algorithm is Algorithm.HT:
                 handle._run_layout()
                 self._open_ht_round(handle)
@@ -343,6 +350,27 @@ class EpGroup:
         self.fabric.registered[self.rank] = 0
         if self._hooks is not None:
             self._hooks.release(self._buffer)
+
+
+class _StreamScope:
+    def __init__(self, stream):
+        self._s = stream
+        self._cur = None
+        self._ctx = None
+
+    def __enter__(self):
+        self._cur = torch.cuda.current_stream()
+        if self._cur != self._s:
+            self._s.wait_stream(self._cur)
+        self._ctx = torch.cuda.stream(self._s)
+        self._ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        self._ctx.__exit__(*exc)
+        if self._cur != self._s:
+            self._cur.wait_stream(self._s)
+        return False
 
 
 def _validated_routing(topk_idx, cfg: EpConfig, device, snapshot: bool = True) -> torch.Tensor:
@@ -626,7 +654,7 @@ class EpHandle:
         if ht:
             if not self._round_open:
                 # handle reuse (e.g. backward): a fresh collective round
-                with torch.cuda.stream(g.stream):
+                with g._on_stream():
                     g._open_ht_round(self)
             _expect_shape(out_tokens, (self._meta["recv_total"], cfg.hidden), "dispatch TOKENS output")
         else:
@@ -637,7 +665,7 @@ class EpHandle:
             _expect_shape(out_scales, tuple(out_tokens.shape[:-1]) + (cfg.hidden // FP8_BLOCK,),
                           "SCALES output")
 
-        with torch.cuda.stream(g.stream):
+        with g._on_stream():
             if ht:
                 self._ht_dispatch(tokens, weights, out_tokens, out_counts)
                 return
@@ -758,7 +786,7 @@ class EpHandle:
             _expect_shape(rows_in, (self._meta["recv_total"], cfg.hidden), "combine TOKENS input")
         else:
             _expect_shape(rows_in, (ell, n * cfg.max_tokens_per_rank, cfg.hidden), "combine TOKENS input")
-        with torch.cuda.stream(g.stream):
+        with g._on_stream():
             y = self._dev_in(rows_in)
             w = self._dev_in(wt)
             if ht:
@@ -849,14 +877,14 @@ class EpHandle:
         g = self.group
         g._check_alive()
         if self.state is HandleState.DISPATCH_STAGED:
-            with torch.cuda.stream(g.stream):
+            with g._on_stream():
                 g.fabric.phase(g.rank)
                 g._launch("epb_ll_dispatch:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
                           ctypes.byref(self._ll_args), self._sp())
                 self._ll_recv()
             return
         if self.state is HandleState.COMBINE_STAGED:
-            with torch.cuda.stream(g.stream):
+            with g._on_stream():
                 g.fabric.phase(g.rank)
                 g._launch("epb_ll_combine:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
                           ctypes.byref(self._ll_cargs), self._sp())

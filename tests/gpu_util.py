@@ -31,6 +31,8 @@ def dispatch_inputs(cfg, tokens, weights, mode="reference"):
     t = []
     if mode == "bf16":
         t.append(ep.tensor_from_f32(tokens, ep.Dtype.BF16, ep.TensorTag.TOKENS))
+    elif mode == "f32":  # f32 tokens quantised by the dispatch kernel (FP8 configs)
+        t.append(ep.tensor_from_f32(tokens, ep.Dtype.F32, ep.TensorTag.TOKENS))
     elif cfg.with_scales:
         codes, scales = oc.quantize_block(tokens)
         tok = ep.tensor_create(codes.shape, ep.Dtype.FP8, ep.TensorTag.TOKENS)
@@ -92,7 +94,8 @@ def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="referen
                 hd.combine(comb_in, [comb_out], send_only=staged)
                 if staged:
                     hd.complete()
-                res.append(dict(recv=recv, counts=counts, out=comb_out.read_f32(),
+                raw = dict(recv_raw=out_tok.raw(), scales_raw=outs[1].raw()) if wire_out and cfg.with_scales else {}
+                res.append(dict(recv=recv, counts=counts, out=comb_out.read_f32(), **raw,
                                 recv_total=hd.get_num_recv_tokens(), rows=rows,
                                 dstats=hd.dispatch_result.stats, cstats=hd.combine_stats))
                 hd.destroy()
