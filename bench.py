@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-extra", action="store_true", help="skip the C4/C5 configs (extra_configs key)")
     p.add_argument("--cpu-sample-steps", type=int, default=3)
     p.add_argument("--no-sweep", action="store_true", help="skip the LL token sweep 1..128 (ll_sweep_us key)")
+    p.add_argument("--ll-zero-copy", action="store_true",
+                   help="LL expert outputs in the registered window: the combine pulls them (default: pushed)")
     return p.parse_args()
 
 
@@ -176,7 +178,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 class LLStep:
-    def __init__(self, world, rank, b, seed=0, shape=None, zipf=False):
+    def __init__(self, world, rank, b, seed=0, shape=None, zipf=False, zero_copy=False):
         import torch
 
         import paper_2603_13606_b200 as ep
@@ -185,8 +187,11 @@ class LLStep:
         self.world, self.rank, self.b = world, rank, b
         E, K, H = shape or (globals()["E"], globals()["K"], globals()["H"])
         self.E, self.K, self.H = E, K, H
+        # zero_copy: the expert outputs live in the group's registered window
+        # (EpHandle.expert_out_buffer); the combine pulls them over NVLink
         self.cfg = ep.EpConfig(ep.Algorithm.LL, world, world, E, K, H, b, ep.Dtype.FP8, True,
-                               combine_dtype=ep.Dtype.BF16)
+                               combine_dtype=ep.Dtype.BF16, expert_out_window=zero_copy)
+        self.zero_copy = zero_copy
         self.g = make_group(world, rank, self.cfg, strict=False)
         wl = (owl.make_zipf_workload if zipf else owl.make_workload)(E, world, b, K, H, seed)
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -201,6 +206,10 @@ class LLStep:
         gen = torch.Generator(device=dev)
         gen.manual_seed(1234 + rank)
         self.y = torch.randn((L, world * b, H), dtype=torch.float32, device=dev, generator=gen).to(torch.bfloat16)
+        if zero_copy:
+            yw = self.g.expert_out_view(L * world * b).view(L, world * b, H)
+            yw.copy_(self.y)
+            self.y = yw
         self.out = torch.zeros((b, H), dtype=torch.bfloat16, device=dev)
         T = ep.TensorTag
         self.X = ep.tensor_from_torch(self.x, T.TOKENS)
@@ -376,7 +385,7 @@ def steps_per_graph(steps):
 def run_ll(args, world, rank, shape=None, zipf=False, light=False):
     """`light`: only the timed step graph (returns step ms; the sweep)."""
     import torch
-    st = LLStep(world, rank, args.tokens, shape=shape, zipf=zipf)
+    st = LLStep(world, rank, args.tokens, shape=shape, zipf=zipf, zero_copy=getattr(args, "ll_zero_copy", False))
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     S = steps_per_graph(args.steps)
     graph, per_step = capture_steps(st, st.g, S, flush, phases=False)

@@ -37,6 +37,20 @@ EPB_DEV void fence_release(bool sys) {
   if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
   else asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+// Stress mode (EPB_CHAOS_NS > 0): a pseudo-random __nanosleep in [0, ns)
+// before payload stores and before releases, so CTAs, warps and ranks
+// interleave differently every round (the analogue of the reference
+// fabric's seeded delivery reordering, fabric.py:203-245).
+EPB_DEV void chaos_delay(uint32_t ns, uint32_t salt) {
+  if (ns == 0) return;
+  uint32_t x;
+  asm volatile("mov.u32 %0, %%clock;" : "=r"(x));
+  x ^= salt * 0x9E3779B9u + (blockIdx.x << 16) + threadIdx.x;
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  __nanosleep(x % ns);
+}
 EPB_DEV uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

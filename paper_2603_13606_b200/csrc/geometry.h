@@ -47,6 +47,7 @@ struct LLGeom {
   uint64_t barrier;  // [N] u64 device-barrier flags (after both parities)
   uint64_t yout, yout_rows, yrow;  // registered expert-output region [L][N*B] bf16 rows (expert_out_window)
   int sys_fence;                   // release fences at system scope (peers on other GPUs)
+  uint32_t chaos_ns;               // stress mode: random delays before stores / releases (EPB_CHAOS_NS)
 };
 
 // HT:
@@ -61,7 +62,8 @@ struct HTGeom {
   int RB, RBp, WBp, HBp, rec_stride, crow_stride;
   uint64_t meta, meta_flag, dflag, cflag, stage, rec, crow;
   uint64_t yout, yout_rows, yrow;  // registered expert-output region (expert_out_window)
-  int sys_fence;                   // release fences at system scope (EPB_SYS_FENCE=1)
+  int sys_fence;                   // release fences at system scope (peers on other GPUs)
+  uint32_t chaos_ns;               // stress mode: random delays before stores / releases (EPB_CHAOS_NS)
   uint64_t window_bytes, logical_bytes;
   uint64_t barrier;  // [N] u64 device-barrier flags
 };

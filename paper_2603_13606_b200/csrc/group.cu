@@ -148,6 +148,8 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
     g->fence_override = f ? (atoi(f) != 0 ? 1 : 0) : -1;
     g->ll.sys_fence = g->ht.sys_fence = g->fence_override == 1 ? 1 : 0;
   }
+  g->ll.chaos_ns = g->ht.chaos_ns = 0;
+  if (const char* c = getenv("EPB_CHAOS_NS")) g->ll.chaos_ns = g->ht.chaos_ns = (uint32_t)strtoul(c, nullptr, 10);
   // LL grid (identical on every rank: receivers count one arrival per
   // source CTA); EPB_LL_CTAS < 148 leaves SMs free for concurrent compute
   if (const char* c = getenv("EPB_LL_CTAS")) {

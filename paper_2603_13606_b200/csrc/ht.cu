@@ -73,11 +73,13 @@ __global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
     reinterpret_cast<int32_t*>(hpeer(p.peers, d) + row_off)[c] = v;
   }
   __syncthreads();
-  if ((int)threadIdx.x < g.N) {
-    fence_release(p.g.sys_fence);
-    uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, threadIdx.x) + g.meta_flag) +
-                     p.parity * g.N + p.rank;
-    st_relaxed_sys_u64(flag, (uint64_t)p.tag);
+  if (threadIdx.x == 0) {
+    chaos_delay(g.chaos_ns, 0x41u);
+    fence_release(g.sys_fence);  // one release covers every thread's row stores
+    for (int d = 0; d < g.N; ++d) {
+      uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, d) + g.meta_flag) + p.parity * g.N + p.rank;
+      st_relaxed_sys_u64(flag, (uint64_t)p.tag);
+    }
   }
 }
 
@@ -257,15 +259,18 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) 
     }
   }
   (void)L;
-  // (3) publish: the last CTA (stage rows and records of every CTA done)
+  // (3) publish: every CTA releases its stage rows and records at GPU scope
+  // and counts in; the last one issues the rank's single system-scope
+  // release (cumulative over all CTAs' stores) and flags every destination
   __syncthreads();
-  if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
-    const int d = threadIdx.x;
-    fence_release(p.g.sys_fence);
-    if (atomicAdd(&p.done[d], 1) == (int)gridDim.x - 1) {
-      p.done[d] = 0;
+  if (threadIdx.x == 0) {
+    chaos_delay(g.chaos_ns, 0x33u);
+    fence_release(false);
+    if (atomicAdd(p.done, 1) == (int)gridDim.x - 1) {
+      *p.done = 0;
       fence_release(p.g.sys_fence);
-      ht_publish_records(p, d);
+      for (int d = 0; d < N; ++d)
+        if (d != me) ht_publish_records(p, d);
     }
   }
 }
@@ -580,12 +585,10 @@ EPB_DEV void ht_publish_comb(const HTCombSend& p, int s, int count) {
 
 template <int IT>
 __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend p) {
-  __shared__ int s_cnt[kMaxRanks];
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H;
   const int me = p.rank;
   if (*reinterpret_cast<const volatile int*>(p.err) != 0) return;
-  if ((int)threadIdx.x < N) s_cnt[threadIdx.x] = 0;
   constexpr int ib = IT == EPB_F32 ? 4 : 2;
   const int bytes = H * ib;
   if (p.row_ptr) {
@@ -605,9 +608,10 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
   if (p.pull) {
     // nothing moves: announce that this rank's expert rows are complete
     // (written by earlier kernels on this stream) to every home rank
-    if (blockIdx.x == 0 && (int)threadIdx.x < N && (int)threadIdx.x != me) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       fence_release(p.g.sys_fence);
-      ht_publish_comb(p, threadIdx.x, 0);
+      for (int s2 = 0; s2 < N; ++s2)
+        if (s2 != me) ht_publish_comb(p, s2, 0);
     }
     return;
   }
@@ -643,23 +647,18 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
       for (int c = lane; c < bytes / 2; c += 32)
         reinterpret_cast<uint16_t*>(dst)[c] = reinterpret_cast<const uint16_t*>(src)[c];
     }
-    if (lane == 0 && half == 0) atomicAdd(&s_cnt[s], 1);
   }
+  // publish: one GPU-scope release per CTA, the last CTA's system-scope
+  // release covers them all, then every home rank is flagged
   __syncthreads();
-  if ((int)threadIdx.x < N && (int)threadIdx.x != me) {
-    const int s = threadIdx.x;
-    const int c = s_cnt[s];
-    const int want = ht_rows_to(p, s);
-    if (c > 0) {
+  if (threadIdx.x == 0) {
+    chaos_delay(g.chaos_ns, 0x35u);
+    fence_release(false);
+    if (atomicAdd(p.done, 1) == (int)gridDim.x - 1) {
+      *p.done = 0;
       fence_release(p.g.sys_fence);
-      const int old = atomicAdd(&p.done[s], c);
-      if (old + c == want) {
-        p.done[s] = 0;
-        fence_release(p.g.sys_fence);
-        ht_publish_comb(p, s, want);
-      }
-    } else if (blockIdx.x == 0 && want == 0) {
-      ht_publish_comb(p, s, 0);
+      for (int s2 = 0; s2 < N; ++s2)
+        if (s2 != me) ht_publish_comb(p, s2, ht_rows_to(p, s2));
     }
   }
 }

@@ -96,9 +96,10 @@ EPB_DEV bool wait_arrivals(const uint64_t* c, uint64_t need, bool sys, uint64_t 
 // per CTA (concurrent system-scope fences from every SM measured several us).
 // All threads call.  `done`: this kind's local counter (reset by the last).
 EPB_DEV void ll_arrive(const uint64_t* peers, uint64_t off, int N, int me, bool fence_sys, bool sys,
-                       unsigned* done) {
+                       unsigned* done, uint32_t chaos_ns) {
   __syncthreads();
   if (threadIdx.x == 0 && N > 1) {
+    chaos_delay(chaos_ns, 0x51u);
     fence_release(false);
     if (atomicAdd(done, 1u) == gridDim.x - 1) {
       *done = 0u;  // next use is a later kernel (stream order)
@@ -517,6 +518,7 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
       __syncthreads();
     }
     if (!has || bad) break;
+    chaos_delay(g.chaos_ns, 0x17u + it);
     LL_STAMP(p, 10);
     // destinations of token t (every warp derives them): lanes k < K
     int e = -1, d = -1, ci = 0, cj = 0;
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     if (p.phases & kPhaseSend) {
       const bool bad = ll_send_fast<XT, WT, SC, OT>(p, smem, seq_ld, seq, parity_off);
       // publish: one system-scope release per rank, one arrival per destination
-      ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done);
+      ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns);
       LL_STAMP(p, 4);
       if (bad) return;
     }
@@ -999,7 +1001,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       if (bad && threadIdx.x == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
     }
     // publish: one release per CTA, one arrival per destination
-    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done);
+    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns);
     LL_STAMP(p, 4);
     if (bad) return;
   }
@@ -1252,6 +1254,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     LL_STAMP(p, 1);
     const int total = s_pre[P];
     const int part = (nch + kParts - 1) / kParts;
+    chaos_delay(g.chaos_ns, 0x2Bu);
     const int tasks = vec ? total * kParts : total;
     for (int task = blockIdx.x * nw + warp; task < tasks; task += gridDim.x * nw) {
       const int r = vec ? task / kParts : task;
@@ -1305,7 +1308,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // one release per CTA, one arrival per home rank (pulled combine: the
     // expert outputs were written by earlier kernels on this stream — the
     // arrival announces them)
-    ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done);
+    ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns);
     LL_STAMP(p, 3);
   }
 

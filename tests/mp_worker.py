@@ -204,6 +204,111 @@ def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert, zero_copy=False):
     g.destroy()
 
 
+def ll_stress(world, rank, rounds):
+    """`rounds` back-to-back LL rounds (C2 path: bf16 -> FP8 + scales, bf16
+    combine) on one handle per round, every round checked bit-for-bit on the
+    device against oracle-derived expectations; mismatches accumulate on the
+    device and are read once at the end.  Run under EPB_CHAOS_NS the kernels
+    sleep a random time before stores and releases (test_acceptance.py:286-292
+    analogue: ordering must not depend on timing)."""
+    e, k, h, b = 256, 8, 7168, 64
+    cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, b, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
+    fab = ep.ProcessFabric(ep.NodeTopology(world, world))
+    g = ep.create_group(fab, rank, cfg, strict=False)
+    wl = owl.make_workload(e, world, b, k, h, 90)
+    wl.tokens = [bf16r(t) for t in wl.tokens]
+    d = oll.dispatch(wl.tokens, wl.routing, e, world, b, h, "fp8", True)
+    ys = [bf16r(oll.apply_experts(d[r]["recv"], d[r]["counts"], r, e, world, b, owl.expert_scale))
+          for r in range(world)]
+    want = torch.from_numpy(oll.combine(ys, wl.routing, wl.weights, e, world, b, h, "bf16")[rank]).cuda()
+    ell = cfg.experts_per_rank
+    codes, scales = oc.quantize_block(np.concatenate(wl.tokens))
+    plan = d[rank]["plan"]
+    rows = torch.from_numpy(plan[:, 0] * (world * b) + plan[:, 1] * b + plan[:, 2]).cuda()
+    gtok = torch.from_numpy(plan[:, 1] * b + plan[:, 3]).cuda()  # source row in the concatenated batch
+    want_codes = torch.from_numpy(codes).cuda()[gtok]
+    want_scales = torch.from_numpy(scales).cuda()[gtok]
+    want_cnt = torch.from_numpy(d[rank]["counts"].astype(np.float32)).cuda()
+    x = torch.from_numpy(wl.tokens[rank]).cuda().to(torch.bfloat16)
+    topk = torch.from_numpy(wl.routing[rank]).cuda()
+    w = torch.from_numpy(wl.weights[rank]).cuda()
+    y = torch.from_numpy(ys[rank]).cuda().to(torch.bfloat16)
+    recv = torch.zeros((ell, world * b, h), dtype=torch.uint8, device="cuda")
+    rsc = torch.zeros((ell, world * b, h // 128), dtype=torch.float32, device="cuda")
+    cnt = torch.zeros((ell, world), dtype=torch.float32, device="cuda")
+    out = torch.zeros((b, h), dtype=torch.float32, device="cuda")
+    X, W, Y = ep.tensor_from_torch(x, T.TOKENS), ep.tensor_from_torch(w, T.TOPK_WEIGHTS), ep.tensor_from_torch(y, T.TOKENS)
+    outs = [ep.tensor_from_torch(recv, T.TOKENS), ep.tensor_from_torch(rsc, T.SCALES),
+            ep.tensor_from_torch(cnt, T.RECV_EXPERT_COUNTER_DEVICE)]
+    OUT = ep.tensor_from_torch(out, T.TOKENS)
+    bad = torch.zeros(4, dtype=torch.int64, device="cuda")
+    for rnd in range(rounds):
+        hd = g.create_handle(topk)
+        hd.dispatch([X], outs, send_only=(rnd % 3 == 1))
+        if rnd % 3 == 1:
+            hd.complete()
+        flat = recv.view(-1, h)
+        bad[0] += (flat[rows] != want_codes).any(1).sum()
+        bad[1] += (rsc.view(-1, h // 128)[rows] != want_scales).any(1).sum()
+        bad[2] += (cnt != want_cnt).sum()
+        hd.combine([Y, W], [OUT], send_only=(rnd % 3 == 2))
+        if rnd % 3 == 2:
+            hd.complete()
+        bad[3] += (out.view(torch.int32) != want.view(torch.int32)).any(1).sum()
+        hd.destroy()
+        recv.zero_()
+        out.zero_()
+    g.check()
+    res = bad.cpu().tolist()
+    print(f"rank {rank}: ll stress {rounds} rounds, mismatching (rows, scale rows, counts, tokens) = {res}", flush=True)
+    assert res == [0, 0, 0, 0], res
+    g.destroy()
+
+
+def ht_stress(world, rank, rounds):
+    """HT rounds (4096 tokens would be slow in Python per round; 512 tokens,
+    DeepSeek-like E=64, K=8, H=2048) under EPB_CHAOS_NS, bit-exact every
+    round on the device."""
+    e, k, h, b = 64, 8, 2048, 512
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, e, k, h, b, ep.Dtype.BF16, expert_out_window=True)
+    fab = ep.ProcessFabric(ep.NodeTopology(world, world))
+    g = ep.create_group(fab, rank, cfg, strict=False)
+    wl = owl.make_workload(e, world, b, k, h, 91)
+    wl.tokens = [bf16r(t) for t in wl.tokens]
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, e, world, h, "bf16")
+    ys = [bf16r(oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_scale)) for r in range(world)]
+    want = torch.from_numpy(oht.combine(ys, wl.routing, wl.weights, e, world, world)[rank]).cuda()
+    want_rows = torch.from_numpy(dd[rank]["rows"]).cuda().to(torch.bfloat16)
+    x = torch.from_numpy(wl.tokens[rank]).cuda().to(torch.bfloat16)
+    topk = torch.from_numpy(wl.routing[rank]).cuda()
+    w = torch.from_numpy(wl.weights[rank]).cuda()
+    y = torch.from_numpy(ys[rank]).cuda().to(torch.bfloat16)
+    tot = dd[rank]["recv_total"]
+    recv = torch.zeros((tot, h), dtype=torch.bfloat16, device="cuda")
+    cnt = torch.zeros((cfg.experts_per_rank, world), dtype=torch.float32, device="cuda")
+    out = torch.zeros((b, h), dtype=torch.float32, device="cuda")
+    X, W = ep.tensor_from_torch(x, T.TOKENS), ep.tensor_from_torch(w, T.TOPK_WEIGHTS)
+    outs = [ep.tensor_from_torch(recv, T.TOKENS), ep.tensor_from_torch(cnt, T.TOKENS_PER_EXPERTS)]
+    OUT = ep.tensor_from_torch(out, T.TOKENS)
+    bad = torch.zeros(2, dtype=torch.int64, device="cuda")
+    for rnd in range(rounds):
+        hd = g.create_handle(topk)
+        hd.dispatch([X, W], outs)
+        bad[0] += (recv.view(torch.int16) != want_rows.view(torch.int16)).any(1).sum()
+        yb = hd.expert_out_buffer()
+        yb.copy_(y)
+        hd.combine([ep.tensor_from_torch(yb, T.TOKENS), W], [OUT])
+        bad[1] += (out.view(torch.int32) != want.view(torch.int32)).any(1).sum()
+        hd.destroy()
+        recv.zero_()
+        out.zero_()
+    g.check()
+    res = bad.cpu().tolist()
+    print(f"rank {rank}: ht stress {rounds} rounds, mismatching (rows, tokens) = {res}", flush=True)
+    assert res == [0, 0], res
+    g.destroy()
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -233,6 +338,12 @@ def main():
         ("ht zero-copy combine (pull)", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 8, True, zero_copy=True)),
         ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
     ]
+    stress = int(os.environ.get("EPB_MP_STRESS", "0"))
+    if stress:
+        cases = [(f"ll stress {stress} rounds (chaos {os.environ.get('EPB_CHAOS_NS', '0')} ns)",
+                  lambda: ll_stress(world, rank, stress)),
+                 (f"ht stress {max(1, stress // 20)} rounds (chaos {os.environ.get('EPB_CHAOS_NS', '0')} ns)",
+                  lambda: ht_stress(world, rank, max(1, stress // 20)))]
     failures = []
     for name, fn in cases:
         try:
