@@ -9,20 +9,23 @@ scales inside the dispatch kernel, bf16 combine; the rank is its own peer
 and experts are block-placed over the ranks; traffic crosses NVLink through
 CUDA-IPC windows.
 
-One step = create_handle (routing layout) + dispatch (send + recv) +
-combine (send + recv), captured once as a CUDA graph and replayed; the L2
-is flushed (256 MB memset) before every step outside the timed events.
-value = mean device time per step in microseconds (max over ranks).
+One step = create_handle (routing snapshot) + dispatch (send + recv) +
+combine (send + recv) through the public API, captured in a CUDA graph and
+replayed; the L2 is flushed (256 MB memset) and all ranks are aligned by a
+device barrier before every step, outside the timed events.  value = mean
+device time per step in microseconds (max over ranks).  After timing, the
+last replayed step's outputs are checked against the CPU oracle ("parity").
 
-Extra keys: `ht` (configs[2]: 4096 tokens/rank HT dispatch/combine, GB/s),
-`e2e` (the same LL step through the public API with host buffers),
-`roofline` (dominant kernel vs measured HBM copy bandwidth), `cpu_baseline`
-(the CPU oracle port on a bounded sample), `clocks` (NVML during the run).
+Extra keys: `ht` (configs[2]: 4096 tokens/rank HT dispatch/combine, GB/s,
+parity-checked), `e2e` (the LL step through the public API with host
+buffers), `roofline` (dominant kernel; N=1 latency-bound against a measured
+two-kernel floor, N>1 NVLink bytes against 770 GB/s), `cpu_baseline` (the
+CPU oracle port on a bounded sample), `clocks` (NVML during the run).
 
 `--impl reference` times the reference algorithm's CPU restatement
 (oracle/, the only executable form of the Python reference on the GPU box)
-on the same config and prints the same line with "impl": "reference",
-using every usable host core (concurrent oracle rounds in forked processes).
+on the same config with every usable host core and prints the same line with
+"impl": "reference".
 """
 
 from __future__ import annotations
@@ -42,6 +45,7 @@ import numpy as np  # noqa: E402
 
 E, K, H = 256, 8, 7168          # DeepSeek-V3 (BASELINE.json configs[1], [2])
 METRIC = "LL dispatch+combine µs @128 tok; HT dispatch/combine GB/s/GPU at 8×B200"
+NVLINK_GBPS = 770.0             # B200_PROFILING.md: measured peer copy per direction (900 nominal)
 
 
 def parse():
@@ -56,12 +60,23 @@ def parse():
     p.add_argument("--no-ht", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed step")
     p.add_argument("--no-extra", action="store_true", help="skip the C4/C5 configs (extra_configs key)")
     p.add_argument("--cpu-sample-steps", type=int, default=3)
     p.add_argument("--no-sweep", action="store_true", help="skip the LL token sweep 1..128 (ll_sweep_us key)")
     p.add_argument("--ll-zero-copy", action="store_true",
-                   help="LL expert outputs in the registered window: the combine pulls them (default: pushed)")
+                   help="headline LL step with the expert outputs in the registered window (pulled combine)")
     return p.parse_args()
+
+
+def workload_config(args, world) -> dict:
+    """The measured workload — identical on both arms."""
+    return {"workload": "configs[1] LL decode step: create_handle + dispatch + combine, DeepSeek-V3 shapes",
+            "experts": E, "top_k": K, "hidden": H, "tokens_per_rank": args.tokens, "ranks": world,
+            "parallelism": f"ep{world}", "dispatch": "bf16 tokens -> FP8 e4m3 + f32 block-128 scales",
+            "combine": "bf16 expert rows and wire, f32 accumulate (ascending k)",
+            "routing": "uniform distinct top-8 (oracle.make_workload, seed 0)",
+            "l2": "flushed (256 MB memset) before every step"}
 
 
 # ---------------------------------------------------------------------------
@@ -90,6 +105,10 @@ def allreduce_max(v: float, world: int) -> float:
     t = torch.tensor([v], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def allreduce_min(v: float, world: int) -> float:
+    return -allreduce_max(-v, world)
 
 
 def allgather_f(v: float, world: int) -> list:
@@ -174,6 +193,20 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# the synthetic expert: x * 2^((e % 3) - 1) — exact in bf16, so the checker
+# knows every expert output the combine reduces
+# ---------------------------------------------------------------------------
+
+def pow2_np(e):
+    return np.float32(2.0) ** ((np.asarray(e, dtype=np.int64) % 3) - 1).astype(np.float32)
+
+
+def pow2_torch(e):
+    import torch
+    return torch.exp2(((e.long() % 3) - 1).float())
+
+
+# ---------------------------------------------------------------------------
 # LL decode step (configs[1])
 # ---------------------------------------------------------------------------
 
@@ -185,143 +218,110 @@ class LLStep:
         from oracle import workload as owl
         self.ep, self.torch = ep, torch
         self.world, self.rank, self.b = world, rank, b
-        E, K, H = shape or (globals()["E"], globals()["K"], globals()["H"])
-        self.E, self.K, self.H = E, K, H
+        E_, K_, H_ = shape or (E, K, H)
+        self.E, self.K, self.H = E_, K_, H_
         # zero_copy: the expert outputs live in the group's registered window
         # (EpHandle.expert_out_buffer); the combine pulls them over NVLink
-        self.cfg = ep.EpConfig(ep.Algorithm.LL, world, world, E, K, H, b, ep.Dtype.FP8, True,
+        self.cfg = ep.EpConfig(ep.Algorithm.LL, world, world, E_, K_, H_, b, ep.Dtype.FP8, True,
                                combine_dtype=ep.Dtype.BF16, expert_out_window=zero_copy)
         self.zero_copy = zero_copy
         self.g = make_group(world, rank, self.cfg, strict=False)
-        wl = (owl.make_zipf_workload if zipf else owl.make_workload)(E, world, b, K, H, seed)
+        self.wl = (owl.make_zipf_workload if zipf else owl.make_workload)(E_, world, b, K_, H_, seed)
         dev = torch.device("cuda", torch.cuda.current_device())
         L = self.cfg.experts_per_rank
-        self.x = torch.from_numpy(wl.tokens[rank]).to(dev).to(torch.bfloat16)
-        self.topk = torch.from_numpy(wl.routing[rank]).to(dev)
-        self.w = torch.from_numpy(wl.weights[rank]).to(dev)
-        self.routing_h = wl.routing[rank]
-        self.recv = torch.zeros((L, world * b, H), dtype=torch.uint8, device=dev)
-        self.recv_sc = torch.zeros((L, world * b, H // 128), dtype=torch.float32, device=dev)
+        self.x = torch.from_numpy(self.wl.tokens[rank]).to(dev).to(torch.bfloat16)
+        self.topk = torch.from_numpy(self.wl.routing[rank]).to(dev)
+        self.w = torch.from_numpy(self.wl.weights[rank]).to(dev)
+        self.recv = torch.zeros((L, world * b, H_), dtype=torch.uint8, device=dev)
+        self.recv_sc = torch.zeros((L, world * b, H_ // 128), dtype=torch.float32, device=dev)
         self.cnt = torch.zeros((L, world), dtype=torch.float32, device=dev)
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(1234 + rank)
-        self.y = torch.randn((L, world * b, H), dtype=torch.float32, device=dev, generator=gen).to(torch.bfloat16)
-        if zero_copy:
-            yw = self.g.expert_out_view(L * world * b).view(L, world * b, H)
-            yw.copy_(self.y)
-            self.y = yw
-        self.out = torch.zeros((b, H), dtype=torch.bfloat16, device=dev)
+        self.out = torch.zeros((b, H_), dtype=torch.bfloat16, device=dev)
         T = ep.TensorTag
         self.X = ep.tensor_from_torch(self.x, T.TOKENS)
         self.RECV = ep.tensor_from_torch(self.recv, T.TOKENS)
         self.RECV_SC = ep.tensor_from_torch(self.recv_sc, T.SCALES)
         self.CNT = ep.tensor_from_torch(self.cnt, T.RECV_EXPERT_COUNTER_DEVICE)
-        self.Y = ep.tensor_from_torch(self.y, T.TOKENS)
         self.W = ep.tensor_from_torch(self.w, T.TOPK_WEIGHTS)
         self.OUT = ep.tensor_from_torch(self.out, T.TOKENS)
+        # the expert outputs: one real dispatch, then y = dequant(row) * 2^((e%3)-1)
+        # in bf16 (exact) for every row of local expert l (e = rank*L + l)
+        if zero_copy:
+            self.y = self.g.expert_out_view(L * world * b).view(L, world * b, H_)
+        else:
+            self.y = torch.zeros((L, world * b, H_), dtype=torch.bfloat16, device=dev)
+        h = self.g.create_handle(self.topk)
+        h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT])
+        deq = self.recv.view(torch.float8_e4m3fn).float().view(L, world * b, H_ // 128, 128) * \
+            self.recv_sc[..., None]
+        eids = torch.arange(L, device=dev) + rank * L
+        self.y.copy_((deq.view(L, world * b, H_) * pow2_torch(eids)[:, None, None]).to(torch.bfloat16))
+        self.Y = ep.tensor_from_torch(self.y, T.TOKENS)
+        h.combine([self.Y, self.W], [self.OUT])
+        h.destroy()
+        torch.cuda.synchronize()
 
     def step(self, upto="combine"):
-        """One LL step; `upto` truncates it ("dispatch", "handle") for the
-        marginal per-kernel timing in run_ll."""
+        """One LL step; "handle" = create_handle only, "staged" = the
+        send_only + complete() form of both ops (api.py:445-451, :521-540)."""
         h = self.g.create_handle(self.topk)
-        if upto == "staged":  # send / complete split (api.py:445-451, :521-540)
+        if upto == "staged":
             h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT], send_only=True)
             h.complete()
             h.combine([self.Y, self.W], [self.OUT], send_only=True)
             h.complete()
-            h.destroy()
-            return
-        if upto != "handle":  # (every dispatch is combined: the arrival protocol counts rounds)
+        elif upto != "handle":  # (every dispatch is combined: the arrival protocol counts rounds)
             h.dispatch([self.X], [self.RECV, self.RECV_SC, self.CNT])
             h.combine([self.Y, self.W], [self.OUT])
         h.destroy()
 
+    def parity(self) -> dict:
+        """The last step's outputs on this rank against the CPU oracle
+        (oracle/ll.py, pinned to the reference by tests/golden): counts,
+        every received row's FP8 codes and block scales at its (l, src, i)
+        position, and the combine output."""
+        import torch
+        from oracle import codecs as oc
+        from oracle import ll as oll
+        wl, E_, H_, b, n, me = self.wl, self.E, self.H, self.b, self.world, self.rank
+        tok = [oc.bf16_to_f32(oc.f32_to_bf16(t)) for t in wl.tokens]  # the bf16 tokens dispatched
+        plan, counts = oll.dispatch_plan(wl.routing, E_, n, me)
+        res = {"counts": bool(np.array_equal(self.cnt.cpu().numpy(), counts))}
+        codes_ok = scales_ok = True
+        dev = self.recv.device
+        for s in range(n):
+            sel = plan[plan[:, 1] == s]
+            if not len(sel):
+                continue
+            c, sc = oc.quantize_block(tok[s][sel[:, 3]])
+            rows = torch.from_numpy(sel[:, 0] * (n * b) + sel[:, 1] * b + sel[:, 2]).to(dev)
+            codes_ok &= torch.equal(self.recv.view(-1, H_)[rows], torch.from_numpy(c).to(dev))
+            scales_ok &= torch.equal(self.recv_sc.view(-1, H_ // 128)[rows].view(torch.int32),
+                                     torch.from_numpy(sc).to(dev).view(torch.int32))
+        res["rows_fp8_codes"] = bool(codes_ok)
+        res["rows_scales"] = bool(scales_ok)
+        wire = oc.wire_roundtrip(tok[me], "fp8", True)
+        want = oll.combine_scaled_experts(wire, wl.routing[me], wl.weights[me], pow2_np, "bf16")
+        got = self.out.float().cpu().numpy()
+        res["combine"] = bool(np.array_equal(got, oc.bf16_to_f32(oc.f32_to_bf16(want))))
+        res["ok"] = all(res.values())
+        return res
+
     # algorithmic bytes per kernel launch (this rank), headers not credited
     def algo_bytes(self):
-        E, K, H = self.E, self.K, self.H
+        E_, K_, H_ = self.E, self.K, self.H
         L = self.cfg.experts_per_rank
-        owner = self.routing_h // L
-        dst_per_tok = np.array([len(set(r)) for r in owner]) if self.b else np.zeros(0)
-        row8 = H + 4 * (H // 128)
-        sent = int(dst_per_tok.sum())
-        recv_rows = int(self.b * K)  # balanced estimate; exact value below for N=1
-        if self.world == 1:
-            recv_rows = int(self.b * K)
-            arrive = sent
-        else:
-            arrive = sent  # symmetric workload: what a rank receives ~ what it sends
+        owner = self.wl.routing[self.rank] // L
+        row8 = H_ + 4 * (H_ // 128)
+        recv_rows = int(self.cnt.sum().item())
         # compulsory HBM bytes per launch (DESIGN.md §4): dispatch = read the
         # bf16 tokens + routing, write the FP8 expert-major rows + scales;
-        # combine = read the bf16 expert rows + weights, write the bf16 output.
-        # Slot traffic in the window is an intermediate (L2-resident at N=1).
-        del sent, arrive
-        return {
-            "epb_routing_layout": self.b * K * 8 + self.b * (K + self.world) * 4 + (E + self.world) * 4,
-            "epb_ll_dispatch": self.b * H * 2 + self.b * K * 8 + recv_rows * row8,
-            "epb_ll_combine": recv_rows * H * 2 + self.b * K * 4 + self.b * H * 2,
-        }, {"dispatch_remote": int(sum(len(set(r) - {self.rank}) for r in owner)) * row8,
-            "combine_remote": int((owner != self.rank).sum()) * H * 2}
-
-
-def capture(step_obj, group, phases: bool, warmup_eager=3):
-    """One CUDA graph of a whole step between two timing events; with
-    `phases`, every kernel launch inside is also preceded by an event."""
-    import torch
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        for _ in range(warmup_eager):
-            step_obj.step()
-    torch.cuda.current_stream().wait_stream(s)
-    torch.cuda.synchronize()
-    marks = []
-    graph = torch.cuda.CUDAGraph()
-    group.trace_phases(marks)
-    with torch.cuda.graph(graph):
-        group.mark("step:start")
-        if not phases:
-            group.trace_phases(None)
-        step_obj.step()
-        group.trace_phases(marks)
-        group.mark("step:end")
-    group.trace_phases(None)
-    torch.cuda.synchronize()
-    return graph, marks
-
-
-def replay_timed(graph, marks, steps, flush, sync_each=False, align=None):
-    """Replay `steps` times back to back, the L2 flushed before each step
-    outside the timed events.  Without `sync_each` the host never waits
-    between steps (per-step events are recorded around each replay on the
-    stream), so ranks stay aligned by the exchange itself instead of by host
-    jitter.  With `sync_each` the in-graph phase events are read after every
-    replay.  Returns (total ms, {phase: ms})."""
-    import torch
-    names = [m[0] for m in marks]
-    phase = {n: 0.0 for n in names[:-1]}
-    if not sync_each:
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        for a, b in evs:
-            flush.zero_()
-            if align is not None:
-                align()  # device barrier of all ranks, outside the timed events
-            a.record()
-            graph.replay()
-            b.record()
-        torch.cuda.synchronize()
-        return sum(a.elapsed_time(b) for a, b in evs), phase
-    total = 0.0
-    for _ in range(steps):
-        flush.zero_()
-        if align is not None:
-            align()
-        graph.replay()
-        torch.cuda.synchronize()
-        evs = [m[1] for m in marks]
-        total += evs[0].elapsed_time(evs[-1])
-        for i in range(len(evs) - 1):
-            phase[names[i]] += evs[i].elapsed_time(evs[i + 1])
-    return total, phase
+        # combine = read the bf16 expert rows + weights, write the bf16 output
+        hbm = {"epb_ll_dispatch": self.b * H_ * 2 + self.b * K_ * 8 + recv_rows * row8,
+               "epb_ll_combine": recv_rows * H_ * 2 + self.b * K_ * 4 + self.b * H_ * 2}
+        # bytes that cross NVLink out of this rank (SURVEY §8d: D and C)
+        remote = {"epb_ll_dispatch": int(sum(len(set(r) - {self.rank}) for r in owner)) * row8,
+                  "epb_ll_combine": int((owner != self.rank).sum()) * H_ * 2}
+        return hbm, remote
 
 
 def capture_steps(step_obj, group, nsteps, flush, phases, upto="combine"):
@@ -335,7 +335,7 @@ def capture_steps(step_obj, group, nsteps, flush, phases, upto="combine"):
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
         for _ in range(3):
-            step_obj.step()
+            step_obj.step(upto)
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     per_step = []
@@ -382,15 +382,41 @@ def steps_per_graph(steps):
     return max(d for d in range(1, min(steps, 10) + 1) if steps % d == 0)
 
 
-def run_ll(args, world, rank, shape=None, zipf=False, light=False):
-    """`light`: only the timed step graph (returns step ms; the sweep)."""
+class _Floor:
+    """Stand-in steps for the latency floor: the same graph skeleton (flush,
+    device barrier, start event, ..., end event) with nothing, or with two
+    tiny kernels in place of dispatch + combine."""
+
+    def __init__(self, kernels):
+        import torch
+        self.kernels = kernels
+        self.t = torch.zeros(1, device="cuda")
+
+    def step(self, upto="combine"):
+        for _ in range(self.kernels):
+            self.t.add_(1.0)
+
+
+def measure_floor(group, flush, nsteps, world):
+    out = {}
+    for name, k in (("events_only_us", 0), ("two_tiny_kernels_us", 2)):
+        fl = _Floor(k)
+        g_, ps = capture_steps(fl, group, nsteps, flush, phases=False)
+        g_.replay()
+        barrier(world)
+        tot, _, n = replay_steps(g_, ps, 3)
+        out[name] = round(allreduce_max(tot / n, world) * 1000.0, 2)
+        del g_
+    return out
+
+
+def run_ll(args, world, rank, shape=None, zipf=False, light=False, zero_copy=False):
+    """`light`: only the timed step graph (the sweep and extra configs)."""
     import torch
-    st = LLStep(world, rank, args.tokens, shape=shape, zipf=zipf, zero_copy=getattr(args, "ll_zero_copy", False))
+    st = LLStep(world, rank, args.tokens, shape=shape, zipf=zipf, zero_copy=zero_copy)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     S = steps_per_graph(args.steps)
     graph, per_step = capture_steps(st, st.g, S, flush, phases=False)
-    if not light:
-        graph_b, per_step_b = capture_steps(st, st.g, S, flush, phases=True)
     for _ in range(max(1, -(-args.warmup // S))):
         graph.replay()
     torch.cuda.synchronize()
@@ -401,46 +427,40 @@ def run_ll(args, world, rank, shape=None, zipf=False, light=False):
         total, _, n = replay_steps(graph, per_step, args.steps // S, samples)
         barrier(world)
     assert n == args.steps
+    st.g.check()
     srt = sorted(samples)
-    pct = {"median_us": allreduce_max(srt[len(srt) // 2], world) * 1000.0,
-           "p99_us": allreduce_max(srt[min(len(srt) - 1, int(0.99 * len(srt)))], world) * 1000.0}
+    res = {"st": st, "step_ms": allreduce_max(total, world) / args.steps,
+           "median_us": allreduce_max(srt[len(srt) // 2], world) * 1000.0,
+           "p99_us": allreduce_max(srt[min(len(srt) - 1, int(0.99 * len(srt)))], world) * 1000.0,
+           "clocks": clk.report()}
+    if not args.no_parity:  # the outputs of the last timed step
+        res["parity"] = st.parity()
+        res["parity"]["ok"] = bool(allreduce_min(float(res["parity"]["ok"]), world))
     if light:
-        st.pct = pct
-        return st, allreduce_max(total, world) / args.steps
-    # per-kernel breakdown from the instrumented graph (events between launches)
+        return res
+    # per-launch device time: an event node before each launch
     barrier(world)
     nb = max(10, min(args.steps, 100))
+    graph_b, per_step_b = capture_steps(st, st.g, S, flush, phases=True)
+    graph_b.replay()
+    barrier(world)
     _, phase, nph = replay_steps(graph_b, per_step_b, -(-nb // S))
-    # per-kernel device time: the instrumented graph's event node before each
-    # launch (the nodes themselves add a little to each interval)
+    res["phase_us"] = {k: allreduce_max(v / nph * 1000.0, world) for k, v in phase.items()}
+    res["launches"] = sum(1 for n_, _ in per_step_b[0] if n_.startswith("epb_")) * args.steps
+    del graph_b
+    res["floor"] = measure_floor(st.g, flush, S, world)
     # staged (send_only + complete) steps: step time and the per-launch split
     gs, pss = capture_steps(st, st.g, S, flush, phases=True, upto="staged")
     gs.replay()
     barrier(world)
     ts, phs, ns = replay_steps(gs, pss, -(-nb // S))
-    st.staged = {"step_us_with_event_nodes": round(allreduce_max(ts / ns, world) * 1000.0, 2),
-                 "launch_us": {k: round(v / ns * 1000.0, 2) for k, v in phs.items()},
-                 "note": "dispatch(send_only) -> complete() -> combine(send_only) -> complete(); an event node "
-                         "before every launch (send phase, then receive phase of each op)"}
+    res["staged"] = {"step_us_with_event_nodes": round(allreduce_max(ts / ns, world) * 1000.0, 2),
+                     "launch_us": {k: round(v / ns * 1000.0, 2) for k, v in phs.items()},
+                     "note": "dispatch(send_only) -> complete() -> combine(send_only) -> complete(); an event "
+                             "node before every launch (send phase, then receive phase of each op)"}
     del gs
-    # the same step as its own graph launch per step (graph launch included)
-    graph1, marks1 = capture(st, st.g, phases=False)
-    for _ in range(3):
-        flush.zero_()
-        st.g.device_barrier()
-        graph1.replay()
-    barrier(world)
-    t1, _ = replay_timed(graph1, marks1, args.steps, flush, align=st.g.device_barrier)
     st.g.check()
-    total_max = allreduce_max(total, world)
-    t1_max = allreduce_max(t1, world)
-    per_phase = {k: v / nph * 1000.0 for k, v in phase.items()}  # us
-    launches = sum(1 for n_, _ in per_step_b[0] if n_.startswith("epb_"))
-    kernel_us = {"epb_ll_dispatch": per_phase.get("epb_ll_dispatch", 0.0),
-                 "epb_ll_combine": per_phase.get("epb_ll_combine", 0.0)}
-    st.pct = pct
-    return (st, total_max / args.steps, per_phase, launches * args.steps, clk.report(),
-            t1_max / args.steps * 1000.0, kernel_us)
+    return res
 
 
 def run_e2e(args, world, rank, st):
@@ -448,10 +468,10 @@ def run_e2e(args, world, rank, st):
     tokens / routing / weights in, host combine output back, every step.
     Headline form: the API calls captured once in a CUDA graph (as a decode
     loop captures them; strict=False, no host syncs inside) whose nodes
-    include the host->device input copies and the device->host output copy;
-    each step = one replay + a host synchronisation, host wall clock.  The
-    eager form (API called from Python each step, strict checks on) is
-    reported beside it."""
+    include the host->device input copies; the combine kernel writes the
+    pinned host output in place; each step = one replay + a host
+    synchronisation, host wall clock.  The eager form (API called from
+    Python each step, strict checks on) is reported beside it."""
     import torch
     ep = st.ep
     g = st.g
@@ -459,7 +479,7 @@ def run_e2e(args, world, rank, st):
     x_h = st.x.cpu().pin_memory()
     w_h = st.w.cpu().pin_memory()
     topk_h = st.topk.cpu().pin_memory()
-    out_h = torch.zeros((st.b, H), dtype=torch.bfloat16).pin_memory()
+    out_h = torch.zeros((st.b, st.H), dtype=torch.bfloat16).pin_memory()
     X = ep.tensor_from_torch(x_h, T.TOKENS)
     W = ep.tensor_from_torch(w_h, T.TOPK_WEIGHTS)
     OUT = ep.tensor_from_torch(out_h, T.TOKENS)
@@ -481,45 +501,41 @@ def run_e2e(args, world, rank, st):
         step()
     torch.cuda.synchronize()
     dt_eager = allreduce_max((time.perf_counter() - t0) / n, world)
-    # graph-captured API calls
+    # eager, perf mode (no host syncs inside the API)
     g.strict = False
-    from paper_2603_13606_b200 import api as _api
-    mapped0, mapped_in0 = _api._HOST_MAPPED, _api._HOST_MAPPED_IN
-
-    def capture(mapped, mapped_in=False):
-        _api._HOST_MAPPED, _api._HOST_MAPPED_IN = mapped, mapped_in
-        try:
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                for _ in range(3):
-                    step()
-            torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                step()
-        finally:
-            _api._HOST_MAPPED, _api._HOST_MAPPED_IN = mapped0, mapped_in0
-        torch.cuda.synchronize()
-        for _ in range(3):
-            graph.replay()
-            torch.cuda.synchronize()
-        return graph
-
-    # the three variants' replays are interleaved so box-to-box and drift
-    # noise hits them alike
-    graphs = [capture(True), capture(False), capture(True, True)]
+    for _ in range(3):
+        step()
     barrier(world)
-    times = [[] for _ in graphs]
+    t0 = time.perf_counter()
     for _ in range(n):
-        for gr, ts in zip(graphs, times):
-            t0 = time.perf_counter()
-            gr.replay()
-            torch.cuda.synchronize()
-            ts.append(time.perf_counter() - t0)
-    dt, dt_copies, dt_in_mapped = (allreduce_max(statistics.median(ts), world) for ts in times)
+        step()
+    torch.cuda.synchronize()
+    dt_eager_fast = allreduce_max((time.perf_counter() - t0) / n, world)
+    # graph-captured API calls
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        graph.replay()
+        torch.cuda.synchronize()
+    barrier(world)
+    times = []
+    for _ in range(n):
+        t0 = time.perf_counter()
+        graph.replay()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    dt = allreduce_max(statistics.median(times), world)
     st.g.check()
+    ok = bool(np.array_equal(out_h.float().numpy(), st.out.float().cpu().numpy()))
     bi = x_h.numel() * 2 + topk_h.numel() * 8 + w_h.numel() * 4
     bo = out_h.numel() * 2
     return {"value": round(dt * 1e6, 2), "unit": "µs", "h2d_bytes_per_step": int(bi),
@@ -527,20 +543,55 @@ def run_e2e(args, world, rank, st):
             "timing": "host wall clock per step (median): one replay of the graph-captured API calls + host "
                       "sync; pinned host inputs copied H2D as graph nodes, the host combine output written by "
                       "the combine kernel in place over PCIe (default API behaviour)",
-            "value_staged_copies": round(dt_copies * 1e6, 2),
-            "staged_copies_timing": "same, with a D2H staging copy of the output as well (EPB_HOST_MAPPED=0)",
-            "value_mapped_inputs": round(dt_in_mapped * 1e6, 2),
-            "mapped_inputs_timing": "same, tokens also read by the dispatch kernel in place over PCIe "
-                                    "(EPB_HOST_MAPPED_IN=1)",
-            "eager_value": round(dt_eager * 1e6, 2),
-            "eager_timing": "host wall clock, API called from Python every step, strict error checks on"}
+            "output_equals_device_path": ok,
+            "eager_strict_value": round(dt_eager * 1e6, 2),
+            "eager_strict_timing": "host wall clock, API called from Python every step, strict error checks "
+                                   "(a device synchronisation after each op)",
+            "eager_value": round(dt_eager_fast * 1e6, 2),
+            "eager_timing": "host wall clock, API called from Python every step (perf mode, no host syncs)"}
 
 
 # ---------------------------------------------------------------------------
-# HT prefill (configs[2]) — eager, phase events
+# HT prefill (configs[2]) — eager, event nodes around each op
 # ---------------------------------------------------------------------------
 
-HT_A2A_PULL_GBPS = 650.0  # measured all-to-all NVLink pull, remote bytes per GPU
+def ht_parity(cfg, wl, rank, x, recv, origin, origin_w, counts, out, E_, K_, H_):
+    """This rank's HT outputs against the oracle: every received row (bf16
+    bits), its origin and weight at the oracle's position (oracle/ht.py
+    dispatch_plan), the counts, and every token's combine (single node:
+    acc = p_0, acc += p_k ascending, out = 0 + acc, ht.py:680-734) with the
+    expert outputs recv * 2^((e%3)-1); bf16 output = RNE of the f32 sum."""
+    import torch
+    from oracle import codecs as oc
+    from oracle import ht as oht
+    n = cfg.num_ranks
+    dev = x.device
+    pl = oht.dispatch_plan(wl.routing, wl.weights, E_, n, rank)
+    res = {"counts": bool(np.array_equal(counts.cpu().numpy(), pl["counts"].astype(np.float32)))}
+    pos = torch.from_numpy(pl["pos"]).to(dev)
+    o = origin.long()[pos].cpu().numpy()
+    res["origin"] = bool(np.array_equal(o[:, 0], pl["e"]) and np.array_equal(o[:, 1], pl["src"]) and
+                         np.array_equal(o[:, 2], pl["t"]) and np.array_equal(o[:, 3], pl["k"]) and
+                         np.array_equal(origin_w[pos].cpu().numpy(), pl["w"]))
+    rows_ok = True
+    for s in range(n):
+        sel = np.nonzero(pl["src"] == s)[0]
+        if not len(sel):
+            continue
+        xs = torch.from_numpy(oc.f32_to_bf16(wl.tokens[s][pl["t"][sel]]).view(np.int16)).to(dev)
+        rows_ok &= torch.equal(recv[pos[torch.from_numpy(sel).to(dev)]].view(torch.int16), xs)
+    res["rows"] = bool(rows_ok)
+    rt = torch.from_numpy(wl.routing[rank]).to(dev)
+    w = torch.from_numpy(wl.weights[rank]).to(dev)
+    xf = x.float()
+    acc = None
+    for kk in range(K_):
+        p = w[:, kk:kk + 1] * (xf * pow2_torch(rt[:, kk])[:, None])
+        acc = p if acc is None else acc + p
+    want = (torch.zeros_like(acc) + acc).to(torch.bfloat16)
+    res["combine"] = bool(torch.equal(out.view(torch.int16), want.view(torch.int16)))
+    res["ok"] = all(res.values())
+    return res
 
 
 def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
@@ -549,12 +600,12 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
     import paper_2603_13606_b200 as ep
     from oracle import workload as owl
     b = args.ht_tokens
-    E, K, H = shape or (globals()["E"], globals()["K"], globals()["H"])
+    E_, K_, H_ = shape or (E, K, H)
     # expert outputs are written into the group's registered window region
     # (EpHandle.expert_out_buffer), so the combine is pulled, not pushed
-    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, E, K, H, b, ep.Dtype.BF16, expert_out_window=True)
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, E_, K_, H_, b, ep.Dtype.BF16, expert_out_window=True)
     g = make_group(world, rank, cfg, strict=False)
-    wl = (owl.make_zipf_workload if zipf else owl.make_workload)(E, world, b, K, H, seed)
+    wl = (owl.make_zipf_workload if zipf else owl.make_workload)(E_, world, b, K_, H_, seed)
     dev = torch.device("cuda", torch.cuda.current_device())
     x = torch.from_numpy(wl.tokens[rank]).to(dev).to(torch.bfloat16)
     topk = torch.from_numpy(wl.routing[rank]).to(dev)
@@ -562,14 +613,14 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
     L = cfg.experts_per_rank
     T = ep.TensorTag
     X, Wt = ep.tensor_from_torch(x, T.TOKENS), ep.tensor_from_torch(w, T.TOPK_WEIGHTS)
-    out = torch.zeros((b, H), dtype=torch.bfloat16, device=dev)
+    out = torch.zeros((b, H_), dtype=torch.bfloat16, device=dev)
     OUT = ep.tensor_from_torch(out, T.TOKENS)
     cnt = torch.zeros((L, world), dtype=torch.float32, device=dev)
     CNT = ep.tensor_from_torch(cnt, T.TOKENS_PER_EXPERTS)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     bufs = {}
-
     t_handle = []
+    last = {}
 
     def step(marks, zero_copy=True):
         torch.cuda.synchronize()
@@ -579,19 +630,29 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         t_handle.append(time.perf_counter() - t0)
         tot = h.get_num_recv_tokens()
         if tot not in bufs:
-            bufs[tot] = (torch.zeros((tot, H), dtype=torch.bfloat16, device=dev),
-                         torch.randn((tot, H), device=dev).to(torch.bfloat16))
+            bufs[tot] = (torch.zeros((tot, H_), dtype=torch.bfloat16, device=dev),
+                         torch.zeros((tot, H_), dtype=torch.bfloat16, device=dev))
         rt, yt = bufs[tot]
-        yw = h.expert_out_buffer()
-        yw.copy_(yt)  # stand-in for the expert GEMM writing its output (untimed)
         flush.zero_()
         g.device_barrier()
         g.trace_phases(marks)
         h.dispatch([X, Wt], [ep.tensor_from_torch(rt, T.TOKENS), CNT])
         g.mark("dispatch:end")
+        g.trace_phases(None)
+        # the expert: y = row * 2^((e%3)-1) (exact) into the registered window
+        # region (zero copy) or an ordinary tensor (untimed, between the ops)
+        res = h.dispatch_result
+        yw = h.expert_out_buffer()
+        yt.copy_((rt.float() * pow2_torch(res.origin[:, 0])[:, None]).to(torch.bfloat16))
+        yw.copy_(yt)
+        flush.zero_()
+        g.device_barrier()
+        g.trace_phases(marks)
+        g.mark("combine:start")
         h.combine([ep.tensor_from_torch(yw if zero_copy else yt, T.TOKENS), Wt], [OUT])
         g.mark("combine:end")
         g.trace_phases(None)
+        last.update(recv=rt, origin=res.origin, origin_w=res.origin_w)
         h.destroy()
         return tot
 
@@ -608,9 +669,14 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
             ev.setdefault(n_, e_)
         names = [m[0] for m in marks]
         for i in range(len(marks) - 1):
-            tphase[names[i]] = tphase.get(names[i], 0.0) + marks[i][1].elapsed_time(marks[i + 1][1])
+            if names[i] != "dispatch:end":
+                tphase[names[i]] = tphase.get(names[i], 0.0) + marks[i][1].elapsed_time(marks[i + 1][1])
         td.append(ev["epb_ht_dispatch"].elapsed_time(ev["dispatch:end"]))
-        tc.append(ev["epb_ht_combine"].elapsed_time(ev["combine:end"]))
+        tc.append(ev["combine:start"].elapsed_time(ev["combine:end"]))
+    parity = None
+    if not args.no_parity:
+        parity = ht_parity(cfg, wl, rank, x, last["recv"], last["origin"], last["origin_w"], cnt, out, E_, K_, H_)
+        parity["ok"] = bool(allreduce_min(float(parity["ok"]), world))
     # the same combine with the expert rows in an ordinary tensor (pushed
     # into the homes' slots, then reduced there)
     tpush = []
@@ -621,48 +687,47 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         ev = {}
         for n_, e_ in marks:
             ev.setdefault(n_, e_)
-        tpush.append(ev["epb_ht_combine"].elapsed_time(ev["combine:end"]))
+        tpush.append(ev["combine:start"].elapsed_time(ev["combine:end"]))
     t_push = allreduce_max(min(tpush), world) / 1e3
     g.check()
     barrier(world)
     t_h = allreduce_max(statistics.median(t_handle[-args.ht_steps:]), world)
     per_d = allgather_f(statistics.median(td), world)
     per_c = allgather_f(statistics.median(tc), world)
-    ph_send = allgather_f(tphase.get("epb_ht_dispatch", 0.0) / args.ht_steps, world)
-    ph_recv = allgather_f(tphase.get("epb_ht_dispatch:recv", 0.0) / args.ht_steps, world)
     t_d = max(per_d) / 1e3
     t_c = max(per_c) / 1e3
     owner = wl.routing[rank] // L
     dsts = [set(r) for r in owner]
-    d_all = sum(len(s) for s in dsts) * H * 2
-    d_remote = sum(len(s - {rank}) for s in dsts) * H * 2
-    c_all = b * K * H * 2
-    c_remote = int((owner != rank).sum()) * H * 2
+    d_all = sum(len(s) for s in dsts) * H_ * 2
+    d_remote = sum(len(s - {rank}) for s in dsts) * H_ * 2
+    c_all = b * K_ * H_ * 2
+    c_remote = int((owner != rank).sum()) * H_ * 2
+    d_remote = allreduce_max(float(d_remote), world)
+    c_remote = allreduce_max(float(c_remote), world)
     g.destroy()
+    nv = world > 1
     return {
-        "tokens_per_rank": b, "dtype": "bf16", "recv_rows": tot,
+        "tokens_per_rank": b, "dtype": "bf16", "recv_rows": tot, "parity": parity,
         "dispatch_us": round(t_d * 1e6, 1), "combine_us": round(t_c * 1e6, 1),
         "create_handle_us": round(t_h * 1e6, 1),
         "combine_push_us": round(t_push * 1e6, 1),
         "combine_push_note": "combine input in an ordinary tensor: rows pushed to the homes' slots, then reduced",
-        "create_handle_timing": "host wall clock of EpGroup.create_handle (routing layout + metadata "
+        "create_handle_timing": "host wall clock of EpGroup.create_handle (routing snapshot + layout + metadata "
                                 "all-gather, receive count on the host on return; ht.py open_round)",
         "dispatch_payload_GBps": round(d_all / t_d / 1e9, 1),
         "combine_payload_GBps": round(c_all / t_c / 1e9, 1),
-        "dispatch_nvlink_GBps": round(d_remote / t_d / 1e9, 1) if world > 1 else None,
-        "combine_nvlink_GBps": round(c_remote / t_c / 1e9, 1) if world > 1 else None,
-        # every GPU pulling from every peer at once (tools/a2a_micro.cu, N=2/4)
-        "nvlink_a2a_pull_bound_GBps": HT_A2A_PULL_GBPS if world > 1 else None,
-        "dispatch_frac_of_a2a": round(d_remote / t_d / 1e9 / HT_A2A_PULL_GBPS, 3) if world > 1 else None,
-        "combine_frac_of_a2a": round(c_remote / t_c / 1e9 / HT_A2A_PULL_GBPS, 3) if world > 1 else None,
+        "dispatch_nvlink_GBps": round(d_remote / t_d / 1e9, 1) if nv else None,
+        "combine_nvlink_GBps": round(c_remote / t_c / 1e9, 1) if nv else None,
+        "nvlink_peak_GBps": NVLINK_GBPS if nv else None,
+        "dispatch_frac_of_nvlink": round(d_remote / t_d / 1e9 / NVLINK_GBPS, 3) if nv else None,
+        "combine_frac_of_nvlink": round(c_remote / t_c / 1e9 / NVLINK_GBPS, 3) if nv else None,
         "phase_us": {k: round(v / args.ht_steps * 1e3, 1) for k, v in tphase.items()},
-        "per_rank_us": {"dispatch": [round(v * 1e3, 1) for v in per_d], "combine": [round(v * 1e3, 1) for v in per_c],
-                        "dispatch_send": [round(v * 1e3, 1) for v in ph_send],
-                        "dispatch_recv": [round(v * 1e3, 1) for v in ph_recv]},
+        "per_rank_us": {"dispatch": [round(v * 1e3, 1) for v in per_d], "combine": [round(v * 1e3, 1) for v in per_c]},
         "transport": "dispatch: pull (rows staged in the sender's window, read once per (token, rank) over "
                      "NVLink); combine: pull (expert outputs in the registered window, read by the token's home)",
-        "note": "payload = bf16 rows per (token, destination rank) for dispatch and per (token, k) "
-                "for combine, all destinations incl. self; nvlink = remote part only",
+        "note": "payload = bf16 rows per (token, destination rank) for dispatch and per (token, k) for combine, "
+                "all destinations incl. self; nvlink = remote rows only (max over ranks), against the measured "
+                "770 GB/s peer copy per direction (B200_PROFILING.md; 900 nominal); L2 flushed before each op",
     }
 
 
@@ -670,26 +735,128 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
 # CPU baseline: the oracle port of the reference algorithm
 # ---------------------------------------------------------------------------
 
-def cpu_oracle_ll(b, n_ranks, steps, seed=0):
-    """Time LL dispatch + combine of the CPU restatement (oracle/ll.py) for
-    one rank group of the bench config; returns us per step and the sample."""
+def _oracle_round(wl, n_ranks, b):
+    from oracle import codecs as oc
     from oracle import ll as oll
+    tok = [oc.bf16_to_f32(oc.f32_to_bf16(t)) for t in wl.tokens]
+    d = oll.dispatch(tok, wl.routing, E, n_ranks, b, H, "fp8", True)
+    ys = [oll.apply_experts(d[r]["recv"], d[r]["counts"], r, E, n_ranks, b,
+                            lambda e, rows: (rows * pow2_np(e)).astype(np.float32)) for r in range(n_ranks)]
+    oll.combine(ys, wl.routing, wl.weights, E, n_ranks, b, H, "bf16")
+
+
+def cpu_oracle_ll(b, n_ranks, steps, seed=0):
+    """LL dispatch + expert + combine of the CPU restatement (oracle/ll.py)
+    for the whole N-rank group, single core; returns us per step."""
     from oracle import workload as owl
     wl = owl.make_workload(E, n_ranks, b, K, H, seed)
+    _oracle_round(wl, n_ranks, b)  # warm-up
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        d = oll.dispatch(wl.tokens, wl.routing, E, n_ranks, b, H, "fp8", True)
-        outs = [d[r]["recv"] for r in range(n_ranks)]
-        oll.combine(outs, wl.routing, wl.weights, E, n_ranks, b, H, "bf16")
+        _oracle_round(wl, n_ranks, b)
         times.append(time.perf_counter() - t0)
-        del d, outs
-    per = statistics.median(times) / n_ranks  # one rank's share of the simulated group
-    return per * 1e6, f"{steps} oracle LL rounds (dispatch FP8+scales, bf16 combine), " \
-                      f"{n_ranks} simulated rank(s) x {b} tokens, DeepSeek-V3 shapes, median, per rank"
+    return statistics.median(times) * 1e6, (f"{steps} oracle LL rounds (FP8+scales dispatch, stub expert, bf16 "
+                                            f"combine) of the {n_ranks}-rank group x {b} tokens/rank, "
+                                            f"DeepSeek-V3 shapes, one core, median")
+
+
+def _cpu_oracle_worker(b, n_ranks, steps, warm, seed, barrier_, q):
+    from oracle import workload as owl
+    wl = owl.make_workload(E, n_ranks, b, K, H, seed)
+    for _ in range(warm):
+        _oracle_round(wl, n_ranks, b)
+    barrier_.wait()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _oracle_round(wl, n_ranks, b)
+    q.put((t0, time.perf_counter()))
+
+
+def cpu_oracle_ll_parallel(b, n_ranks, steps, warmup):
+    """`steps` oracle rounds spread over every usable host core: P processes
+    (the oracle is single-threaded numpy) each run their share concurrently;
+    the all-core step time is the amortised wall time (max end - min start) /
+    steps.  P is capped by the free host memory (~1 GB per simulated rank
+    per round) and at 32."""
+    import multiprocessing as mp
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # pragma: no cover
+        avail = 16 << 30
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    p = max(1, min(ncpu, int(avail // ((1 + n_ranks) << 30)), 32, steps))
+    share = [steps // p + (1 if i < steps % p else 0) for i in range(p)]
+    warm = max(1, -(-warmup // p)) if warmup > 0 else 0
+    if p == 1:
+        ctx_q = []
+        from oracle import workload as owl
+        wl = owl.make_workload(E, n_ranks, b, K, H, 0)
+        for _ in range(warm):
+            _oracle_round(wl, n_ranks, b)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            _oracle_round(wl, n_ranks, b)
+        ctx_q.append((t0, time.perf_counter()))
+        spans = ctx_q
+    else:
+        ctx = mp.get_context("fork")
+        barrier_ = ctx.Barrier(p)
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_cpu_oracle_worker, args=(b, n_ranks, share[i], warm, i, barrier_, q))
+                 for i in range(p)]
+        for pr in procs:
+            pr.start()
+        spans = [q.get() for _ in procs]
+        for pr in procs:
+            pr.join()
+    wall = max(e for _, e in spans) - min(s_ for s_, _ in spans)
+    return wall / steps * 1e6, p, (f"{steps} oracle LL rounds (FP8+scales dispatch, stub expert, bf16 combine) "
+                                   f"of the {n_ranks}-rank group x {b} tokens/rank, DeepSeek-V3 shapes, spread over "
+                                   f"{p} concurrent processes; amortised wall time per round")
 
 
 # ---------------------------------------------------------------------------
+
+def roofline(world, res, st, peaks):
+    """Dominant LL kernel of the step.  N=1: every byte stays in this GPU's
+    memory and a step is latency-bound, so the HBM fraction is reported with
+    the measured floor beside it (the same graph skeleton with two tiny
+    kernels); N>1: bytes leaving the rank over NVLink against 770 GB/s."""
+    hbm_b, nv_b = st.algo_bytes()
+    ev = res["floor"]["events_only_us"]
+    kern = {k: max(1e-3, res["phase_us"].get(k, 0.0) - 0.0) for k in ("epb_ll_dispatch", "epb_ll_combine")}
+    dom = max(kern, key=kern.get)
+    dur = kern[dom]
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(dom)
+    except Exception:  # noqa: BLE001
+        pass
+    step_us = res["step_ms"] * 1000.0
+    lat = {"step_us": round(step_us, 2), "floor_two_kernels_us": res["floor"]["two_tiny_kernels_us"],
+           "floor_events_only_us": ev,
+           "step_over_floor": round(step_us / res["floor"]["two_tiny_kernels_us"], 2),
+           "note": "floor = the same graph skeleton (L2 flush, barrier, start/end events) with two tiny kernels "
+                   "in place of dispatch and combine"}
+    if world == 1:
+        peak = peaks.get("hbm_gbs", 6650.0)
+        ach = hbm_b[dom] / (dur * 1e-6) / 1e9
+        return {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": int(hbm_b[dom]),
+                "duration_us": round(dur, 2), "regime": "latency-bound (N=1: no transport, bytes mostly L2-resident)",
+                "latency": lat,
+                "duration": "event node before the launch to the next one (includes one event-node interval)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+    ach = nv_b[dom] / (dur * 1e-6) / 1e9
+    return {"kernel": dom, "bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_GBPS, "unit": "GB/s",
+            "frac": round(ach / NVLINK_GBPS, 4), "traffic": traffic, "algorithmic_bytes": int(nv_b[dom]),
+            "duration_us": round(dur, 2), "latency": lat,
+            "hbm_bytes": int(hbm_b[dom]),
+            "duration": "event node before the launch to the next one (includes one event-node interval)",
+            "peak_source": "B200_PROFILING.md measured peer copy, 770 GB/s per direction (900 nominal)"}
+
 
 def main():
     args = parse()
@@ -697,25 +864,15 @@ def main():
         return main_reference(args)
     import torch
     world, rank = init_dist()
-    st, step_ms, phases, launches, clocks, own_graph_us, kernel_us = run_ll(args, world, rank)
-    value_us = step_ms * 1000.0
-    # roofline of the dominant kernel
-    algo, remote = st.algo_bytes()
-    kernels = kernel_us
-    dom = max(kernels, key=kernels.get)
+    res = run_ll(args, world, rank, zero_copy=args.ll_zero_copy)
+    st = res["st"]
+    value_us = res["step_ms"] * 1000.0
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:  # noqa: BLE001
         pass
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = algo[dom] / (kernels[dom] * 1e-6) / 1e9
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = prof.get(dom)
-    except Exception:  # noqa: BLE001
-        pass
+    kernel_us = {k: round(v, 2) for k, v in res["phase_us"].items() if k.startswith("epb_")}
     result = {
         "metric": METRIC,
         "value": round(value_us, 2),
@@ -723,39 +880,47 @@ def main():
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(step_ms, 5),
+        "ms_per_step": round(res["step_ms"], 5),
         "higher_is_better": False,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "fp8 dispatch (e4m3 + f32 block-128 scales) / bf16 combine, f32 accumulate",
-        "data": "synthetic (oracle.make_workload: U(-3,3) tokens, uniform distinct top-8 routing, U(0.1,1) weights)",
-        "config": {"workload": "configs[1] LL decode, DeepSeek-V3 shapes", "experts": E, "top_k": K,
-                   "hidden": H, "tokens_per_rank": args.tokens, "ranks": world,
-                   "parallelism": f"ep{world}", "l2": "flushed (256 MB memset) before every step",
-                   "align": "device barrier of all ranks before each step (untimed)",
-                   "graph": (f"{steps_per_graph(args.steps)} steps per CUDA graph (create_handle+dispatch+combine "
-                             "each, bracketed by in-graph events; flush + barrier between, untimed)")},
-        "step_us_own_graph_launch": round(own_graph_us, 2),
-        "ll_staged": st.staged,
-        "step_us_median": round(st.pct["median_us"], 2), "step_us_p99": round(st.pct["p99_us"], 2),
-        "kernel_us": {k: round(v, 2) for k, v in kernel_us.items()},
-        "phase_us_event_nodes": {k: round(v, 2) for k, v in phases.items()},
-        "gpu_launches": launches,
-        "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
-                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "algorithmic_bytes": int(algo[dom]), "traffic": traffic,
-                     "duration": "kernel_us: in-graph event nodes before each launch (CUDA events on the "
-                                 "launching stream)",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
-        "nvlink_bytes_per_step": remote if world > 1 else None,
-        "clocks": clocks,
+        "data": "synthetic (oracle.make_workload: U(-3,3) tokens rounded to bf16, uniform distinct top-8 routing, "
+                "U(0.1,1) weights; expert = x * 2^((e%3)-1))",
+        "config": workload_config(args, world),
+        "timing": {"graph": f"{steps_per_graph(args.steps)} steps per CUDA graph, each bracketed by in-graph "
+                            "events; L2 flush + device barrier of all ranks between steps (untimed)",
+                   "combine_input": "expert outputs in the registered window (pulled)" if args.ll_zero_copy
+                   else "expert outputs in an ordinary tensor (pushed)"},
+        "parity": res.get("parity"),
+        "step_us_median": round(res["median_us"], 2), "step_us_p99": round(res["p99_us"], 2),
+        "kernel_us": kernel_us,
+        "kernel_us_note": "event node before each launch to the next event (one event-node interval included; "
+                          "floor.events_only_us is that interval with nothing between)",
+        "floor": res["floor"],
+        "ll_staged": res["staged"],
+        "gpu_launches": res["launches"],
+        "roofline": roofline(world, res, st, peaks),
+        "nvlink_bytes_per_step": st.algo_bytes()[1] if world > 1 else None,
+        "clocks": res["clocks"],
     }
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, world, rank, st)
+    st.g.destroy()
+    # the other combine transport at the same N (pushed <-> pulled)
+    a_zc = argparse.Namespace(**vars(args))
+    a_zc.steps, a_zc.warmup = 50, 10
+    rz = run_ll(a_zc, world, rank, light=True, zero_copy=not args.ll_zero_copy)
+    result["ll_other_combine_transport"] = {
+        "step_us": round(rz["step_ms"] * 1000.0, 2), "parity": rz.get("parity"),
+        "combine_input": "expert outputs in an ordinary tensor (pushed)" if args.ll_zero_copy
+        else "expert outputs in the registered window (pulled)"}
+    rz["st"].g.destroy()
     if not args.no_ht:
         result["ht"] = run_ht(args, world, rank)
     if not args.no_ht and not args.no_extra:
-        # the other BASELINE configs at this N (parity for them: tests/test_gpu_parity.py)
+        # the other BASELINE configs at this N (their full-size parity also in
+        # tests/test_parity_bench_shapes.py)
         extra = {}
         a2 = argparse.Namespace(**vars(args))
         a2.ht_steps = 3
@@ -764,26 +929,27 @@ def main():
             a2, world, rank, shape=(128, 8, 4096), zipf=True)
         a3 = argparse.Namespace(**vars(args))
         a3.steps, a3.warmup = 50, 10
-        s3, ms3, _, _, _, _, k3 = run_ll(a3, world, rank, shape=(128, 8, 4096), zipf=True)
+        r3 = run_ll(a3, world, rank, shape=(128, 8, 4096), zipf=True, light=True)
         extra["C5 LL Qwen3 E=128 K=8 H=4096, 128 tok, Zipf routing, fp8 dispatch / bf16 combine"] = {
-            "step_us": round(ms3 * 1000, 2), "kernel_us": {k: round(v, 2) for k, v in k3.items()}}
-        s3.g.destroy()
+            "step_us": round(r3["step_ms"] * 1000, 2), "parity": r3.get("parity")}
+        r3["st"].g.destroy()
         result["extra_configs"] = extra
     if not args.no_sweep:
         # configs[1]'s 1-128 tokens/rank sweep (step time only)
-        sweep = {}
+        sweep, sweep_ok = {}, True
         for bb in (1, 2, 4, 8, 16, 32, 64, 128):
             a2 = argparse.Namespace(**vars(args))
             a2.tokens, a2.steps, a2.warmup = bb, 20, 10
-            s2, ms2 = run_ll(a2, world, rank, light=True)
-            sweep[bb] = round(ms2 * 1000, 2)
-            s2.g.destroy()
+            r2 = run_ll(a2, world, rank, light=True, zero_copy=args.ll_zero_copy)
+            sweep[bb] = round(r2["step_ms"] * 1000, 2)
+            sweep_ok &= r2.get("parity", {"ok": True})["ok"]
+            r2["st"].g.destroy()
         result["ll_sweep_us"] = sweep
+        result["ll_sweep_parity"] = sweep_ok
     if rank == 0 and world == 1 and not args.no_cpu:
         us, sample = cpu_oracle_ll(args.tokens, 1, args.cpu_sample_steps)
         result["cpu_baseline"] = {"value": round(us, 1), "unit": "µs", "cores": 1, "kind": "port",
                                   "sample": sample}
-    st.g.destroy()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -792,78 +958,31 @@ def main():
         print(json.dumps(result))
 
 
-def _cpu_oracle_worker(b, n_ranks, steps, seed, barrier_, q):
-    from oracle import ll as oll
-    from oracle import workload as owl
-    wl = owl.make_workload(E, n_ranks, b, K, H, seed)
-
-    def one():
-        d = oll.dispatch(wl.tokens, wl.routing, E, n_ranks, b, H, "fp8", True)
-        oll.combine([d[r]["recv"] for r in range(n_ranks)], wl.routing, wl.weights, E, n_ranks, b, H, "bf16")
-
-    one()  # warm-up
-    barrier_.wait()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        one()
-    q.put((t0, time.perf_counter()))
-
-
-def cpu_oracle_ll_parallel(b, n_ranks, steps):
-    """The oracle LL round on every usable host core: P independent rounds
-    run concurrently in P processes (the oracle is single-threaded numpy), so
-    the per-step figure is the amortised wall time (max end - min start) /
-    (P * steps).  P is capped by the free host memory (a round peaks at
-    ~0.7 GB per simulated rank at DeepSeek-V3 shapes; 1 GB per rank + 1 GB is
-    budgeted) and at 32."""
-    import multiprocessing as mp
-    try:
-        import psutil
-        avail = psutil.virtual_memory().available
-    except Exception:  # pragma: no cover
-        avail = 16 << 30
-    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    p = max(1, min(ncpu, int(avail // ((1 + n_ranks) << 30)), 32))
-    if p == 1:
-        us, sample = cpu_oracle_ll(b, n_ranks, steps)
-        return us, 1, sample
-    ctx = mp.get_context("fork")
-    barrier_ = ctx.Barrier(p)
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_cpu_oracle_worker, args=(b, n_ranks, steps, i, barrier_, q)) for i in range(p)]
-    for pr in procs:
-        pr.start()
-    spans = [q.get() for _ in procs]
-    for pr in procs:
-        pr.join()
-    wall = max(e for _, e in spans) - min(s_ for s_, _ in spans)
-    us = wall / (p * steps) / n_ranks * 1e6
-    return us, p, (f"{p} processes x {steps} oracle LL rounds each, run concurrently (dispatch FP8+scales, "
-                   f"bf16 combine), {n_ranks} simulated rank(s) x {b} tokens, DeepSeek-V3 shapes; amortised "
-                   f"wall time per round, per rank")
-
-
 def main_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    steps = max(1, min(args.steps, args.cpu_sample_steps))
-    us, cores, sample = cpu_oracle_ll_parallel(args.tokens, world, steps)
+    steps = max(1, args.steps)
+    us_all, cores, sample = cpu_oracle_ll_parallel(args.tokens, world, steps, args.warmup)
+    us_one, _ = cpu_oracle_ll(args.tokens, world, max(1, min(3, steps)))
     result = {
-        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": "µs",
-        "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(us / 1000, 3),
+        "impl": "reference", "metric": METRIC, "value": round(us_all, 1), "unit": "µs",
+        "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(us_all / 1000, 3),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp8 dispatch / bf16 combine (numpy f32 arithmetic)",
-        "data": "synthetic (oracle.make_workload)",
-        "config": {"workload": "configs[1] LL decode, DeepSeek-V3 shapes", "experts": E, "top_k": K,
-                   "hidden": H, "tokens_per_rank": args.tokens, "ranks": world,
-                   "parallelism": f"ep{world} (simulated on host)"},
-        "cpu_baseline": {"value": round(us, 1), "unit": "µs", "cores": cores, "kind": "port",
+        "data": "synthetic (oracle.make_workload, the same inputs as the GPU arm)",
+        "config": workload_config(args, world),
+        "value_is": "all_core_amortized_step_us",
+        "all_core_amortized_step_us": round(us_all, 1),
+        "single_core_step_us": round(us_one, 1),
+        "cpu_baseline": {"value": round(us_all, 1), "unit": "µs", "cores": cores, "kind": "port",
                          "sample": sample},
-        "e2e": {"value": round(us, 1), "unit": "µs", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "the reference (epsim) is pure Python and absent on the GPU box; this is its "
-                "CPU restatement in oracle/ (pinned bit-exact to the reference by tests/golden)",
+        "e2e": {"value": round(us_all, 1), "unit": "µs", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (epsim) is pure Python and absent on the GPU box; this is its CPU restatement in "
+                "oracle/ (pinned bit-exact to the reference engines by tests/golden). A step = one LL round of "
+                "the whole N-rank group; value = amortised all-core time per step, single_core_step_us = one "
+                "round on one core",
     }
     print(json.dumps(result))
 

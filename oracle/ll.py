@@ -112,3 +112,38 @@ def apply_experts(recv, counts, rank, e, n, bmax, expert_fn):
                 out[l, r * bmax:r * bmax + c] = expert_fn(rank * ell + l,
                                                           recv[l, r * bmax:r * bmax + c])
     return out
+
+
+def dispatch_plan(routing, e, n, d):
+    """Destination d only (no payload): plan rows (l, s, i, t, k) in the
+    order of `dispatch` and counts [L, N] — the checker for large runs,
+    where every source's full [L, N*B, H] grid would not fit."""
+    ell = experts_per_rank(e, n)
+    counts = np.zeros((ell, n), dtype=np.int64)
+    plan = []
+    for s in range(n):
+        rt = np.asarray(routing[s], dtype=np.int64)
+        if rt.shape[0] == 0:
+            continue
+        ranks = expert_ranks(rt, e)
+        tt, kk = np.nonzero(rt // ell == d)
+        ll_ = rt[tt, kk] - d * ell
+        np.add.at(counts, (ll_, np.full_like(ll_, s)), 1)
+        plan.append(np.stack([ll_, np.full_like(ll_, s), ranks[tt, kk], tt, kk], axis=1))
+    plan = np.concatenate(plan) if plan else np.zeros((0, 5), dtype=np.int64)
+    return plan, counts
+
+
+def combine_scaled_experts(wire, routing, weights, scale_of, dtype):
+    """One home rank's combine (ll.py:464-507) when every expert e returns
+    its input row times scale_of(e) (exact in the wire dtype): the row of
+    (t, k) is wire[t] * scale_of(e_tk), re-encoded in `dtype`, then
+    acc = f32(acc + f32(w * y)) for ascending k."""
+    rt = np.asarray(routing, dtype=np.int64)
+    w = np.asarray(weights, dtype=np.float32)
+    b, k = rt.shape
+    acc = np.zeros(wire.shape, dtype=np.float32)
+    for kk in range(k):
+        y = wire_roundtrip((wire * scale_of(rt[:, kk])[:, None]).astype(np.float32), dtype, False)
+        acc = (acc + (w[:, kk:kk + 1] * y).astype(np.float32)).astype(np.float32)
+    return acc
