@@ -157,6 +157,39 @@ class HTDispatchResult:
         return self._stats
 
 
+class _Scratch:
+    """A handle's small device state in one int32 allocation (pooled per
+    group, reused by later handles of the same batch size): the routing
+    layout (m, q, tok_rank, tok_slot), the LL round word and the LL round
+    state (counts, src_info, self_row, owner_row).  Pointers are handed to
+    the kernels; torch views exist only for what the API exposes."""
+
+    def __init__(self, group: "EpGroup", b: int):
+        cfg = group.config
+        n, e, k = cfg.num_ranks, cfg.num_experts, cfg.top_k
+        ell = cfg.experts_per_rank
+        bb = max(b, 1)
+        ll_rows = ell * n * cfg.max_tokens_per_rank if cfg.algorithm is Algorithm.LL else 1
+        sizes = [("m", e), ("q", n), ("tok_rank", bb * k), ("tok_slot", bb * n), ("hseq", 1),
+                 ("counts", ell * n), ("src_info", ll_rows), ("self_row", bb * k), ("owner_row", bb * k)]
+        off, self.off = 0, {}
+        for name, size in sizes:
+            self.off[name] = (off, size)
+            off += (size + 3) // 4 * 4  # 16-B aligned pieces
+        self.b = b
+        self.buf = torch.empty(off, dtype=torch.int32, device=group.device)
+        base = self.buf.data_ptr()
+        self.ptr = {name: base + o * 4 for name, (o, _) in self.off.items()}
+        self._views = {}
+
+    def view(self, name: str, shape) -> torch.Tensor:
+        v = self._views.get(name)
+        if v is None:
+            o, size = self.off[name]
+            v = self._views[name] = self.buf[o:o + size].view(shape)
+        return v
+
+
 class EpGroup:
     """One rank's context: config, window, peers, handles (api.py:178-253)."""
 
@@ -186,7 +219,12 @@ class EpGroup:
         self._alive = True
         self.strict = strict
         self._marks = None
+        self._scratch_pool: dict = {}
         self.device = torch.device("cuda", torch.cuda.current_device())
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        # the group's kernels go to whatever stream is current at the call
+        self._follows_current = bool(getattr(fabric, "process_mode", False)) or config.num_ranks == 1
+        self._call_sp = 0  # raw stream of the call in progress (set by _on_stream)
 
     # -- properties -----------------------------------------------------------
     @property
@@ -233,6 +271,15 @@ class EpGroup:
         return bool(cap) and isinstance(self._buffer, torch.Tensor) and t.dtype == torch.bfloat16 and \
             t.data_ptr() == self._buffer.data_ptr() + off
 
+    def _take_scratch(self, b: int) -> _Scratch:
+        free = self._scratch_pool.get(b)
+        return free.pop() if free else _Scratch(self, b)
+
+    def _give_scratch(self, sc: _Scratch) -> None:
+        # later work reusing it is enqueued on this group's stream, after
+        # everything that used it (stream order)
+        self._scratch_pool.setdefault(sc.b, []).append(sc)
+
     def _pinned_i32(self, n: int) -> torch.Tensor:
         buf = getattr(self, "_pinned_buf", None)
         if buf is None or buf.numel() < n:
@@ -242,9 +289,13 @@ class EpGroup:
     def _on_stream(self):
         """Context for a call's device work: the group's stream, ordered after
         the caller's current stream (inputs the caller just produced) and
-        followed by it (outputs the caller consumes next).  A no-op when they
-        are the same stream (ProcessFabric, one emulated rank)."""
-        return _StreamScope(self.stream)
+        followed by it (outputs the caller consumes next).  When the group
+        follows the caller's stream (ProcessFabric, one emulated rank) the
+        scope only looks up the raw current stream once per call."""
+        if self._follows_current:
+            self._call_sp = _raw_current_stream(self._dev_index)
+            return _NULL_SCOPE
+        return _StreamScope(self)
 
     def check(self) -> None:
         """Synchronise and raise any error the kernels recorded (timeouts,
@@ -268,7 +319,8 @@ class EpGroup:
         if not self.fabric.process_mode and self.config.num_ranks > 1:
             self.fabric.phase(self.rank)
             return
-        _lib.call("epb_group_barrier", self._g, ctypes.c_void_p(self.stream.cuda_stream))
+        with self._on_stream():
+            _lib.call("epb_group_barrier", self._g, ctypes.c_void_p(self._call_sp))
 
     # -- kernel launches (optionally bracketed by timing marks) -------------
     def trace_phases(self, marks: Optional[list]) -> None:
@@ -352,9 +404,31 @@ class EpGroup:
             self._hooks.release(self._buffer)
 
 
+def _raw_current_stream(device_index: int) -> int:
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:
+        return get(device_index)
+    return torch.cuda.current_stream(device_index).cuda_stream
+
+
+class _NullScope:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NULL_SCOPE = _NullScope()
+
+
 class _StreamScope:
-    def __init__(self, stream):
-        self._s = stream
+    """A group with its own stream (ranks emulated on one GPU): that stream
+    waits for the caller's, runs the call, and the caller's waits for it."""
+
+    def __init__(self, group):
+        self._g = group
+        self._s = group.stream
         self._cur = None
         self._ctx = None
 
@@ -364,6 +438,7 @@ class _StreamScope:
             self._s.wait_stream(self._cur)
         self._ctx = torch.cuda.stream(self._s)
         self._ctx.__enter__()
+        self._g._call_sp = self._s.cuda_stream
         return self
 
     def __exit__(self, *exc):
@@ -498,14 +573,10 @@ class EpHandle:
         cfg = group.config
         dev = group.device
         self._b = routing.shape[0]
-        n, e, k = cfg.num_ranks, cfg.num_experts, cfg.top_k
-        self._m = torch.empty(e, dtype=torch.int32, device=dev)
-        self._q = torch.empty(n, dtype=torch.int32, device=dev)
-        self._tok_rank = torch.empty(max(self._b, 1) * k, dtype=torch.int32, device=dev)
-        self._tok_slot = torch.empty(max(self._b, 1) * n, dtype=torch.int32, device=dev)
-        self._lay = _lib.Layout(self._m.data_ptr(), self._q.data_ptr(), self._tok_rank.data_ptr(),
-                                self._tok_slot.data_ptr(), self._b)
-        self._hseq = torch.empty(1, dtype=torch.int32, device=dev)  # LL round sequence (device)
+        del dev
+        sc = self._sc = group._take_scratch(self._b)
+        self._lay = _lib.Layout(sc.ptr["m"], sc.ptr["q"], sc.ptr["tok_rank"], sc.ptr["tok_slot"], self._b)
+        self._hseq_p = ctypes.c_void_p(sc.ptr["hseq"])  # LL round sequence (device word)
         self._round: Optional[int] = None
         self._round_open = False
         self._meta = None
@@ -530,7 +601,8 @@ class EpHandle:
             raise EpError(ErrorCode.HANDLE_STATE_ERROR, f"cannot {verb} in state {self.state.value}")
 
     def _sp(self) -> ctypes.c_void_p:
-        return ctypes.c_void_p(self.group.stream.cuda_stream)
+        """The stream of the public call in progress (EpGroup._on_stream)."""
+        return ctypes.c_void_p(self.group._call_sp)
 
     def _run_layout(self) -> None:
         self.group._launch("epb_routing_layout", self.group._g, _ptr(self.routing), self._b,
@@ -541,29 +613,29 @@ class EpHandle:
         g = self.group
         cfg = g.config
         n, e = cfg.num_ranks, cfg.num_experts
-        dev = g.device
         self._round = rnd
         nm = n * (e + n)
-        mt = torch.empty(nm + 1, dtype=torch.int32, device=dev)  # meta rows | receive total
-        meta, total = mt[:nm].view(n, e + n), mt[nm:]
-        offsets = torch.empty((e, n), dtype=torch.int32, device=dev)
+        # one round is open per group at a time (ht.py:355-357), so the round
+        # buffers (meta rows | receive total, group offsets) are the group's
+        if getattr(g, "_ht_bufs", None) is None:
+            mt = torch.empty(nm + 1, dtype=torch.int32, device=g.device)
+            g._ht_bufs = (mt, torch.empty((e, n), dtype=torch.int32, device=g.device),
+                          ctypes.c_void_p(mt.data_ptr()), ctypes.c_void_p(mt.data_ptr() + nm * 4))
+        mt, offsets, meta_p, total_p = g._ht_bufs
         g._launch("epb_ht_meta_send", g._g, rnd, ctypes.byref(self._lay), self._sp())
         g.fabric.phase(g.rank)
-        g._launch("epb_ht_meta_recv", g._g, rnd, _ptr(meta), _ptr(offsets), _ptr(total), self._sp())
-        ell = cfg.experts_per_rank
-        lo = g.rank * ell
-        hi = min(lo + ell, e)
-        counts_dev = torch.zeros((ell, n), dtype=torch.float32, device=dev)  # TOKENS_PER_EXPERTS
-        counts_dev[:hi - lo] = meta[:, lo:hi].t().float()
+        g._launch("epb_ht_meta_recv", g._g, rnd, meta_p, _ptr(offsets), total_p, self._sp())
         host = g._pinned_i32(nm + 1)
         host.copy_(mt, non_blocking=True)
         g.check()  # one synchronisation: receive shapes are host-known on return (api.py:235-237)
-        meta_h = host[:nm].numpy().reshape(n, e + n).copy()
-        counts = np.zeros((ell, n), dtype=np.float32)  # (api.py:437-441)
+        meta_h = host.numpy()[:nm].reshape(n, e + n).astype(np.int64)
+        ell = cfg.experts_per_rank
+        lo = g.rank * ell
+        hi = min(lo + ell, e)
+        counts = np.zeros((ell, n), dtype=np.float32)  # TOKENS_PER_EXPERTS (api.py:437-441)
         counts[:hi - lo] = meta_h[:, lo:hi].T
-        self._meta = dict(m=meta_h[:, :e].astype(np.int64), q=meta_h[:, e:].astype(np.int64),
-                          recv_total=int(host[nm]), offsets=offsets,
-                          counts_host=counts, counts_dev=counts_dev)
+        self._meta = dict(m=meta_h[:, :e], q=meta_h[:, e:], recv_total=int(host[nm]), offsets=offsets,
+                          counts_host=counts)
         self._round_open = True
 
     # -- staging helpers ----------------------------------------------------------
@@ -676,29 +748,27 @@ class EpHandle:
             out_t, back_t = self._dev_out(out_tokens)
             out_s, back_s = self._dev_out(out_scales) if out_scales is not None else (None, False)
             cnt_f, back_c = self._dev_out(out_counts, full=True, mapped=True)
-            self._counts_i32 = torch.empty((ell, n), dtype=torch.int32, device=dev)
-            self._src_info = torch.empty((ell, n * cfg.max_tokens_per_rank), dtype=torch.int32, device=dev)
-            self._self_row = torch.empty(max(b, 1) * cfg.top_k, dtype=torch.int32, device=dev)
-            self._owner_row = torch.empty(max(b, 1) * cfg.top_k, dtype=torch.int32, device=dev) \
-                if g._expert_out[1] else None
+            sc = self._sc
+            self._counts_i32 = sc.view("counts", (ell, n))
+            self._src_info = sc.view("src_info", (ell, n * cfg.max_tokens_per_rank))
             a = _lib.LLDispatchArgs(x.data_ptr(), tokens.dtype.code, xs.data_ptr() if xs is not None else None,
                                     self.routing.data_ptr(), b, out_t.data_ptr(), out_tokens.dtype.code,
                                     out_s.data_ptr() if out_s is not None else None, cnt_f.data_ptr(),
-                                    self._counts_i32.data_ptr(), self._src_info.data_ptr(),
-                                    self._self_row.data_ptr(), _ptr(self._owner_row))
+                                    sc.ptr["counts"], sc.ptr["src_info"], sc.ptr["self_row"],
+                                    sc.ptr["owner_row"] if g._expert_out[1] else None)
             self._ll_args = a
             self._keep_alive = (x, xs)
             self._staged = (out_tokens, out_counts, out_scales, out_t, out_s, cnt_f, back_t, back_s, back_c)
             if send_only:
-                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_dispatch", g._g, self._hseq_p, _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 self.state = HandleState.DISPATCH_STAGED
                 return
             if g._fused_ok():
-                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_dispatch", g._g, self._hseq_p, _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
             else:
-                g._launch("epb_ll_dispatch", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_dispatch", g._g, self._hseq_p, _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_dispatch:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_dispatch:recv", g._g, self._hseq_p, _lib.PHASE_RECV, ctypes.byref(a), self._sp())
             self._ll_recv()
 
     def _ll_recv(self) -> None:
@@ -732,7 +802,7 @@ class EpHandle:
         origin = torch.empty((max(total, 1), 4), dtype=torch.int32, device=g.device)
         origin_w = torch.empty(max(total, 1), dtype=torch.float32, device=g.device)
         a = _lib.HTDispatchArgs(x.data_ptr(), tokens.dtype.code, w.data_ptr(), self.routing.data_ptr(), self._b,
-                                self._q.data_ptr(), self._tok_rank.data_ptr(), self._tok_slot.data_ptr(),
+                                self._sc.ptr["q"], self._sc.ptr["tok_rank"], self._sc.ptr["tok_slot"],
                                 meta["offsets"].data_ptr(), out_t.data_ptr(), out_tokens.dtype.code,
                                 origin.data_ptr(), origin_w.data_ptr())
         if g._fused_ok() and g._marks is None:
@@ -749,11 +819,8 @@ class EpHandle:
         ell, n = cfg.experts_per_rank, cfg.num_ranks
         lo = g.rank * ell
         hi = min(lo + ell, cfg.num_experts)
-        oc = out_counts.view()
-        if oc.device.type == "cpu":
-            oc.copy_(torch.from_numpy(meta["counts_host"]).reshape(oc.shape))  # host-known since the meta round
-        else:
-            oc.copy_(meta["counts_dev"])
+        oc = out_counts.view()  # host-known since the meta round
+        oc.copy_(torch.from_numpy(meta["counts_host"]).reshape(oc.shape), non_blocking=oc.device.type != "cpu")
         self._round_open = False
         self._dispatch_result = HTDispatchResult(out_t, origin[:total], origin_w[:total], meta["m"],
                                                  meta["q"], total, _stats_fn=self._ht_dispatch_stats)
@@ -793,22 +860,23 @@ class EpHandle:
                 self._ht_combine(y, rows_in.dtype, w, out)
                 return
             o, back = self._dev_out(out, full=True, mapped=_HOST_MAPPED)
-            a = _lib.LLCombineArgs(y.data_ptr(), rows_in.dtype.code, self._counts_i32.data_ptr(),
-                                   self._src_info.data_ptr(), w.data_ptr(), b, o.data_ptr(), out.dtype.code,
-                                   self._self_row.data_ptr(), self.routing.data_ptr() if b else None,
-                                   _ptr(self._owner_row), int(g._in_expert_out(y)))
+            sc = self._sc
+            a = _lib.LLCombineArgs(y.data_ptr(), rows_in.dtype.code, sc.ptr["counts"],
+                                   sc.ptr["src_info"], w.data_ptr(), b, o.data_ptr(), out.dtype.code,
+                                   sc.ptr["self_row"], self.routing.data_ptr() if b else None,
+                                   sc.ptr["owner_row"] if g._expert_out[1] else None, int(g._in_expert_out(y)))
             self._ll_cargs = a
             self._staged = (out, o, back, w, y)
             if send_only:
-                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_combine", g._g, self._hseq_p, _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 self.state = HandleState.COMBINE_STAGED
                 return
             if g._fused_ok():
-                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_combine", g._g, self._hseq_p, _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
             else:
-                g._launch("epb_ll_combine", g._g, _ptr(self._hseq), _lib.PHASE_SEND, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_combine", g._g, self._hseq_p, _lib.PHASE_SEND, ctypes.byref(a), self._sp())
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_combine:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV, ctypes.byref(a), self._sp())
+                g._launch("epb_ll_combine:recv", g._g, self._hseq_p, _lib.PHASE_RECV, ctypes.byref(a), self._sp())
             self._ll_combine_recv()
 
     def _ll_combine_recv(self) -> None:
@@ -832,7 +900,7 @@ class EpHandle:
         # mismatch aborts the combine kernels before any traffic)
         o, back = self._dev_out(out, full=True)
         a = _lib.HTCombineArgs(y.data_ptr(), y_dtype.code, res.origin.data_ptr(), res.recv_total,
-                               self.routing.data_ptr(), w.data_ptr(), self._b, self._tok_rank.data_ptr(),
+                               self.routing.data_ptr(), w.data_ptr(), self._b, self._sc.ptr["tok_rank"],
                                self._meta["offsets"].data_ptr(), o.data_ptr(), out.dtype.code,
                                self._weights.data_ptr(), self._row_ptr_scratch().data_ptr(),
                                int(g._in_expert_out(y)))
@@ -879,14 +947,14 @@ class EpHandle:
         if self.state is HandleState.DISPATCH_STAGED:
             with g._on_stream():
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_dispatch:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
+                g._launch("epb_ll_dispatch:recv", g._g, self._hseq_p, _lib.PHASE_RECV,
                           ctypes.byref(self._ll_args), self._sp())
                 self._ll_recv()
             return
         if self.state is HandleState.COMBINE_STAGED:
             with g._on_stream():
                 g.fabric.phase(g.rank)
-                g._launch("epb_ll_combine:recv", g._g, _ptr(self._hseq), _lib.PHASE_RECV,
+                g._launch("epb_ll_combine:recv", g._g, self._hseq_p, _lib.PHASE_RECV,
                           ctypes.byref(self._ll_cargs), self._sp())
                 self._ll_combine_recv()
             return
@@ -947,6 +1015,9 @@ class EpHandle:
             self._round_open = False
             self.group._close_ht_round(self)
         self.state = HandleState.DESTROYED
+        sc, self._sc = self._sc, None
+        if sc is not None:
+            self.group._give_scratch(sc)
         try:
             self.group._handles.remove(self)
         except ValueError:

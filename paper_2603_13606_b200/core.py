@@ -226,10 +226,16 @@ class NDTensor:
         return self.data.device
 
     def view(self) -> torch.Tensor:
-        """The typed torch view (no copy)."""
+        """The typed torch view (no copy), built once per descriptor."""
         # storage_offset is absolute in the storage: a `data` that is itself a
         # view (a slice of a larger tensor) contributes its own offset
-        return torch.as_strided(self.data, self.shape, self.strides, self.data.storage_offset() + self.offset)
+        key = (self.data.data_ptr(), self.shape, self.strides, self.offset)
+        cached = self.__dict__.get("_view")
+        if cached is None or cached[0] != key:
+            cached = (key, torch.as_strided(self.data, self.shape, self.strides,
+                                            self.data.storage_offset() + self.offset))
+            self.__dict__["_view"] = cached
+        return cached[1]
 
     def is_contiguous_view(self) -> bool:
         return self.strides == _row_major_strides(self.shape)

@@ -32,6 +32,8 @@
 // fence per rank (system scope when peers are other GPUs; the last CTA to finish), then one arrival per destination; receivers
 // poll N counters, not per-CTA flags.
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "internal.h"
@@ -1496,17 +1498,41 @@ bool coop_attr_enabled() {
   return v == 1;
 }
 
+// per-kernel launch state, set up once: the dynamic shared memory opt-in and
+// the co-residency check of the cooperative launch (cudaFuncSetAttribute and
+// the occupancy query cost several microseconds of host time per call)
+struct KernState {
+  size_t smem_set = 0;  // dynamic shared memory opted in so far
+  size_t occ_smem = 0;  // smem the occupancy was computed for
+  int per_sm = -1;
+};
+std::mutex g_kern_mu;
+std::unordered_map<uint64_t, KernState> g_kern;  // key: kernel address ^ device (attributes are per device)
+
 template <typename Params>
 cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const Params& p, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max<size_t>(smem, 48 * 1024));
-  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_kern_mu);
+    KernState& ks = g_kern[reinterpret_cast<uint64_t>(kern) ^ ((uint64_t)dev << 56)];
+    const size_t want = std::max<size_t>(smem, 48 * 1024);
+    if (want > ks.smem_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+      if (e != cudaSuccess) return e;
+      ks.smem_set = want;
+    }
+    if (coop && (ks.per_sm < 0 || smem > ks.occ_smem)) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ks.per_sm, kern, kThreads, smem);
+      if (e != cudaSuccess) return e;
+      ks.occ_smem = smem;
+    }
+    per_sm = ks.per_sm;
+  }
   if (coop) {
-    // both phases in one launch: CTAs in the receive phase wait on flags the
-    // send phase of other CTAs writes, so all CTAs must be co-resident
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-    if (e != cudaSuccess) return e;
+    // both phases in one launch: CTAs in the receive phase wait on arrivals
+    // other GPUs' CTAs publish, so all CTAs must be co-resident
     if (per_sm * sm_count() < grid) return cudaErrorCooperativeLaunchTooLarge;
     if (!coop_attr_enabled()) {
       kern<<<grid, kThreads, smem, s>>>(p);
