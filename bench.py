@@ -612,7 +612,13 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
     w = torch.from_numpy(wl.weights[rank]).to(dev)
     L = cfg.experts_per_rank
     T = ep.TensorTag
-    X, Wt = ep.tensor_from_torch(x, T.TOKENS), ep.tensor_from_torch(w, T.TOPK_WEIGHTS)
+    # zero-copy input: the tokens live in this rank's registered token stage
+    # (EpGroup.token_in_view), which peers read in place; the plain tensor
+    # (the kernel stages it first) is timed beside it
+    xs = g.token_in_view(b)
+    xs.copy_(x)
+    X_plain, Wt = ep.tensor_from_torch(x, T.TOKENS), ep.tensor_from_torch(w, T.TOPK_WEIGHTS)
+    X = ep.tensor_from_torch(xs, T.TOKENS)
     out = torch.zeros((b, H_), dtype=torch.bfloat16, device=dev)
     OUT = ep.tensor_from_torch(out, T.TOKENS)
     cnt = torch.zeros((L, world), dtype=torch.float32, device=dev)
@@ -622,7 +628,7 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
     t_handle = []
     last = {}
 
-    def step(marks, zero_copy=True):
+    def step(marks, zero_copy=True, zc_in=True):
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
@@ -636,7 +642,7 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         flush.zero_()
         g.device_barrier()
         g.trace_phases(marks)
-        h.dispatch([X, Wt], [ep.tensor_from_torch(rt, T.TOKENS), CNT])
+        h.dispatch([X if zc_in else X_plain, Wt], [ep.tensor_from_torch(rt, T.TOKENS), CNT])
         g.mark("dispatch:end")
         g.trace_phases(None)
         # the expert: y = row * 2^((e%3)-1) (exact) into the registered window
@@ -689,6 +695,17 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
             ev.setdefault(n_, e_)
         tpush.append(ev["combine:start"].elapsed_time(ev["combine:end"]))
     t_push = allreduce_max(min(tpush), world) / 1e3
+    # the dispatch from an ordinary input tensor (staged into the window first)
+    tstg = []
+    for _ in range(2):
+        marks = []
+        step(marks, zc_in=False)
+        torch.cuda.synchronize()
+        ev = {}
+        for n_, e_ in marks:
+            ev.setdefault(n_, e_)
+        tstg.append(ev["epb_ht_dispatch"].elapsed_time(ev["dispatch:end"]))
+    t_stg = allreduce_max(min(tstg), world) / 1e3
     g.check()
     barrier(world)
     t_h = allreduce_max(statistics.median(t_handle[-args.ht_steps:]), world)
@@ -711,6 +728,9 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         "dispatch_us": round(t_d * 1e6, 1), "combine_us": round(t_c * 1e6, 1),
         "create_handle_us": round(t_h * 1e6, 1),
         "combine_push_us": round(t_push * 1e6, 1),
+        "dispatch_staged_input_us": round(t_stg * 1e6, 1),
+        "dispatch_input": "tokens in the registered token stage (EpGroup.token_in_view, read in place by peers); "
+                          "dispatch_staged_input_us = from an ordinary tensor (copied into the stage first)",
         "combine_push_note": "combine input in an ordinary tensor: rows pushed to the homes' slots, then reduced",
         "create_handle_timing": "host wall clock of EpGroup.create_handle (routing snapshot + layout + metadata "
                                 "all-gather, receive count on the host on return; ht.py open_round)",
@@ -723,7 +743,7 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         "combine_frac_of_nvlink": round(c_remote / t_c / 1e9 / NVLINK_GBPS, 3) if nv else None,
         "phase_us": {k: round(v / args.ht_steps * 1e3, 1) for k, v in tphase.items()},
         "per_rank_us": {"dispatch": [round(v * 1e3, 1) for v in per_d], "combine": [round(v * 1e3, 1) for v in per_c]},
-        "transport": "dispatch: pull (rows staged in the sender's window, read once per (token, rank) over "
+        "transport": "dispatch: pull (rows in the sender's registered stage, read once per (token, rank) over "
                      "NVLink); combine: pull (expert outputs in the registered window, read by the token's home)",
         "note": "payload = bf16 rows per (token, destination rank) for dispatch and per (token, k) for combine, "
                 "all destinations incl. self; nvlink = remote rows only (max over ranks), against the measured "

@@ -99,6 +99,11 @@ typedef struct epb_window_info {
   uint64_t expert_out_offset; /* HT with expert_out_window: byte offset of the
                                  expert-output region in the window */
   uint64_t expert_out_rows;   /* its capacity in rows of hidden bf16 */
+  uint64_t token_in_offset;   /* HT: byte offset of the token stage (this rank's
+                                 rows in the wire dtype, read by the peers);
+                                 a dispatch whose TOKENS input IS this region
+                                 skips the stage copy (zero-copy input) */
+  uint64_t token_in_rows;     /* its capacity in rows (max_tokens_per_rank); 0 for LL */
 } epb_window_info;
 
 /* per-handle routing layout; caller-owned device buffers (K1 outputs) */

@@ -30,7 +30,8 @@ class Config(ctypes.Structure):
 
 class WindowInfo(ctypes.Structure):
     _fields_ = [("physical_bytes", ctypes.c_uint64), ("logical_bytes", ctypes.c_uint64),
-                ("expert_out_offset", ctypes.c_uint64), ("expert_out_rows", ctypes.c_uint64)]
+                ("expert_out_offset", ctypes.c_uint64), ("expert_out_rows", ctypes.c_uint64),
+                ("token_in_offset", ctypes.c_uint64), ("token_in_rows", ctypes.c_uint64)]
 
 
 class Layout(ctypes.Structure):

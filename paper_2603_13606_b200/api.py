@@ -266,6 +266,26 @@ class EpGroup:
         h = self.config.hidden
         return self._buffer[off:off + rows * h * 2].view(torch.bfloat16).view(rows, h)
 
+    def token_in_view(self, rows: int) -> torch.Tensor:
+        """HT: [rows, H] view (the wire dtype) of this rank's token stage in
+        the registered window.  Tokens written here and passed unchanged as
+        the dispatch TOKENS input skip the stage copy: peers read them in
+        place (zero-copy input).  Needs a torch-backed window
+        (EpConfig.expert_out_window or allocation hooks returning a tensor).
+        The rows must stay unchanged until the round's combine."""
+        off, cap = getattr(self, "_token_in", (0, 0))
+        if not cap or not isinstance(self._buffer, torch.Tensor):
+            raise EpError(ErrorCode.INVALID_ARGUMENT, "group has no torch-backed HT token stage")
+        if rows > cap:
+            raise EpError(ErrorCode.CAPACITY_EXCEEDED, f"{rows} rows exceed the stage ({cap})")
+        dt = self.config.token_dtype.torch_dtype
+        h = self.config.hidden
+        rb = h * self.config.token_dtype.byte_width
+        if rb % 16:
+            raise EpError(ErrorCode.INVALID_ARGUMENT, "stage rows are padded to 16 B; hidden * width must be a multiple")
+        nb = rows * rb
+        return self._buffer[off:off + nb].view(dt).view(rows, h)
+
     def _in_expert_out(self, t: torch.Tensor) -> bool:
         off, cap = getattr(self, "_expert_out", (0, 0))
         return bool(cap) and isinstance(self._buffer, torch.Tensor) and t.dtype == torch.bfloat16 and \
@@ -549,6 +569,7 @@ def create_group(fabric, rank: int, config: EpConfig, hooks: Optional[Allocation
     grp = EpGroup(fabric, rank, config, layout, cg, int(info.logical_bytes), int(info.physical_bytes),
                   hooks, buffer, strict)
     grp._expert_out = (int(info.expert_out_offset), int(info.expert_out_rows))
+    grp._token_in = (int(info.token_in_offset), int(info.token_in_rows))
     return grp
 
 

@@ -111,6 +111,8 @@ int epb_window_geometry(const epb_config* cfg, epb_window_info* out) {
   if (rc) return rc;
   out->expert_out_offset = 0;
   out->expert_out_rows = 0;
+  out->token_in_offset = 0;
+  out->token_in_rows = 0;
   if (cfg->algorithm == EPB_LL) {
     LLGeom g;
     make_ll_geom(*cfg, g);
@@ -125,6 +127,8 @@ int epb_window_geometry(const epb_config* cfg, epb_window_info* out) {
     out->logical_bytes = g.logical_bytes;
     out->expert_out_offset = g.yout;
     out->expert_out_rows = g.yout_rows;
+    out->token_in_offset = g.stage;
+    out->token_in_rows = (uint64_t)g.B;
   }
   return EPB_OK;
 }

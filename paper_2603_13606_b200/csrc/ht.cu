@@ -168,6 +168,7 @@ struct HTSend {
   int* done;
   HTGeom g;
   int b, rank;
+  int stage_ready;  // x IS this rank's stage region in the wire dtype
   uint32_t tag;
 };
 
@@ -190,8 +191,10 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) 
   constexpr int EPC = Elems<WT>::n;
   constexpr int XW = XT == EPB_F32 ? 4 : 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  // (1) stage
-  if ((H % EPC) == 0 && g.RBp == H * (int)sizeof(uint16_t) * (WT == EPB_F32 ? 2 : 1)) {
+  // (1) stage (skipped when the caller wrote the tokens into the stage
+  // region itself: zero-copy input)
+  if (p.stage_ready) {
+  } else if ((H % EPC) == 0 && g.RBp == H * (int)sizeof(uint16_t) * (WT == EPB_F32 ? 2 : 1)) {
     const int64_t nq = (int64_t)p.b * (H / EPC);
     const int64_t gs = (int64_t)gridDim.x * blockDim.x;
     const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
@@ -1063,6 +1066,7 @@ int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases, const epb_ht_d
     p.done = g->d_done; p.g = g->ht;
     p.b = a->num_tokens; p.rank = g->rank; p.tag = ht_tag(round);
     p.stage = g->window + g->ht.stage;
+    p.stage_ready = a->x == p.stage && a->x_dtype == wire && g->ht.RB == g->ht.RBp;
     cudaError_t e;
     switch (a->x_dtype) {
       case EPB_F32: e = launch_hsend_x<EPB_F32>(p, a->out_dtype, s); break;

@@ -49,7 +49,7 @@ def expert_pow2(e, rows):
     return (rows * np.float32(pow2_scale(e))).astype(np.float32)
 
 
-def run_ht_device(cfg, wl, zero_copy):
+def run_ht_device(cfg, wl, zero_copy, zc_in=False):
     n, h = cfg.num_ranks, cfg.hidden
     ell = cfg.experts_per_rank
     fabric = ep.Fabric(ep.NodeTopology(n, cfg.ranks_per_node))
@@ -59,6 +59,10 @@ def run_ht_device(cfg, wl, zero_copy):
         g = ep.create_group(fabric, rank, cfg)
         try:
             x = torch.from_numpy(wl.tokens[rank]).to(dev).to(torch.bfloat16)
+            if zc_in:  # tokens written into the registered stage: peers read them in place
+                xs = g.token_in_view(x.shape[0])
+                xs.copy_(x)
+                x = xs
             topk = torch.from_numpy(wl.routing[rank]).to(dev)
             w = torch.from_numpy(wl.weights[rank]).to(dev)
             hd = g.create_handle(topk)
@@ -80,7 +84,7 @@ def run_ht_device(cfg, wl, zero_copy):
             out = torch.empty((x.shape[0], h), dtype=torch.float32, device=dev)
             hd.combine([yin, W], [ep.tensor_from_torch(out, T.TOKENS)])
             torch.cuda.synchronize()
-            r = dict(x=x, recv=recv, origin=res.origin.clone(), origin_w=res.origin_w.clone(), counts=cnt,
+            r = dict(x=x.clone(), recv=recv, origin=res.origin.clone(), origin_w=res.origin_w.clone(), counts=cnt,
                      out=out, total=tot)
             hd.destroy()
             return r
@@ -217,3 +221,14 @@ def test_ll_fp8_quantiser_at_midpoints():
     np.testing.assert_array_equal(res[0]["recv_raw"][rows], codes[plan[:, 3]])
     np.testing.assert_array_equal(res[0]["scales_raw"][rows].view(np.uint32), scales[plan[:, 3]].view(np.uint32))
     assert (codes == 0x80).any() and (codes[:, 1:] != 0).any()
+
+
+@pytest.mark.parametrize("n", [2, 8])
+def test_ht_zero_copy_input_and_combine(n):
+    """Tokens in the registered token stage (no stage copy) and expert
+    outputs in the registered window: both directions zero-copy."""
+    e, k, h, b = 256, 8, 7168, 4096
+    cfg = ep.EpConfig(ep.Algorithm.HT, n, n, e, k, h, b, ep.Dtype.BF16, expert_out_window=True)
+    wl = owl.make_workload(e, n, b, k, h, seed=121 + n)
+    res = run_ht_device(cfg, wl, True, zc_in=True)
+    check_ht(cfg, wl, res)
