@@ -506,6 +506,8 @@ def create_group(fabric, rank: int, config: EpConfig, hooks: Optional[Allocation
     every peer window is mapped (CUDA IPC across processes)."""
     if not 0 <= rank < config.num_ranks:
         raise EpError(ErrorCode.INVALID_ARGUMENT, f"rank {rank} outside 0..{config.num_ranks - 1}")
+    if getattr(fabric, "devices", None) is not None:
+        torch.cuda.set_device(fabric.device_of(rank))  # ranks of one process on several GPUs
     topo = fabric.topology
     if topo.num_ranks != config.num_ranks or topo.ranks_per_node != config.ranks_per_node:
         raise EpError(ErrorCode.INVALID_ARGUMENT, "fabric topology does not match the config")

@@ -279,6 +279,23 @@ int epb_group_open_peers(epb_group* g, const epb_ipc_desc* descs) {
 
 int epb_group_set_peers(epb_group* g, const uint64_t* peer_windows) {
   if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  // one process driving several GPUs: a peer window on another device is
+  // reached through peer access (UVA pointers), and ordering towards it
+  // needs system-scope releases, exactly as for CUDA-IPC peers
+  for (int r = 0; r < g->cfg.num_ranks; ++r) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, reinterpret_cast<const void*>(peer_windows[r])) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (at.type == cudaMemoryTypeDevice && at.device != g->device) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return cuda_check(e, "cudaDeviceEnablePeerAccess");
+      g->sys_scope = true;
+    }
+  }
+  if (g->sys_scope) g->ll.sys_fence = g->ht.sys_fence = g->fence_override == 0 ? 0 : 1;
   EPB_CUDA(cudaMemcpy(g->d_peers, peer_windows, sizeof(uint64_t) * g->cfg.num_ranks,
                       cudaMemcpyHostToDevice));
   g->peers_ready = true;

@@ -69,9 +69,9 @@ EPB_DEV uint64_t ld_acq(const uint64_t* p, bool sys) {
   return v;
 }
 // one arrival (the caller released first: fence_release, then these)
-EPB_DEV void red_arrive(uint64_t* p, bool sys) {
-  if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
-  else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+EPB_DEV void red_arrive(uint64_t* p, uint64_t v, bool sys) {
+  if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 // spin until *c >= need (bounded; records TransportClosed).  Acquire: what
 // the arriving CTAs stored before their release is visible afterwards.
@@ -88,29 +88,44 @@ EPB_DEV bool wait_arrivals(const uint64_t* c, uint64_t need, bool sys, uint64_t 
     }
   }
 }
-// Publish this rank's part of a round: every CTA releases its stores at GPU
-// scope and counts itself in at a local counter; the last CTA then issues
-// the one system-scope release of the rank and adds one arrival at each
-// peer.  By cumulativity the system-scope fence covers every CTA's stores
-// (each CTA's GPU-scope release is acquired by the last CTA's RMW on the
-// counter), so peers on other GPUs see all payload once they see the
-// arrival — at the cost of one MEMBAR.SYS per rank per phase instead of one
-// per CTA (concurrent system-scope fences from every SM measured several us).
+// Publish this rank's part of a round: each round adds `grid` to every
+// peer's arrival counter for this rank, after a system-scope release that
+// covers every payload store of the round.  Two schemes, chosen per launch
+// by the sender alone (the receiver only waits for grid*(rounds)):
+//  * few CTAs stored (W <= 32, e.g. a small decode batch): each of CTAs
+//    0..W-1 releases its own stores and adds 1; CTA grid-1 (which is not
+//    one of them) releases and adds grid - W for itself and the idle CTAs;
+//  * otherwise every CTA releases at GPU scope and counts in at a local
+//    counter; the last one issues the rank's single system-scope release
+//    (cumulative over all CTAs' stores: each CTA's GPU-scope release is
+//    acquired by the last CTA's RMW on the counter) and adds grid.
+// Concurrent system-scope fences from every SM measured several us; the
+// last-CTA chain costs a local atomic round trip, which a small batch avoids.
 // All threads call.  `done`: this kind's local counter (reset by the last).
+constexpr int kDirectArrive = 32;
 EPB_DEV void ll_arrive(const uint64_t* peers, uint64_t off, int N, int me, bool fence_sys, bool sys,
-                       unsigned* done, uint32_t chaos_ns) {
+                       unsigned* done, uint32_t chaos_ns, int W) {
   __syncthreads();
-  if (threadIdx.x == 0 && N > 1) {
+  if (threadIdx.x != 0 || N == 1) return;
+  const int G = gridDim.x, c = blockIdx.x;
+  uint64_t add = 0;
+  if (W <= kDirectArrive && W < G) {
+    add = c < W ? 1ull : (c == G - 1 ? (uint64_t)(G - W) : 0ull);
+    if (add == 0) return;
+    chaos_delay(chaos_ns, 0x53u);
+    fence_release(fence_sys);
+  } else {
     chaos_delay(chaos_ns, 0x51u);
     fence_release(false);
-    if (atomicAdd(done, 1u) == gridDim.x - 1) {
-      *done = 0u;  // next use is a later kernel (stream order)
-      fence_release(fence_sys);
-      for (int d = 0; d < N; ++d)
-        if (d != me) red_arrive(reinterpret_cast<uint64_t*>(peer_base(peers, d) + off) + me, sys);
-    }
+    if (atomicAdd(done, 1u) != (unsigned)G - 1) return;
+    *done = 0u;  // next use is a later kernel (stream order)
+    fence_release(fence_sys);
+    add = (uint64_t)G;
   }
+  for (int d = 0; d < N; ++d)
+    if (d != me) red_arrive(reinterpret_cast<uint64_t*>(peer_base(peers, d) + off) + me, add, sys);
 }
+
 // warp: wait until every source in `need` (bit per rank) has arrived; bits
 // already seen are cached in `seen`.  Lane 0 polls; __syncwarp orders the
 // other lanes' later loads after its acquire.
@@ -356,6 +371,15 @@ EPB_DEV int sel8(const int* v, int i) {
   return r;
 }
 
+// parts per token and work units (token, part) of the fast send path: a
+// small batch spreads each token over up to 8 CTAs (chunk ranges are
+// multiples of 8 chunks, the FP8 blocks)
+EPB_DEV int fast_parts(int b, int G, int nch) {
+  int P = b > 0 ? G / b : 1;
+  return max(1, min(min(P, 8), max(1, nch / 8)));
+}
+EPB_DEV int fast_units(int b, int G, int nch) { return b * fast_parts(b, G, nch); }
+
 // Send phase, fast path (top-k <= 8, batch <= block size, hidden % 16 == 0).
 // Thread tau holds routing row tau in registers: validation, the earlier-
 // token prefix counts of the CTA's token and the counting CTA's histograms
@@ -379,9 +403,7 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
   const bool legacy = g.layout == EPB_LAYOUT_LEGACY;
   const int lo = me * L;
   const int nloc = max(0, min(L, E - lo));
-  // parts per token: chunk ranges are multiples of 8 chunks (FP8 blocks)
-  int P = b > 0 ? G / b : 1;
-  P = max(1, min(min(P, 8), max(1, nch / 8)));
+  const int P = fast_parts(b, G, nch);
   const int per = ((nch + P - 1) / P + 7) & ~7;
   const int units = b * P;
   __shared__ int s_part[kThreads / 32][16];  // per-warp prefix partials (i of k, then j of k)
@@ -713,7 +735,8 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
     if (p.phases & kPhaseSend) {
       const bool bad = ll_send_fast<XT, WT, SC, OT>(p, smem, seq_ld, seq, parity_off);
       // publish: one system-scope release per rank, one arrival per destination
-      ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns);
+      ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns,
+                fast_units(p.b, gridDim.x, g.H / Elems<WT>::n));
       LL_STAMP(p, 4);
       if (bad) return;
     }
@@ -1003,7 +1026,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       if (bad && threadIdx.x == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
     }
     // publish: one release per CTA, one arrival per destination
-    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns);
+    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, G);
     LL_STAMP(p, 4);
     if (bad) return;
   }
@@ -1017,7 +1040,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
     }
     if (N == 1) return;  // own rows and counts were placed by the send phase
-    const uint64_t target = (uint64_t)((seq >> 1) + 1);
+    const uint64_t target = (uint64_t)G * ((seq >> 1) + 1);
     const uint64_t* arr = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.d_arr);
     const uint32_t* crows = reinterpret_cast<const uint32_t*>(p.win + parity_off + g.cnt_row);
     const int R = L + 1;
@@ -1085,8 +1108,31 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const int j = r / nsrc, so = r - j * nsrc;
       const int s = me + 1 + so < N ? me + 1 + so : me + 1 + so - N;
       if (!warp_wait_sources(1ull << s, seen, arr, target, sys, p.timeout_ns, p.err, lane)) return;
+      if (f2 == (int)blockIdx.x) LL_STAMP(p, 6);  // warp 0's first arrival seen
+      // the slot count, the slot header and the first batch of the row are
+      // loaded together (one round trip; slot (s, j) exists even when the
+      // source sent fewer slots — those loads are then simply unused)
       const uint32_t* crow = crows + s * R;
+      const uint8_t* slot = p.win + parity_off + g.disp_slot + ((int64_t)s * B + j) * g.slot_stride;
+      const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
+      const int nch2 = H / EPC;
+      const int per = (nch2 + 1) / 2;
+      const int c0 = half * per, c1 = min(nch2, c0 + per);
+      int4 v0[kUnroll];
+      if (FAST || fan) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c < c1) v0[u] = ld_weak_v4(slot + (int64_t)c * 16);
+        }
+      }
       const uint32_t q = crow[L];
+      int e = -1, ci = 0;
+      if (lane < K) {
+        e = (int)hdr[2 + lane];
+        ci = (int)hdr[2 + K + lane];
+      }
+      const uint32_t tok = hdr[0];
       if (q == kPoison) {
         if (lane == 0) atomicCAS(p.err, 0, EPB_TRANSPORT_CLOSED);
         return;
@@ -1098,17 +1144,10 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           p.counts_f32[l * N + s] = (float)m;
         }
       if (j >= (int)q) continue;
-      const uint8_t* slot = p.win + parity_off + g.disp_slot + ((int64_t)s * B + j) * g.slot_stride;
-      const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
-      int e = -1, ci = 0;
-      if (lane < K) {
-        e = (int)hdr[2 + lane];
-        ci = (int)hdr[2 + K + lane];
-      }
       const bool loc = lane < K && e >= lo && e < lo + nloc;
       const int my_orow = (e - lo) * N * B + s * B + ci;
       const unsigned lm = __ballot_sync(0xffffffffu, loc);
-      if (half == 0 && loc) p.src_info[my_orow] = (int32_t)(hdr[0] * K + lane);
+      if (half == 0 && loc) p.src_info[my_orow] = (int32_t)(tok * K + lane);
       if (!FAST && !fan) {
         for (unsigned mm = lm; mm; mm &= mm - 1) {
           const int64_t row = __shfl_sync(0xffffffffu, my_orow, __ffs(mm) - 1);
@@ -1117,15 +1156,13 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         }
         continue;
       }
-      const int nch2 = H / EPC;
-      const int per = (nch2 + 1) / 2;
-      const int c0 = half * per, c1 = min(nch2, c0 + per);
       for (int base = c0; base < c1; base += 32 * kUnroll) {
         int4 v[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const int c = base + u * 32 + lane;
-          if (c < c1) v[u] = ld_weak_v4(slot + (int64_t)c * 16);
+          if (base == c0) v[u] = v0[u];
+          else if (c < c1) v[u] = ld_weak_v4(slot + (int64_t)c * 16);
         }
         float sc_c[kUnroll];
         if constexpr (SC && OT != WT) {
@@ -1234,6 +1271,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     seq = s_seq;
   }
   const uint64_t parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
+  int send_ctas = 0;  // CTAs that store rows this round (task t of the first pass goes to CTA t / warps)
 
   if (send) {
     // block-wide exclusive scan of the remote (l, src) counts
@@ -1256,6 +1294,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     LL_STAMP(p, 1);
     const int total = s_pre[P];
     const int part = (nch + kParts - 1) / kParts;
+    send_ctas = min((int)gridDim.x, ((vec ? total * kParts : total) + nw - 1) / nw);
     chaos_delay(g.chaos_ns, 0x2Bu);
     const int tasks = vec ? total * kParts : total;
     for (int task = blockIdx.x * nw + warp; task < tasks; task += gridDim.x * nw) {
@@ -1310,7 +1349,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // one release per CTA, one arrival per home rank (pulled combine: the
     // expert outputs were written by earlier kernels on this stream — the
     // arrival announces them)
-    ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns);
+    ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, send_ctas);
     LL_STAMP(p, 3);
   }
 
@@ -1346,7 +1385,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
       }
     };
     if (vec && task < tasks) fetch(task / segs);
-    const uint64_t target = (uint64_t)((seq >> 1) + 1);
+    const uint64_t target = (uint64_t)G * ((seq >> 1) + 1);
     const uint64_t* arr = reinterpret_cast<const uint64_t*>(p.win + parity_off + g.c_arr);
     uint64_t seen = 0;
     LL_STAMP(p, 5);
@@ -1360,6 +1399,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
           const uint64_t need = (uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)bit) |
                                 ((uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)(bit >> 32)) << 32);
           if (!warp_wait_sources(need, seen, arr, target, sys, p.timeout_ns, p.err, lane)) return;
+          if (task == (int)blockIdx.x) LL_STAMP(p, 7);  // warp 0's first token's sources seen
         }
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
         const int cbase = sg * kSeg + lane;

@@ -82,12 +82,24 @@ class Fabric:
 
     process_mode = False
 
-    def __init__(self, topology: NodeTopology, seed: int = 0, device=None, timeout: float = 120.0):
+    def __init__(self, topology: NodeTopology, seed: int = 0, device=None, timeout: float = 120.0, devices=None):
+        """`devices`: one CUDA device per rank — ranks on several GPUs of one
+        process (threads; peer windows through peer access, system-scope
+        ordering); default: every rank on `device` (the current one)."""
         self.topology = topology
         self.seed = seed
         n = topology.num_ranks
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self._stream = torch.cuda.Stream(device=self.device) if n > 1 else None
+        self.devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices] \
+            if devices is not None else None
+        if self.devices is not None and len(self.devices) != n:
+            raise EpError(ErrorCode.INVALID_ARGUMENT, f"{len(self.devices)} devices for {n} ranks")
+        if self.devices is not None:
+            self._streams = [torch.cuda.Stream(device=d) for d in self.devices]
+            self._stream = None
+        else:
+            self._streams = None
+            self._stream = torch.cuda.Stream(device=self.device) if n > 1 else None
         self._barrier = _Barrier(n, timeout)
         self._lock = threading.Lock()
         self._calls = {}
@@ -114,7 +126,12 @@ class Fabric:
         if self.topology.num_ranks > 1:
             self._barrier.wait()
 
+    def device_of(self, rank: int) -> torch.device:
+        return self.devices[rank] if self.devices is not None else self.device
+
     def stream(self, rank: int):
+        if self._streams is not None:
+            return self._streams[rank]
         return self._stream if self._stream is not None else torch.cuda.current_stream(self.device)
 
     def registered_bytes(self, rank: int) -> int:

@@ -19,9 +19,9 @@ import bench  # noqa: E402
 from paper_2603_13606_b200 import _lib  # noqa: E402
 
 # stamp indices of ll_dispatch_kernel / ll_combine_kernel (csrc/ll.cu LL_STAMP)
-DISP = ["start", "validated", "positioned", "tokens-done", "arrived", "recv", "", "recv-done", "routing-in",
-        "quantised(w1)", "prefix(w0)"]
-COMB = ["start", "prefix", "sent", "arrived", "recv", "fetched", "reduced"]
+DISP = ["start", "", "emitted", "tokens-done", "arrived", "recv", "first-src-seen", "recv-done", "rows-in",
+        "quantised(w1)", "after-barrier"]
+COMB = ["start", "prefix", "sent", "arrived", "recv", "fetched", "reduced", "srcs-seen"]
 
 
 def show(name, buf, labels):
@@ -59,6 +59,7 @@ def main():
         elif a.flush == "read":
             flush.view(torch.int32).sum()
         bench.barrier(world)
+        g.device_barrier()  # ranks start the step together (as bench.py does)
         h = g.create_handle(st.topk)
         _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(tr_d.data_ptr()))
         h.dispatch([st.X], [st.RECV, st.RECV_SC, st.CNT])
@@ -67,8 +68,11 @@ def main():
         _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(0))
         h.destroy()
         torch.cuda.synchronize()
+        t0s = bench.allgather_f(float(tr_d.view(-1, 16)[:, 0][tr_d.view(-1, 16)[:, 0] > 0].min().item()), world)
         if rank == 0:
-            print(f"== rep {rep} (rank 0 of {world}, L2 flush: {a.flush})")
+            print(f"== rep {rep} (rank 0 of {world}, L2 flush: {a.flush}); dispatch start per rank vs rank 0 "
+                  f"(globaltimer, comparable only if the GPUs' timers agree): "
+                  f"{[round((t - t0s[0]) / 1e3, 2) for t in t0s]} us")
             show("dispatch", tr_d, DISP)
             show("combine", tr_c, COMB)
         bench.barrier(world)
