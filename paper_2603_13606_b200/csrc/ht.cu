@@ -97,18 +97,15 @@ struct HTMetaRecv {
 
 __global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
   extern __shared__ int32_t s_meta[];  // [N][C]
-  __shared__ int s_fail;
   const HTGeom& g = p.g;
   const int N = g.N, E = g.E, C = E + N, L = g.L;
-  if (threadIdx.x == 0) s_fail = 0;
-  __syncthreads();
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.meta_flag) + p.parity * N;
+  bool fail = false;
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v;
-    if (!wait_tag(&flags[s], p.tag, 0, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    fail |= !wait_tag(&flags[s], p.tag, 0, 0xFFFFFFFFu, p.timeout_ns, p.err, &v);
   }
-  __syncthreads();
-  if (s_fail) return;
+  if (__syncthreads_or(fail)) return;
   const int32_t* rows = reinterpret_cast<const int32_t*>(p.win + g.meta + (uint64_t)p.parity * N * C * 4);
   for (int i = threadIdx.x; i < N * C; i += blockDim.x) {
     const int32_t v = *reinterpret_cast<const volatile int32_t*>(&rows[i]);
@@ -302,20 +299,17 @@ struct HTRecv {
 template <int WT, int OT>
 __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) {
   __shared__ int s_pre[kMaxRanks + 1], s_q[kMaxRanks];
-  __shared__ int s_fail;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H, L = g.L;
   const int me = p.rank;
-  if (threadIdx.x == 0) s_fail = 0;
-  __syncthreads();
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
+  bool fail = false;
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
-    if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    if (s != me) fail |= !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v);
     s_q[s] = s == me ? p.q[me] : (int)(v & 0xFFFFFFFFu);
   }
-  __syncthreads();
-  if (s_fail) return;
+  if (__syncthreads_or(fail)) return;
   // remote records interleaved over the sources in chunks of kRC: chunk c
   // reads source me+1+(c % (N-1)), its chunk c / (N-1), so every source's
   // stage is read by all receivers at an even rate for the whole phase
@@ -451,7 +445,7 @@ EPB_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "m
 __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(HTRecv p) {
   extern __shared__ __align__(128) uint8_t s_buf[];  // [warps][2][hb] then [warps][2] mbarriers
   __shared__ int s_q[kMaxRanks];
-  __shared__ int s_fail, s_maxq;
+  __shared__ int s_maxq;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, L = g.L;
   const int me = p.rank;
@@ -464,16 +458,15 @@ __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x == 0) s_fail = 0;
-  __syncthreads();
+  __syncthreads();  // the mbarrier initialisation
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.dflag);
+  bool fail = false;
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
-    if (s != me && !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) s_fail = 1;
+    if (s != me) fail |= !wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v);
     s_q[s] = s == me ? p.q[me] : (int)(v & 0xFFFFFFFFu);
   }
-  __syncthreads();
-  if (s_fail) return;
+  if (__syncthreads_or(fail)) return;
   // the staged rows were acquired through generic loads; the bulk copies
   // read them through the async proxy
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -778,25 +771,22 @@ EPB_DEV void ht_load8(const uint8_t* row, int c, float* y) {
 
 template <int IT, int OT>
 __global__ void __launch_bounds__(kHTThreads, 1) ht_combine_recv_kernel(HTCombRecv p) {
-  __shared__ int s_fail;
   const HTGeom& g = p.g;
   const int N = g.N, K = g.K, H = g.H, L = g.L;
   const int me = p.rank;
   constexpr int YB = IT == EPB_F32 ? 4 : 2;
   constexpr int OW = OT == EPB_F32 ? 4 : 2;
-  if (threadIdx.x == 0) s_fail = *reinterpret_cast<const volatile int*>(p.err) != 0;
-  __syncthreads();
-  if (s_fail) return;
+  if (__syncthreads_or(threadIdx.x == 0 && *reinterpret_cast<const volatile int*>(p.err) != 0)) return;
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.cflag);
+  bool fail = false;
   for (int s = threadIdx.x; s < N; s += blockDim.x) {
     uint64_t v = 0;
     if (s == me) continue;
-    if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) { s_fail = 1; continue; }
+    if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) { fail = true; continue; }
     // every rank must combine in the same dtype (the rows are raw bytes)
-    if ((int)((v >> 28) & 0xF) != IT) { atomicCAS(p.err, 0, EPB_TAG_MISMATCH); s_fail = 1; }
+    if ((int)((v >> 28) & 0xF) != IT) { atomicCAS(p.err, 0, EPB_TAG_MISMATCH); fail = true; }
   }
-  __syncthreads();
-  if (s_fail) return;
+  if (__syncthreads_or(fail)) return;
   const uint8_t* crow = p.win + g.crow;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const bool one_node = g.rpn == N;

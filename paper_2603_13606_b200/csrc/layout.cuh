@@ -110,18 +110,17 @@ EPB_DEV void block_layout(const TopkT* topk, int b, int K, int E, int N, int L, 
 // row validation: ids in [0, E), distinct within a row (api.py:150-170)
 template <typename TopkT>
 EPB_DEV bool block_validate(const TopkT* topk, int b, int K, int E, int* s_bad) {
-  if (threadIdx.x == 0) *s_bad = 0;
-  __syncthreads();
+  (void)s_bad;
+  bool bad = false;
   for (int t = threadIdx.x; t < b; t += blockDim.x) {
     for (int k = 0; k < K; ++k) {
       const int64_t e = (int64_t)topk[(int64_t)t * K + k];
-      if (e < 0 || e >= E) { *s_bad = 1; break; }
+      if (e < 0 || e >= E) { bad = true; break; }
       for (int j = 0; j < k; ++j)
-        if ((int64_t)topk[(int64_t)t * K + j] == e) *s_bad = 1;
+        if ((int64_t)topk[(int64_t)t * K + j] == e) bad = true;
     }
   }
-  __syncthreads();
-  return *s_bad == 0;
+  return __syncthreads_or(bad) == 0;  // one verdict per block (a barrier)
 }
 
 }  // namespace epb

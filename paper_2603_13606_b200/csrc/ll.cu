@@ -725,7 +725,6 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   // round sequence: thread 0 issues the load now; it lands in shared memory
   // at the first block barrier
   __shared__ uint32_t s_seq;
-  __shared__ int s_bad;
   uint32_t seq_ld = 0;
   if (threadIdx.x == 0) seq_ld = ld_round_u32((p.phases & kPhaseSend) ? p.dseq + blockIdx.x : p.hseq);
   uint32_t seq = 0;
@@ -758,11 +757,11 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       s_topk[i] = (e >= 0 && e < E) ? (int)e : -1;
     }
     if ((int)threadIdx.x < 2 * kMaxTopK) s_cnt[threadIdx.x] = 0;
-    if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
     LL_STAMP(p, 8);
     // routing validation (api.py:150-170): ids in range, distinct per row;
     // every CTA reaches the same verdict before any traffic
+    bool row_bad = false;
     for (int t = threadIdx.x; t < b; t += blockDim.x) {
       bool ok = true;
       for (int k = 0; k < K; ++k) {
@@ -770,7 +769,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         ok &= e >= 0;
         for (int j = 0; j < k; ++j) ok &= s_topk[t * K + j] != e;
       }
-      if (!ok) s_bad = 1;
+      row_bad |= !ok;
     }
     if (threadIdx.x == 0) {
       // the round: every CTA advances its own copy of the sequence (all
@@ -780,11 +779,10 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       p.dseq[blockIdx.x] = seq_ld + 1;
       if (blockIdx.x == 0) *p.hseq = seq_ld;
     }
-    __syncthreads();
+    const bool bad = __syncthreads_or(row_bad) != 0;
     LL_STAMP(p, 1);
     seq = s_seq;
     parity_off = (uint64_t)(seq & 1) * g.parity_bytes;
-    const bool bad = s_bad != 0;
     const uint64_t slot_off = parity_off + g.disp_slot;
 
     // one token chunk: input (prefetched for the CTA's first token) ->
