@@ -828,9 +828,9 @@ class EpHandle:
                                 self._sc.ptr["q"], self._sc.ptr["tok_rank"], self._sc.ptr["tok_slot"],
                                 meta["offsets"].data_ptr(), out_t.data_ptr(), out_tokens.dtype.code,
                                 origin.data_ptr(), origin_w.data_ptr())
-        if g._fused_ok() and g._marks is None:
+        if g._fused_ok():
             g._launch("epb_ht_dispatch", g._g, rnd, _lib.PHASE_BOTH, ctypes.byref(a), self._sp())
-        else:  # (timing marks: one launch per phase so each half is timed)
+        else:
             g._launch("epb_ht_dispatch", g._g, rnd, _lib.PHASE_SEND, ctypes.byref(a), self._sp())
             if not g._fused_ok():
                 g.fabric.phase(g.rank)
