@@ -62,6 +62,16 @@ EPB_DEV uint32_t ld_round_u32(const uint32_t* p) {
 }
 EPB_DEV uint8_t* peer_base(const uint64_t* peers, int r) { return reinterpret_cast<uint8_t*>(peers[r]); }
 
+// Programmatic dependent launch: the LL kernels are launched so that the
+// next kernel's grid is scheduled while this one drains; each kernel first
+// waits for its predecessors to complete (their writes visible), then lets
+// its own dependents start launching.  Without the launch attribute both
+// instructions are no-ops.
+EPB_DEV void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 EPB_DEV uint64_t ld_acq(const uint64_t* p, bool sys) {
   uint64_t v;
   if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -690,6 +700,7 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
 template <int XT, int WT, bool SC, int OT, bool FAST>
 __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   extern __shared__ int smem[];
+  pdl_enter();
   const LLGeom& g = p.g;
   const int K = g.K, N = g.N, H = g.H, L = g.L, E = g.E, B = g.B, G = gridDim.x;
   const int b = p.b, me = p.rank;
@@ -1236,6 +1247,7 @@ struct LLComb {
 template <int IT, int WT, int OT, bool VEC>
 __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
   extern __shared__ int s_pre[];  // [L*N + 1]
+  pdl_enter();
   const LLGeom& g = p.g;
   const int N = g.N, L = g.L, B = g.B, H = g.H, K = g.K, G = gridDim.x;
   const int me = p.rank;
@@ -1525,6 +1537,16 @@ int sm_count() {
   return n;
 }
 
+// EPB_PDL=0 launches the LL kernels without programmatic dependent launch
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EPB_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // EPB_COOP=0 launches the fused kernels without the cooperative attribute
 // (co-residency then rests on grid <= SMs x occupancy, checked below)
 bool coop_attr_enabled() {
@@ -1584,6 +1606,21 @@ cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+  }
+  if (pdl_enabled()) {
+    // not cooperative: let this grid be scheduled while its predecessor
+    // drains (it waits for the predecessor's completion in pdl_enter)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
