@@ -797,8 +797,9 @@ def cpu_oracle_ll_parallel(b, n_ranks, steps, warmup):
     """`steps` oracle rounds spread over every usable host core: P processes
     (the oracle is single-threaded numpy) each run their share concurrently;
     the all-core step time is the amortised wall time (max end - min start) /
-    steps.  P is capped by the free host memory (~1 GB per simulated rank
-    per round) and at 32."""
+    steps.  P is capped by the free host memory (a round of the N-rank group
+    peaks at ~1.6 GB per simulated rank; 2 GB per rank + 2 GB is budgeted per
+    process) and at 32."""
     import multiprocessing as mp
     try:
         import psutil
@@ -806,7 +807,7 @@ def cpu_oracle_ll_parallel(b, n_ranks, steps, warmup):
     except Exception:  # pragma: no cover
         avail = 16 << 30
     ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    p = max(1, min(ncpu, int(avail // ((1 + n_ranks) << 30)), 32, steps))
+    p = max(1, min(ncpu, int(avail // ((2 + 2 * n_ranks) << 30)), 32, steps))
     share = [steps // p + (1 if i < steps % p else 0) for i in range(p)]
     warm = max(1, -(-warmup // p)) if warmup > 0 else 0
     if p == 1:
