@@ -18,6 +18,7 @@
  *   LLRank.combine (ll.py:404-462)               | epb_ll_combine phase SEND     (K4a)
  *   LLRank.complete_combine (ll.py:464-507)      | epb_ll_combine phase RECV     (K4b)
  *   HTRank.exchange_metadata (ht.py:291-331)     | epb_ht_meta_send / _recv      (K5a)
+ *   HTRank.open_round (ht.py:335-368)            | epb_ht_open (K1 + K5a, one launch)
  *   HTRank.dispatch + _assemble (ht.py:381-583)  | epb_ht_dispatch               (K5b)
  *   HTRank.combine (ht.py:587-735)               | epb_ht_combine                (K6)
  *   quantize_block / dequantize_block            | epb_fp8_quantize / _dequantize (K7)
@@ -150,6 +151,11 @@ int epb_group_set_trace(epb_group* g, uint64_t* trace);
 int epb_group_barrier(epb_group* g, void* stream);
 /* reads (and with clear!=0 resets) the device error word; synchronises */
 int epb_group_poll_error(epb_group* g, int clear, int32_t* code);
+/* Host address of a pinned mirror of the error word: the kernel recording
+ * a failure also writes its code there, so after synchronising the group's
+ * streams a zero read means no failure was recorded (a nonzero one is
+ * confirmed and cleared with epb_group_poll_error).  Valid until destroy. */
+int epb_group_error_word(epb_group* g, const int32_t** host_word);
 int epb_group_destroy(epb_group* g);
 
 /* K1: validation + counts + dedup slots + per-expert ranks */
@@ -218,6 +224,17 @@ int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay,
  * offset of group (e, src) on owner(e); recv_total: [1] i32 */
 int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out,
                      int32_t* offsets, int32_t* recv_total, void* stream);
+/* K1 + K5a in one cooperative launch (HTRank.open_round, ht.py:335-368):
+ * validation + routing layout into `lay` (tok_slot required), the metadata
+ * all-gather and the group offsets [E, N].  host_meta: device-accessible
+ * pinned host memory of N*(E+N) + 2 i32 = the metadata rows, the receive
+ * total, then the group's error word, written by the kernel (read them
+ * after synchronising `stream`; a nonzero error word means the round did
+ * not open: poll and clear it with epb_group_poll_error).  Requires every
+ * rank's kernel to be able to run concurrently (ranks on distinct GPUs, or
+ * N = 1); ranks emulated on one GPU use the separate launches. */
+int epb_ht_open(epb_group* g, uint32_t round, const int64_t* topk_idx, int32_t b,
+                const epb_layout* lay, int32_t* host_meta, int32_t* offsets, void* stream);
 /* K5b: HT dispatch (ht.py:381-583).  phases: SEND writes one record per
  * (token, remote destination) and places rows for this rank's own experts
  * directly in `out`; RECV waits for every source and scatters record rows to

@@ -101,12 +101,14 @@ SIGNATURES = {
     "epb_group_set_trace": [_P, _P],
     "epb_group_barrier": [_P, _P],
     "epb_group_poll_error": [_P, ctypes.c_int, ctypes.POINTER(_I)],
+    "epb_group_error_word": [_P, ctypes.POINTER(ctypes.c_void_p)],
     "epb_group_destroy": [_P],
     "epb_routing_layout": [_P, _P, _I, ctypes.POINTER(Layout), _P],
     "epb_ll_dispatch": [_P, _P, _I, ctypes.c_void_p, _P],
     "epb_ll_combine": [_P, _P, _I, ctypes.c_void_p, _P],
     "epb_ht_meta_send": [_P, _U, ctypes.POINTER(Layout), _P],
     "epb_ht_meta_recv": [_P, _U, _P, _P, _P, _P],
+    "epb_ht_open": [_P, _U, _P, _I, ctypes.POINTER(Layout), _P, _P, _P],
     "epb_ht_dispatch": [_P, _U, _I, ctypes.c_void_p, _P],
     "epb_ht_combine": [_P, _U, _I, ctypes.c_void_p, _P],
     "epb_weights_equal": [_P, _P, _P, _L, _P],

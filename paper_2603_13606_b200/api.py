@@ -220,6 +220,10 @@ class EpGroup:
         self.strict = strict
         self._marks = None
         self._scratch_pool: dict = {}
+        # pinned host mirror of the device error word (read after a sync)
+        word = ctypes.c_void_p()
+        _lib.call("epb_group_error_word", cgroup, ctypes.byref(word))
+        self._err_word = ctypes.c_int32.from_address(word.value)
         self.device = torch.device("cuda", torch.cuda.current_device())
         self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         # the group's kernels go to whatever stream is current at the call
@@ -322,8 +326,10 @@ class EpGroup:
         routing validation, weight mismatch).  The whole device is
         synchronised: the group's kernels may have gone to any stream that
         was current at the call (ProcessFabric follows the caller's stream)."""
-        code = ctypes.c_int32(0)
         torch.cuda.synchronize(self.device)
+        if self._err_word.value == 0:  # the kernels mirror any failure to host memory
+            return
+        code = ctypes.c_int32(0)
         _lib.call("epb_group_poll_error", self._g, 1, ctypes.byref(code))
         if code.value:
             raise_status(code.value, "device-side failure recorded by the EP kernels")
@@ -380,7 +386,6 @@ class EpGroup:
         handle = EpHandle(self, routing)
         with self._on_stream():
             if self.config.algorithm is Algorithm.HT:
-                handle._run_layout()
                 self._open_ht_round(handle)
             elif self.strict:
                 # the LL dispatch kernel validates and lays out the routing
@@ -645,12 +650,22 @@ class EpHandle:
             g._ht_bufs = (mt, torch.empty((e, n), dtype=torch.int32, device=g.device),
                           ctypes.c_void_p(mt.data_ptr()), ctypes.c_void_p(mt.data_ptr() + nm * 4))
         mt, offsets, meta_p, total_p = g._ht_bufs
-        g._launch("epb_ht_meta_send", g._g, rnd, ctypes.byref(self._lay), self._sp())
-        g.fabric.phase(g.rank)
-        g._launch("epb_ht_meta_recv", g._g, rnd, meta_p, _ptr(offsets), total_p, self._sp())
-        host = g._pinned_i32(nm + 1)
-        host.copy_(mt, non_blocking=True)
-        g.check()  # one synchronisation: receive shapes are host-known on return (api.py:235-237)
+        host = g._pinned_i32(nm + 2)
+        if g._fused_ok():
+            # layout + metadata all-gather in one launch, the shapes written
+            # straight into pinned host memory with the error word after them
+            g._launch("epb_ht_open", g._g, rnd, _ptr(self.routing), self._b, ctypes.byref(self._lay),
+                      ctypes.c_void_p(host.data_ptr()), _ptr(offsets), self._sp())
+            g.check()  # one synchronisation: receive shapes are host-known on return (api.py:235-237)
+        else:
+            # ranks emulated on one GPU: every rank's row is sent before any
+            # rank waits for its peers'
+            self._run_layout()
+            g._launch("epb_ht_meta_send", g._g, rnd, ctypes.byref(self._lay), self._sp())
+            g.fabric.phase(g.rank)
+            g._launch("epb_ht_meta_recv", g._g, rnd, meta_p, _ptr(offsets), total_p, self._sp())
+            host[:nm + 1].copy_(mt, non_blocking=True)
+            g.check()  # one synchronisation: receive shapes are host-known on return (api.py:235-237)
         meta_h = host.numpy()[:nm].reshape(n, e + n).astype(np.int64)
         ell = cfg.experts_per_rank
         lo = g.rank * ell

@@ -81,6 +81,20 @@ EPB_DEV void st_na_v4(void* p, int4 v) {
 
 // Bounded spin on a tagged flag.  Returns false (and records
 // EPB_TRANSPORT_CLOSED, the analogue of fabric.py:284-291) on timeout.
+// Record the first failure in the group's error word err[0].  err[2..3]
+// hold the device address of a mapped pinned host mirror (or 0): the winner
+// also writes the code there, so the host learns "no failure" from one host
+// read after a synchronisation instead of a device->host copy.
+EPB_DEV void raise_err(int* err, int code) {
+  if (atomicCAS(err, 0, code) == 0) {
+    int* mirror = reinterpret_cast<int*>(*reinterpret_cast<volatile unsigned long long*>(err + 2));
+    if (mirror != nullptr) {
+      __threadfence_system();
+      *reinterpret_cast<volatile int*>(mirror) = code;
+    }
+  }
+}
+
 EPB_DEV bool wait_tag(const uint64_t* flag, uint32_t tag, int shift, uint32_t mask,
                       uint64_t timeout_ns, int* err, uint64_t* value_out) {
   uint64_t start = 0;
@@ -95,7 +109,7 @@ EPB_DEV bool wait_tag(const uint64_t* flag, uint32_t tag, int shift, uint32_t ma
     if (++spins == 64) start = globaltimer();
     if (spins > 64 && (spins & 255) == 0) {
       if (globaltimer() - start > timeout_ns) {
-        atomicCAS(err, 0, EPB_TRANSPORT_CLOSED);
+        raise_err(err, EPB_TRANSPORT_CLOSED);
         return false;
       }
     }

@@ -171,6 +171,7 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
     if (g->d_scratch) cudaFree(g->d_scratch);
     if (g->d_seq) cudaFree(g->d_seq);
     if (g->d_lay) cudaFree(g->d_lay);
+    if (g->h_err) cudaFreeHost(g->h_err);
     delete g;
     return code;
   };
@@ -203,6 +204,15 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
   if (e == cudaSuccess) e = cudaMemsetAsync(g->d_done, 0, sizeof(int) * 4 * n, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->d_scratch, 0, sizeof(int) * (8 * n + 2 * l * n + 64), s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  // host mirror of the error word (raise_err, common.cuh): its device
+  // address lives in d_err[2..3]
+  if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&g->h_err), 16, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    g->h_err[0] = 0;
+    void* dp = nullptr;
+    e = cudaHostGetDevicePointer(&dp, g->h_err, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_err + 2, &dp, sizeof(dp), cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) return cleanup(cuda_check(e, "group setup"));
   if (const char* t = getenv("EPB_TIMEOUT_MS")) g->timeout_ns = strtoull(t, nullptr, 10) * 1000000ull;
   // a single rank is its own peer
@@ -319,7 +329,16 @@ int epb_group_poll_error(epb_group* g, int clear, int32_t* code) {
   int v = 0;
   EPB_CUDA(cudaMemcpy(&v, g->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   *code = v;
-  if (clear && v) EPB_CUDA(cudaMemset(g->d_err, 0, sizeof(int)));
+  if (clear && v) {
+    EPB_CUDA(cudaMemset(g->d_err, 0, sizeof(int)));
+    reinterpret_cast<volatile int*>(g->h_err)[0] = 0;
+  }
+  return EPB_OK;
+}
+
+int epb_group_error_word(epb_group* g, const int32_t** host_word) {
+  if (!g || !host_word) return fail(EPB_INVALID_ARGUMENT, "null argument");
+  *host_word = g->h_err;
   return EPB_OK;
 }
 
@@ -334,6 +353,7 @@ int epb_group_destroy(epb_group* g) {
   cudaFree(g->d_scratch);
   cudaFree(g->d_seq);
   cudaFree(g->d_lay);
+  cudaFreeHost(g->h_err);
   delete g;
   return EPB_OK;
 }

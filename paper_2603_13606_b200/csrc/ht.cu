@@ -27,8 +27,14 @@
 //  * single-node transport only: the reference's rail FIFOs / forwarders
 //    (ht.py:479-551) are out of scope on one NVSwitch domain, but the
 //    hierarchical SUM ORDER is reproduced for any ranks_per_node.
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
+
 #include "common.cuh"
 #include "internal.h"
+#include "layout.cuh"
 
 namespace epb {
 
@@ -62,9 +68,10 @@ struct HTMetaSend {
   uint32_t tag;
 };
 
-__global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
+// block-wide: this rank's row (m | q) into every peer's metadata slot, then
+// one release and the per-source tags
+EPB_DEV void meta_send_block(const HTMetaSend& p) {
   const HTGeom& g = p.g;
-  if (*reinterpret_cast<const volatile int*>(p.err) != 0) return;
   const int C = g.E + g.N;
   const uint64_t row_off = g.meta + ((uint64_t)p.parity * g.N + p.rank) * C * 4;
   for (int i = threadIdx.x; i < g.N * C; i += blockDim.x) {
@@ -83,6 +90,11 @@ __global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
   }
 }
 
+__global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
+  if (*reinterpret_cast<const volatile int*>(p.err) != 0) return;
+  meta_send_block(p);
+}
+
 struct HTMetaRecv {
   const uint8_t* win;
   int32_t* meta_out;
@@ -95,8 +107,9 @@ struct HTMetaRecv {
   uint32_t tag;
 };
 
-__global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
-  extern __shared__ int32_t s_meta[];  // [N][C]
+// block-wide: wait for every source's row, then the group offsets and this
+// rank's receive total (s_meta: [N*C + E] ints of shared memory)
+EPB_DEV void meta_recv_block(const HTMetaRecv& p, int32_t* s_meta) {
   const HTGeom& g = p.g;
   const int N = g.N, E = g.E, C = E + N, L = g.L;
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(p.win + g.meta_flag) + p.parity * N;
@@ -146,6 +159,137 @@ __global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
       p.offsets[e * N + s] = base;
       base += s_meta[s * C + e];
     }
+  }
+}
+
+__global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
+  extern __shared__ int32_t s_meta[];  // [N][C]
+  meta_recv_block(p, s_meta);
+}
+
+// ---------------------------------------------------------------------------
+// K1 + K5a fused: HTRank.open_round (ht.py:335-368) in ONE launch.  CTA c
+// lays out tokens [c*kLayChunk, (c+1)*kLayChunk) (validation, local ranks
+// and slots, per-chunk column histogram); grid barrier; the column prefix
+// over chunks is spread over every warp of the grid (m, q); grid barrier;
+// every CTA adds its chunk bases while CTA 0 sends this rank's metadata row,
+// waits for every source's and writes the receive shapes straight into
+// host-mapped pinned memory, followed by the group's error word, so the
+// host reads the round's shapes after one stream synchronisation and no
+// copy.  Same integers as the three-kernel K1 + the K5a pair.  All CTAs are
+// co-resident (cooperative launch); the two barrier words are reset by the
+// last CTA out.
+struct HTOpen {
+  const int64_t* topk;
+  int b, K, L, chunk;  // tokens per CTA (one CTA: chunk = b)
+  int32_t* hist;  // [grid][E+N] per-chunk column histograms, then their exclusive prefixes
+  int32_t* tok_rank;
+  int32_t* tok_slot;
+  unsigned* bar;  // [2]: arrivals, exits
+  HTMetaSend ms;  // m/q = the layout's outputs
+  HTMetaRecv mr;  // meta_out / recv_total in host-mapped memory
+  int32_t* host_err;
+  uint64_t* stamps;  // optional [grid][16] %globaltimer checkpoints (diagnostics, epb_group_set_trace)
+};
+
+#define OPEN_STAMP(I) \
+  do { if (p.stamps && threadIdx.x == 0) p.stamps[blockIdx.x * 16 + (I)] = globaltimer(); } while (0)
+
+EPB_DEV void grid_arrive_wait(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) ht_open_kernel(HTOpen p) {
+  extern __shared__ int smem[];
+  const HTGeom& g = p.ms.g;
+  const int E = g.E, N = g.N, C = E + N;
+  const int G = gridDim.x;
+  OPEN_STAMP(0);
+  // (1) chunk layout (one CTA: the whole routing, final m / q directly)
+  const int t0 = blockIdx.x * p.chunk, bc = max(0, min(p.chunk, p.b - t0));
+  const int64_t* tk = p.topk + (int64_t)t0 * p.K;
+  int32_t* h = p.hist + (int64_t)blockIdx.x * C;
+  int32_t* m_out = G == 1 ? const_cast<int32_t*>(p.ms.m) : h;
+  int32_t* q_out = G == 1 ? const_cast<int32_t*>(p.ms.q) : h + E;
+  const BlockLayoutSmem sm = BlockLayoutSmem::carve(smem, blockDim.x >> 5, E, N);
+  if (!block_layout_checked(tk, bc, p.K, E, N, p.L, sm, m_out, q_out, p.tok_rank + (int64_t)t0 * p.K,
+                            p.tok_slot + (int64_t)t0 * N, p.stamps ? p.stamps + blockIdx.x * 16 + 10 : nullptr) &&
+      threadIdx.x == 0)
+    raise_err(p.mr.err, EPB_INVALID_ARGUMENT);
+  OPEN_STAMP(1);
+  if (G > 1) grid_arrive_wait(p.bar, G);
+  else __syncthreads();
+  OPEN_STAMP(2);
+  // (2) exclusive prefix of every column over the chunks: one warp per column
+  if (G > 1) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < C; c += G * wpb) {
+      int carry = 0;
+      for (int j0 = 0; j0 < G; j0 += 32) {
+        const int j = j0 + lane;
+        const int v = j < G ? __ldcg(&p.hist[(int64_t)j * C + c]) : 0;
+        int incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
+        if (j < G) p.hist[(int64_t)j * C + c] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) {
+        if (c < E) const_cast<int32_t*>(p.ms.m)[c] = carry;
+        else const_cast<int32_t*>(p.ms.q)[c - E] = carry;
+      }
+    }
+  }
+  OPEN_STAMP(3);
+  if (G > 1) grid_arrive_wait(p.bar, 2 * G);
+  OPEN_STAMP(4);
+  const bool bad = *reinterpret_cast<const volatile int*>(p.mr.err) != 0;
+  // (3) chunk bases into this CTA's ranks and slots
+  if (!bad && bc > 0 && G > 1) {
+    const int32_t* base = p.hist + (int64_t)blockIdx.x * C;
+    for (int i = threadIdx.x; i < bc * p.K; i += blockDim.x) {
+      const int e = (int)tk[i];
+      p.tok_rank[(int64_t)t0 * p.K + i] += __ldcg(&base[e]);
+    }
+    for (int i = threadIdx.x; i < bc * N; i += blockDim.x) {
+      int32_t* sl = p.tok_slot + (int64_t)t0 * N + i;
+      const int v = *sl;
+      if (v >= 0) *sl = v + __ldcg(&base[E + i % N]);
+    }
+  }
+  // (4) CTA 0: the metadata all-gather (a rejected routing sends nothing)
+  OPEN_STAMP(5);
+  if (blockIdx.x == 0) {
+    if (!bad) {
+      meta_send_block(p.ms);
+      OPEN_STAMP(6);
+      meta_recv_block(p.mr, smem);
+    }
+    __syncthreads();
+    OPEN_STAMP(7);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      *reinterpret_cast<volatile int32_t*>(p.host_err) = *reinterpret_cast<const volatile int*>(p.mr.err);
+    }
+  }
+  OPEN_STAMP(8);
+  // the last CTA out resets the barrier words for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(p.bar + 1, 1u) == (unsigned)G - 1) {
+    p.bar[0] = 0u;
+    p.bar[1] = 0u;
   }
 }
 
@@ -784,7 +928,7 @@ __global__ void __launch_bounds__(kHTThreads, 1) ht_combine_recv_kernel(HTCombRe
     if (s == me) continue;
     if (!wait_tag(&flags[s], p.tag, 32, 0xFFFFFFFFu, p.timeout_ns, p.err, &v)) { fail = true; continue; }
     // every rank must combine in the same dtype (the rows are raw bytes)
-    if ((int)((v >> 28) & 0xF) != IT) { atomicCAS(p.err, 0, EPB_TAG_MISMATCH); fail = true; }
+    if ((int)((v >> 28) & 0xF) != IT) { raise_err(p.err, EPB_TAG_MISMATCH); fail = true; }
   }
   if (__syncthreads_or(fail)) return;
   const uint8_t* crow = p.win + g.crow;
@@ -947,7 +1091,7 @@ __global__ void __launch_bounds__(kHTThreads, 1) ht_combine_recv_kernel(HTCombRe
 
 __global__ void weights_equal_kernel(const float* a, const float* b, int64_t n, int* err) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (__float_as_uint(a[i]) != __float_as_uint(b[i]) && !(a[i] == b[i])) atomicCAS(err, 0, EPB_INVALID_ARGUMENT);
+    if (__float_as_uint(a[i]) != __float_as_uint(b[i]) && !(a[i] == b[i])) raise_err(err, EPB_INVALID_ARGUMENT);
 }
 
 }  // namespace epb
@@ -1038,6 +1182,73 @@ int epb_ht_meta_recv(epb_group* g, uint32_t round, int32_t* meta_out, int32_t* o
   EPB_CUDA(cudaFuncSetAttribute(ht_meta_recv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ht_meta_recv_kernel<<<1, 1024, smem, as_stream(stream)>>>(p);
   EPB_LAUNCH_CHECK();
+  return EPB_OK;
+}
+
+int epb_ht_open(epb_group* g, uint32_t round, const int64_t* topk_idx, int32_t b, const epb_layout* lay,
+                int32_t* host_meta, int32_t* offsets, void* stream) {
+  if (int rc = check_ht(g, 3)) return rc;
+  if (!lay || !host_meta || !offsets) return fail(EPB_INVALID_ARGUMENT, "null argument");
+  if (b < 0 || b > g->cfg.max_tokens_per_rank)
+    return fail(EPB_INVALID_ARGUMENT, "token count exceeds max_tokens_per_rank");
+  if (!g->d_lay || !lay->tok_slot) return fail(EPB_INVALID_ARGUMENT, "layout needs per-token slots");
+  const int E = g->ht.E, N = g->ht.N;
+  const int C = E + N;
+  // 128-token chunks, 256 threads each (one chunk: no grid barriers).
+  // EPB_OPEN_SINGLE=n lays out up to n tokens in one CTA of 1024 threads
+  // instead (measured slower at 4096 tokens: 44 vs 5.5 us, the per-SM
+  // shared-atomic rate bounds the layout passes; tools/ht_handle_profile.py)
+  static const int kOpenSingle = [] {
+    const char* e = getenv("EPB_OPEN_SINGLE");
+    return e ? atoi(e) : 0;
+  }();
+  const bool single = b <= kOpenSingle;
+  int thr = single ? 1024 : 256;
+  while (thr > 128 && BlockLayoutSmem::bytes(thr / 32, E, N) > 200 * 1024) thr >>= 1;
+  const size_t smem = std::max(BlockLayoutSmem::bytes(thr / 32, E, N), sizeof(int32_t) * ((size_t)N * C + E));
+  if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "metadata too large");
+  HTOpen p;
+  p.topk = topk_idx; p.b = b; p.K = g->cfg.top_k; p.L = g->ht.L;
+  p.chunk = single ? std::max(1, b) : kLayChunk;
+  const int grid = single ? 1 : (b + kLayChunk - 1) / kLayChunk;
+  p.hist = g->d_lay; p.tok_rank = lay->tok_rank; p.tok_slot = lay->tok_slot;
+  p.bar = reinterpret_cast<unsigned*>(g->d_scratch) + 8;
+  p.ms.err = g->d_err; p.ms.m = lay->expert_count; p.ms.q = lay->rank_count; p.ms.peers = g->d_peers;
+  p.ms.g = g->ht; p.ms.rank = g->rank; p.ms.parity = round & 1; p.ms.tag = ht_tag(round);
+  p.mr.win = g->window; p.mr.meta_out = host_meta; p.mr.offsets = offsets; p.mr.recv_total = host_meta + N * C;
+  p.mr.err = g->d_err; p.mr.g = g->ht; p.mr.timeout_ns = g->timeout_ns; p.mr.rank = g->rank;
+  p.mr.parity = round & 1; p.mr.tag = ht_tag(round);
+  p.host_err = host_meta + N * C + 1;
+  p.stamps = g->trace;
+  static std::mutex mu;
+  struct OpenState { size_t smem = 0; int per_sm = 0, sms = 0; };
+  static std::unordered_map<int, OpenState> state;  // per device: smem opted in, co-resident CTAs
+  int dev = 0;
+  EPB_CUDA(cudaGetDevice(&dev));
+  int cap = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    OpenState& st = state[dev];
+    if (st.smem < smem) {
+      EPB_CUDA(cudaFuncSetAttribute(ht_open_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      EPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&st.per_sm, ht_open_kernel, 256, smem));
+      EPB_CUDA(cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev));
+      st.smem = smem;
+    }
+    cap = st.per_sm * st.sms;
+  }
+  if (!single && cap < grid) return fail(EPB_CAPACITY_EXCEEDED, "routing too large for one co-resident grid");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(thr);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  EPB_CUDA(cudaLaunchKernelEx(&cfg, ht_open_kernel, p));
   return EPB_OK;
 }
 

@@ -18,7 +18,8 @@ struct epb_group {
   void* alloc_base = nullptr;   // allocation holding `window` (for IPC)
   uint64_t* d_peers = nullptr;  // [N] window bases as seen from this GPU
   std::vector<void*> ipc_opened;
-  int* d_err = nullptr;         // device error word
+  int* d_err = nullptr;         // device error word [4]: code, -, mirror address
+  int* h_err = nullptr;         // mapped pinned host mirror of the code (raise_err)
   int* d_done = nullptr;        // [2*N] arrival counters (dispatch, combine)
   int* d_scratch = nullptr;     // [8*N + 2*L*N + 64] small per-call state
   uint32_t* d_seq = nullptr;    // [kLLGrid] LL round sequence, one copy per dispatch CTA

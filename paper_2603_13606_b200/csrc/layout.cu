@@ -14,15 +14,9 @@ __global__ void __launch_bounds__(1024)
 routing_layout_kernel(const int64_t* __restrict__ topk, int b, int K, int E, int N, int L,
                       int32_t* m_out, int32_t* q_out, int32_t* tok_rank, int32_t* tok_slot, int* err) {
   extern __shared__ int smem[];
-  __shared__ int s_bad;
-  if (!block_validate(topk, b, K, E, &s_bad)) {
-    if (threadIdx.x == 0) atomicCAS(err, 0, EPB_INVALID_ARGUMENT);
-    return;
-  }
-  BlockLayoutSmem sm;
-  sm.hist = smem;
-  sm.ballot = reinterpret_cast<uint32_t*>(smem + (blockDim.x >> 5) * (E + N));
-  block_layout(topk, b, K, E, N, L, sm, m_out, q_out, tok_rank, tok_slot, nullptr);
+  const BlockLayoutSmem sm = BlockLayoutSmem::carve(smem, blockDim.x >> 5, E, N);
+  if (!block_layout_checked(topk, b, K, E, N, L, sm, m_out, q_out, tok_rank, tok_slot) && threadIdx.x == 0)
+    raise_err(err, EPB_INVALID_ARGUMENT);
 }
 
 // Multi-CTA form for large batches: (1) CTA c lays out tokens
@@ -34,18 +28,13 @@ __global__ void __launch_bounds__(256)
 layout_chunk_kernel(const int64_t* __restrict__ topk, int b, int K, int E, int N, int L, int chunk, int32_t* hist,
                     int32_t* tok_rank, int32_t* tok_slot, int* err) {
   extern __shared__ int smem[];
-  __shared__ int s_bad;
   const int t0 = blockIdx.x * chunk, bc = min(chunk, b - t0);
   const int64_t* tk = topk + (int64_t)t0 * K;
-  if (!block_validate(tk, bc, K, E, &s_bad)) {
-    if (threadIdx.x == 0) atomicCAS(err, 0, EPB_INVALID_ARGUMENT);
-    return;
-  }
-  BlockLayoutSmem sm;
-  sm.hist = smem;
-  sm.ballot = reinterpret_cast<uint32_t*>(smem + (blockDim.x >> 5) * (E + N));
+  const BlockLayoutSmem sm = BlockLayoutSmem::carve(smem, blockDim.x >> 5, E, N);
   int32_t* h = hist + (int64_t)blockIdx.x * (E + N);
-  block_layout(tk, bc, K, E, N, L, sm, h, h + E, tok_rank + (int64_t)t0 * K, tok_slot + (int64_t)t0 * N, nullptr);
+  if (!block_layout_checked(tk, bc, K, E, N, L, sm, h, h + E, tok_rank + (int64_t)t0 * K,
+                            tok_slot + (int64_t)t0 * N) && threadIdx.x == 0)
+    raise_err(err, EPB_INVALID_ARGUMENT);
 }
 
 // one warp per column: 32 chunks per step loaded at once, shuffle scan

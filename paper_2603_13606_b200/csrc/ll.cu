@@ -93,7 +93,7 @@ EPB_DEV bool wait_arrivals(const uint64_t* c, uint64_t need, bool sys, uint64_t 
     if (*(volatile int*)err != 0) return false;
     if (spins == 63) start = globaltimer();
     if (spins > 64 && (spins & 255) == 255 && globaltimer() - start > timeout_ns) {
-      atomicCAS(err, 0, EPB_TRANSPORT_CLOSED);
+      raise_err(err, EPB_TRANSPORT_CLOSED);
       return false;
     }
   }
@@ -686,7 +686,7 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
       p.counts_i32[l * N + me] = m;
       p.counts_f32[l * N + me] = (float)m;
     }
-    if (bad && tid == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
+    if (bad && tid == 0) raise_err(p.err, EPB_INVALID_ARGUMENT);
   }
   (void)nw;
   return bad;
@@ -1032,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         p.counts_i32[l * N + me] = m;
         p.counts_f32[l * N + me] = (float)m;
       }
-      if (bad && threadIdx.x == 0) atomicCAS(p.err, 0, EPB_INVALID_ARGUMENT);
+      if (bad && threadIdx.x == 0) raise_err(p.err, EPB_INVALID_ARGUMENT);
     }
     // publish: one release per CTA, one arrival per destination
     ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, G);
@@ -1070,7 +1070,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         if (!s_ok) return;
         const uint32_t* crow = crows + s * R;
         if (crow[L] == kPoison) {
-          if (threadIdx.x == 0) atomicCAS(p.err, 0, EPB_TRANSPORT_CLOSED);
+          if (threadIdx.x == 0) raise_err(p.err, EPB_TRANSPORT_CLOSED);
           return;
         }
         if ((int)blockIdx.x == s % G)
@@ -1143,7 +1143,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       }
       const uint32_t tok = hdr[0];
       if (q == kPoison) {
-        if (lane == 0) atomicCAS(p.err, 0, EPB_TRANSPORT_CLOSED);
+        if (lane == 0) raise_err(p.err, EPB_TRANSPORT_CLOSED);
         return;
       }
       if (j == 0 && half == 0)
