@@ -151,6 +151,21 @@ int epb_group_set_trace(epb_group* g, uint64_t* trace);
 int epb_group_barrier(epb_group* g, void* stream);
 /* reads (and with clear!=0 resets) the device error word; synchronises */
 int epb_group_poll_error(epb_group* g, int clear, int32_t* code);
+/* Op trace (the reference fabric's trace sink, fabric.py:83-111,186-201):
+ * with a ring set, every transport kernel appends one record per window
+ * transfer — a row record or count row stored into a peer's window (put), a
+ * row read from a peer's window by a pulled transport (get), an arrival
+ * counter add or flag store (signal).  ring: device memory of 4 + 4 *
+ * capacity u64; ring[0] counts appended records (records past `capacity`
+ * are dropped, the count still grows); record i = ring[4 + 4i ..]:
+ *   w0 = op (1 put, 2 signal, 3 get) | window << 4 | src << 8 | dst << 20
+ *        | signal_id << 32;  w1 = byte offset in dst's window;
+ *   w2 = length in bytes;  w3 = signal value.
+ * src is the initiating rank, dst the rank whose window is addressed.
+ * Signal ids: LL dispatch arrivals parity*N + src, LL combine arrivals
+ * 2N + parity*N + src; HT metadata flags parity*N + src, HT dispatch flags
+ * 2N + src, HT combine flags 3N + src.  NULL ring: tracing off. */
+int epb_group_set_op_trace(epb_group* g, uint64_t* ring, uint32_t capacity);
 /* Host address of a pinned mirror of the error word: the kernel recording
  * a failure also writes its code there, so after synchronising the group's
  * streams a zero read means no failure was recorded (a nonzero one is

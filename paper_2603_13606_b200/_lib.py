@@ -102,6 +102,7 @@ SIGNATURES = {
     "epb_group_barrier": [_P, _P],
     "epb_group_poll_error": [_P, ctypes.c_int, ctypes.POINTER(_I)],
     "epb_group_error_word": [_P, ctypes.POINTER(ctypes.c_void_p)],
+    "epb_group_set_op_trace": [_P, _P, _U],
     "epb_group_destroy": [_P],
     "epb_routing_layout": [_P, _P, _I, ctypes.POINTER(Layout), _P],
     "epb_ll_dispatch": [_P, _P, _I, ctypes.c_void_p, _P],

@@ -21,6 +21,7 @@ working unchanged):
 from __future__ import annotations
 
 import ctypes
+import warnings
 import weakref
 from dataclasses import dataclass
 from enum import Enum
@@ -226,6 +227,13 @@ class EpGroup:
         self._err_word = ctypes.c_int32.from_address(word.value)
         self.device = torch.device("cuda", torch.cuda.current_device())
         self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        # op trace (fabric `trace`): a device ring the kernels append to,
+        # drained into the fabric's sink after every call
+        self._op_ring = None
+        sink = getattr(fabric, "trace", None)
+        if sink is not None and sink.active:
+            self._op_ring = torch.zeros(4 + 4 * sink.capacity, dtype=torch.int64, device=self.device)
+            _lib.call("epb_group_set_op_trace", cgroup, ctypes.c_void_p(self._op_ring.data_ptr()), sink.capacity)
         # the group's kernels go to whatever stream is current at the call
         self._follows_current = bool(getattr(fabric, "process_mode", False)) or config.num_ranks == 1
         self._call_sp = 0  # raw stream of the call in progress (set by _on_stream)
@@ -318,8 +326,26 @@ class EpGroup:
         scope only looks up the raw current stream once per call."""
         if self._follows_current:
             self._call_sp = _raw_current_stream(self._dev_index)
-            return _NULL_SCOPE
-        return _StreamScope(self)
+            scope = _NULL_SCOPE
+        else:
+            scope = _StreamScope(self)
+        return scope if self._op_ring is None else _TraceScope(self, scope)
+
+    def _drain_ops(self) -> None:
+        """Hand the op records of the call just made to the fabric's trace
+        sink (waits for the call's kernels)."""
+        ring = self._op_ring
+        torch.cuda.current_stream(self.device).synchronize()
+        n = int(ring[0].item())
+        if n == 0:
+            return
+        sink = self.fabric.trace
+        m = min(n, sink.capacity)
+        recs = ring[4:4 + 4 * m].view(m, 4).cpu().numpy().view(np.uint64)
+        ring[0].zero_()
+        sink.emit(recs, dropped=n - m)
+        if n > m:
+            warnings.warn(f"op trace: {n - m} records beyond the ring capacity {sink.capacity} were dropped")
 
     def check(self) -> None:
         """Synchronise and raise any error the kernels recorded (timeouts,
@@ -445,6 +471,23 @@ class _NullScope:
 
 
 _NULL_SCOPE = _NullScope()
+
+
+class _TraceScope:
+    """A call scope that drains the op trace when the call's work is issued."""
+
+    def __init__(self, group, inner):
+        self._g = group
+        self._inner = inner
+
+    def __enter__(self):
+        self._inner.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        self._inner.__exit__(*exc)
+        self._g._drain_ops()
+        return False
 
 
 class _StreamScope:

@@ -81,6 +81,35 @@ EPB_DEV void st_na_v4(void* p, int4 v) {
 
 // Bounded spin on a tagged flag.  Returns false (and records
 // EPB_TRANSPORT_CLOSED, the analogue of fabric.py:284-291) on timeout.
+// Op trace: the B200 counterpart of the reference fabric's per-op log
+// (fabric.py:104-111, one CSV line per put / signal / lsa_store).  When a
+// ring is registered (epb_group_set_op_trace) the transport kernels append
+// one 32-byte record per window transfer they perform: a row record or
+// count row stored into a peer's window (PUT), a row read from a peer's
+// window (GET: pulled transports), an arrival counter add or flag store
+// (SIGNAL).  ring[0] counts appended records (beyond `cap` they are
+// dropped, the count keeps growing); record i is ring[4 + 4i .. 4i + 7]:
+//   w0 = op | window << 4 | src << 8 | dst << 20 | signal_id << 32
+//   w1 = byte offset in dst's window, w2 = length, w3 = signal value.
+// A null ring costs one uniform branch per site.
+enum { EPB_OP_PUT = 1, EPB_OP_SIGNAL = 2, EPB_OP_GET = 3 };
+struct OpTrace {
+  unsigned long long* ring;
+  uint32_t cap;
+};
+EPB_DEV void op_record(const OpTrace& t, int op, int src, int dst, uint64_t off, uint64_t len, uint32_t sig = 0,
+                       uint64_t value = 0) {
+  if (t.ring == nullptr) return;
+  const unsigned long long i = atomicAdd(t.ring, 1ull);
+  if (i >= t.cap) return;
+  unsigned long long* r = t.ring + 4 + 4 * i;
+  r[0] = (unsigned long long)op | ((unsigned long long)(src & 0xfff) << 8) |
+         ((unsigned long long)(dst & 0xfff) << 20) | ((unsigned long long)sig << 32);
+  r[1] = off;
+  r[2] = len;
+  r[3] = value;
+}
+
 // Record the first failure in the group's error word err[0].  err[2..3]
 // hold the device address of a mapped pinned host mirror (or 0): the winner
 // also writes the code there, so the host learns "no failure" from one host

@@ -336,6 +336,14 @@ int epb_group_poll_error(epb_group* g, int clear, int32_t* code) {
   return EPB_OK;
 }
 
+int epb_group_set_op_trace(epb_group* g, uint64_t* ring, uint32_t capacity) {
+  if (!g) return fail(EPB_INVALID_ARGUMENT, "null group");
+  if (ring && capacity == 0) return fail(EPB_INVALID_ARGUMENT, "op trace capacity must be positive");
+  g->op_ring = reinterpret_cast<unsigned long long*>(ring);
+  g->op_cap = ring ? capacity : 0;
+  return EPB_OK;
+}
+
 int epb_group_error_word(epb_group* g, const int32_t** host_word) {
   if (!g || !host_word) return fail(EPB_INVALID_ARGUMENT, "null argument");
   *host_word = g->h_err;

@@ -66,6 +66,7 @@ struct HTMetaSend {
   HTGeom g;
   int rank, parity;
   uint32_t tag;
+  OpTrace ops;
 };
 
 // block-wide: this rank's row (m | q) into every peer's metadata slot, then
@@ -86,6 +87,9 @@ EPB_DEV void meta_send_block(const HTMetaSend& p) {
     for (int d = 0; d < g.N; ++d) {
       uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, d) + g.meta_flag) + p.parity * g.N + p.rank;
       st_relaxed_sys_u64(flag, (uint64_t)p.tag);
+      op_record(p.ops, EPB_OP_PUT, p.rank, d, row_off, 4ull * C);
+      op_record(p.ops, EPB_OP_SIGNAL, p.rank, d, g.meta_flag + 8ull * (p.parity * g.N + p.rank), 8,
+                p.parity * g.N + p.rank, p.tag);
     }
   }
 }
@@ -311,11 +315,14 @@ struct HTSend {
   int b, rank;
   int stage_ready;  // x IS this rank's stage region in the wire dtype
   uint32_t tag;
+  OpTrace ops;
 };
 
 EPB_DEV void ht_publish_records(const HTSend& p, int d) {
   uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, d) + p.g.dflag) + p.rank;
-  st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | (uint32_t)p.q[d]);
+  const uint64_t v = ((uint64_t)p.tag << 32) | (uint32_t)p.q[d];
+  st_relaxed_sys_u64(flag, v);
+  op_record(p.ops, EPB_OP_SIGNAL, p.rank, d, p.g.dflag + 8ull * p.rank, 8, 2 * p.g.N + p.rank, v);
 }
 
 // Send: (1) every token row, converted once to the wire dtype, into this
@@ -400,6 +407,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_send_kernel(HTSend p) 
       if (j < 0) continue;
       uint8_t* rec = hpeer(p.peers, d) + g.rec + (rec0 + j) * g.rec_stride;
       if (lane < nvec) st_plain_v4(rec + 16 * lane, piece);
+      if (lane == 0) op_record(p.ops, EPB_OP_PUT, me, d, g.rec + (uint64_t)(rec0 + j) * g.rec_stride, 16ull * nvec);
     }
   }
   (void)L;
@@ -431,6 +439,7 @@ struct HTRecv {
   uint64_t timeout_ns;
   int rank;
   uint32_t tag;
+  OpTrace ops;
 };
 
 // Receive: every record names a source token and the output rows of this
@@ -493,6 +502,8 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
     const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.WBp);
     const uint8_t* row = hpeer(p.peers, s) + g.stage + (int64_t)hdr[0] * g.RBp;
+    if (half == 0 && lane == 0)  // one record per row pulled from the source's stage
+      op_record(p.ops, EPB_OP_GET, me, s, g.stage + (uint64_t)hdr[0] * g.RBp, (uint64_t)g.RB);
     int e = -1, pos = 0;
     if (lane < K) {
       e = (int)hdr[2 + lane];
@@ -663,6 +674,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(
     const int half = cur & 1;
     const uint8_t* rec = p.win + g.rec + ((int64_t)s * g.B + j) * g.rec_stride;
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec + g.WBp);
+    if (half == 0 && lane == 0)  // one record per row pulled from the source's stage
+      op_record(p.ops, EPB_OP_GET, me, s, g.stage + (uint64_t)hdr[0] * g.RBp, (uint64_t)g.RB);
     int e = -1, pos = 0;
     if (lane < K) {
       e = (int)hdr[2 + lane];
@@ -708,6 +721,7 @@ struct HTCombSend {
   int rows, rank, in_dtype, b;
   int pull;  // expert rows are this rank's window region: homes pull them
   uint32_t tag;
+  OpTrace ops;
 };
 
 EPB_DEV int ht_rows_to(const HTCombSend& p, int s) {
@@ -720,7 +734,9 @@ EPB_DEV int ht_rows_to(const HTCombSend& p, int s) {
 
 EPB_DEV void ht_publish_comb(const HTCombSend& p, int s, int count) {
   uint64_t* flag = reinterpret_cast<uint64_t*>(hpeer(p.peers, s) + p.g.cflag) + p.rank;
-  st_relaxed_sys_u64(flag, ((uint64_t)p.tag << 32) | ((uint64_t)p.in_dtype << 28) | (uint32_t)count);
+  const uint64_t v = ((uint64_t)p.tag << 32) | ((uint64_t)p.in_dtype << 28) | (uint32_t)count;
+  st_relaxed_sys_u64(flag, v);
+  op_record(p.ops, EPB_OP_SIGNAL, p.rank, s, p.g.cflag + 8ull * p.rank, 8, 3 * p.g.N + p.rank, v);
 }
 
 template <int IT>
@@ -738,8 +754,11 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.b * K; i += gridDim.x * blockDim.x) {
       const int e = (int)p.topk[i];
       const uint64_t srow = (uint64_t)(p.offsets[e * N + me] + p.tok_rank[i]);  // row on owner(e)
-      if (p.pull)  // the owner's registered expert-output region, read over NVLink
+      if (p.pull) {  // the owner's registered expert-output region, read over NVLink
         p.row_ptr[i] = reinterpret_cast<uint64_t>(hpeer(p.peers, e / L) + g.yout) + srow * g.yrow;
+        if (e / L != me)  // the receive phase of this op reads it: one record per remote row
+          op_record(p.ops, EPB_OP_GET, me, e / L, g.yout + srow * g.yrow, (uint64_t)bytes);
+      }
       else
         p.row_ptr[i] = e / L == me ? reinterpret_cast<uint64_t>(p.y) + srow * bytes
                                    : reinterpret_cast<uint64_t>(p.win + g.crow + (int64_t)i * g.crow_stride);
@@ -766,6 +785,8 @@ __global__ void __launch_bounds__(kHTThreads) ht_combine_send_kernel(HTCombSend 
     const int t = p.origin[(int64_t)r * 4 + 2];
     const int k = p.origin[(int64_t)r * 4 + 3];
     uint8_t* dst = hpeer(p.peers, s) + g.crow + ((int64_t)t * K + k) * g.crow_stride;
+    if (half == 0 && lane == 0)  // one record per expert row pushed to its token's home
+      op_record(p.ops, EPB_OP_PUT, me, s, g.crow + (uint64_t)((int64_t)t * K + k) * g.crow_stride, (uint64_t)bytes);
     const uint8_t* src = reinterpret_cast<const uint8_t*>(p.y) + (int64_t)r * bytes;
     if (nch) {
       const int per = (nch + 1) / 2;
@@ -1163,6 +1184,7 @@ extern "C" {
 int epb_ht_meta_send(epb_group* g, uint32_t round, const epb_layout* lay, void* stream) {
   if (int rc = check_ht(g, 1)) return rc;
   HTMetaSend p;
+  p.ops = OpTrace{g->op_ring, g->op_cap};
   p.err = g->d_err; p.m = lay->expert_count; p.q = lay->rank_count; p.peers = g->d_peers; p.g = g->ht;
   p.rank = g->rank; p.parity = round & 1; p.tag = ht_tag(round);
   ht_meta_send_kernel<<<1, 256, 0, as_stream(stream)>>>(p);
@@ -1215,6 +1237,7 @@ int epb_ht_open(epb_group* g, uint32_t round, const int64_t* topk_idx, int32_t b
   p.bar = reinterpret_cast<unsigned*>(g->d_scratch) + 8;
   p.ms.err = g->d_err; p.ms.m = lay->expert_count; p.ms.q = lay->rank_count; p.ms.peers = g->d_peers;
   p.ms.g = g->ht; p.ms.rank = g->rank; p.ms.parity = round & 1; p.ms.tag = ht_tag(round);
+  p.ms.ops = OpTrace{g->op_ring, g->op_cap};
   p.mr.win = g->window; p.mr.meta_out = host_meta; p.mr.offsets = offsets; p.mr.recv_total = host_meta + N * C;
   p.mr.err = g->d_err; p.mr.g = g->ht; p.mr.timeout_ns = g->timeout_ns; p.mr.rank = g->rank;
   p.mr.parity = round & 1; p.mr.tag = ht_tag(round);
@@ -1262,6 +1285,7 @@ int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases, const epb_ht_d
   if (phases & 1) {
     if (a->num_tokens > 0 && !a16(a->x)) return fail(EPB_INVALID_ARGUMENT, "x must be 16-byte aligned");
     HTSend p;
+    p.ops = OpTrace{g->op_ring, g->op_cap};
     p.x = a->x; p.w = a->weights; p.topk = a->topk_idx; p.q = a->rank_count; p.tok_rank = a->tok_rank;
     p.tok_slot = a->tok_slot; p.offsets = a->offsets; p.peers = g->d_peers;
     p.done = g->d_done; p.g = g->ht;
@@ -1279,6 +1303,7 @@ int epb_ht_dispatch(epb_group* g, uint32_t round, int32_t phases, const epb_ht_d
   }
   if (phases & 2) {
     HTRecv p;
+    p.ops = OpTrace{g->op_ring, g->op_cap};
     p.peers = g->d_peers; p.q = a->rank_count; p.out = a->out; p.origin = a->origin; p.origin_w = a->origin_w;
     p.win = g->window; p.err = g->d_err;
     p.g = g->ht; p.timeout_ns = g->timeout_ns; p.rank = g->rank; p.tag = ht_tag(round);
@@ -1316,6 +1341,7 @@ int epb_ht_combine(epb_group* g, uint32_t round, int32_t phases, const epb_ht_co
   if (phases & 1) {
     // the metadata rows of this round live in the window (parity = round & 1)
     HTCombSend p;
+    p.ops = OpTrace{g->op_ring, g->op_cap};
     p.err = g->d_err;
     p.y = a->expert_rows; p.origin = a->origin;
     p.meta = reinterpret_cast<const int32_t*>(g->window + g->ht.meta +

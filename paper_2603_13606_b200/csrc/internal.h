@@ -28,6 +28,8 @@ struct epb_group {
   epb::HTGeom ht;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   uint64_t* trace = nullptr;    // optional [grid][16] globaltimer stamps (diagnostics)
+  unsigned long long* op_ring = nullptr;  // optional op trace ring (epb_group_set_op_trace)
+  uint32_t op_cap = 0;
   bool peers_ready = false;
   bool sys_scope = false;       // peers on other GPUs: system-scope fences/flags
   int fence_override = -1;      // EPB_SYS_FENCE: -1 auto, 0 GPU scope, 1 system scope

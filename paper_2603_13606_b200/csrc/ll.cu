@@ -114,7 +114,7 @@ EPB_DEV bool wait_arrivals(const uint64_t* c, uint64_t need, bool sys, uint64_t 
 // All threads call.  `done`: this kind's local counter (reset by the last).
 constexpr int kDirectArrive = 32;
 EPB_DEV void ll_arrive(const uint64_t* peers, uint64_t off, int N, int me, bool fence_sys, bool sys,
-                       unsigned* done, uint32_t chaos_ns, int W) {
+                       unsigned* done, uint32_t chaos_ns, int W, const OpTrace& ops, uint32_t sig_base) {
   __syncthreads();
   if (threadIdx.x != 0 || N == 1) return;
   const int G = gridDim.x, c = blockIdx.x;
@@ -133,7 +133,10 @@ EPB_DEV void ll_arrive(const uint64_t* peers, uint64_t off, int N, int me, bool 
     add = (uint64_t)G;
   }
   for (int d = 0; d < N; ++d)
-    if (d != me) red_arrive(reinterpret_cast<uint64_t*>(peer_base(peers, d) + off) + me, add, sys);
+    if (d != me) {
+      red_arrive(reinterpret_cast<uint64_t*>(peer_base(peers, d) + off) + me, add, sys);
+      op_record(ops, EPB_OP_SIGNAL, me, d, off + 8ull * me, 8, sig_base + me, add);
+    }
 }
 
 // warp: wait until every source in `need` (bit per rank) has arrived; bits
@@ -240,6 +243,7 @@ struct LLDisp {
   uint32_t* dseq;  // [grid] round sequence: CTA c reads and advances its own copy
   unsigned* done;  // local CTA-completion counter of the send phase (ll_arrive)
   uint64_t* trace;
+  OpTrace ops;
   LLGeom g;
   uint64_t timeout_ns;
   int b, rank, phases;
@@ -595,6 +599,9 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
         if (lane < 2 + 2 * K)
           reinterpret_cast<uint32_t*>(peer_base(p.peers, dd) + slot_off + (int64_t)jj * g.slot_stride + g.RBp +
                                       g.SBp)[lane] = word;
+        if (lane == 0)  // one record per (token, destination): row, scales, header
+          op_record(p.ops, EPB_OP_PUT, me, dd, slot_off + (uint64_t)jj * g.slot_stride,
+                    (uint64_t)g.RBp + g.SBp + 4ull * (2 + 2 * K));
       }
     }
     // chunk c to every destination slot and every own-expert output row
@@ -680,6 +687,9 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
       const uint32_t v = bad ? kPoison : (l < L ? (d2 * L + l < E ? (uint32_t)s_m[d2 * L + l] : 0u) : (uint32_t)s_q[d2]);
       reinterpret_cast<uint32_t*>(peer_base(p.peers, d2) + parity_off + g.cnt_row)[me * R + l] = v;
     }
+    if (tid == 0)
+      for (int d2 = 0; d2 < N; ++d2)
+        if (d2 != me) op_record(p.ops, EPB_OP_PUT, me, d2, parity_off + g.cnt_row + 4ull * me * R, 4ull * R);
 #pragma unroll 1
     for (int l = tid; l < L; l += BD) {
       const int m = l < nloc && !bad ? s_m[lo + l] : 0;
@@ -746,7 +756,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const bool bad = ll_send_fast<XT, WT, SC, OT>(p, smem, seq_ld, seq, parity_off);
       // publish: one system-scope release per rank, one arrival per destination
       ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns,
-                fast_units(p.b, gridDim.x, g.H / Elems<WT>::n));
+                fast_units(p.b, gridDim.x, g.H / Elems<WT>::n), p.ops, (seq & 1) * N);
       LL_STAMP(p, 4);
       if (bad) return;
     }
@@ -960,6 +970,10 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
           uint8_t* slot = peer_base(p.peers, s_dst[i]) + slot_off + (int64_t)s_j[i] * g.slot_stride;
           reinterpret_cast<uint32_t*>(slot + g.RBp + g.SBp)[w] = s_hdr[w];
         }
+      if (threadIdx.x == 0)  // one record per (token, destination): row, scales, header
+        for (int i = 0; i < nd; ++i)
+          op_record(p.ops, EPB_OP_PUT, me, s_dst[i], slot_off + (uint64_t)s_j[i] * g.slot_stride,
+                    (uint64_t)g.RBp + g.SBp + 4ull * (2 + 2 * K));
       if (split) {
         if (warp > 0) {
 #pragma unroll
@@ -1027,6 +1041,9 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         const uint32_t v = bad ? kPoison : (l < L ? (d * L + l < E ? (uint32_t)s_m[d * L + l] : 0u) : (uint32_t)s_q[d]);
         reinterpret_cast<uint32_t*>(peer_base(p.peers, d) + parity_off + g.cnt_row)[me * R + l] = v;
       }
+      if (threadIdx.x == 0)
+        for (int d = 0; d < N; ++d)
+          if (d != me) op_record(p.ops, EPB_OP_PUT, me, d, parity_off + g.cnt_row + 4ull * me * R, 4ull * R);
       for (int l = threadIdx.x; l < L; l += blockDim.x) {
         const int m = l < nloc && !bad ? s_m[lo + l] : 0;
         p.counts_i32[l * N + me] = m;
@@ -1035,7 +1052,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       if (bad && threadIdx.x == 0) raise_err(p.err, EPB_INVALID_ARGUMENT);
     }
     // publish: one release per CTA, one arrival per destination
-    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, G);
+    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, G, p.ops, (seq & 1) * N);
     LL_STAMP(p, 4);
     if (bad) return;
   }
@@ -1236,6 +1253,7 @@ struct LLComb {
   int* err;
   unsigned* done;  // local CTA-completion counter of the send phase (ll_arrive)
   uint64_t* trace;
+  OpTrace ops;
   LLGeom g;
   uint64_t timeout_ns;
   int b, rank, phases;
@@ -1325,6 +1343,9 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
                              ? (int64_t)(p.rank * L + l) * B + (int64_t)(((uint64_t)info * g.Kmagic) >> 32)
                              : (int64_t)info;
       uint8_t* dst = peer_base(p.peers, s) + parity_off + g.comb_slot + cs * g.comb_stride;
+      if (lane == 0 && q == 0)  // one record per (token, k) row pushed to its home
+        op_record(p.ops, EPB_OP_PUT, me, s, parity_off + g.comb_slot + (uint64_t)cs * g.comb_stride,
+                  (uint64_t)H * dtype_width(WT));
       const uint8_t* yrow = reinterpret_cast<const uint8_t*>(p.y) + row * H * dtype_width(IT);
       if (vec) {
         const int c0 = q * part, c1 = min(nch, c0 + part);
@@ -1359,7 +1380,8 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // one release per CTA, one arrival per home rank (pulled combine: the
     // expert outputs were written by earlier kernels on this stream — the
     // arrival announces them)
-    ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, send_ctas);
+    ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, send_ctas, p.ops,
+              2 * N + (seq & 1) * N);
     LL_STAMP(p, 3);
   }
 
@@ -1413,6 +1435,9 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
         }
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
         const int cbase = sg * kSeg + lane;
+        if (p.pull && sg == 0 && lane < K && my_owner != me)  // one record per (token, k) row pulled
+          op_record(p.ops, EPB_OP_GET, me, my_owner,
+                    g.yout + (uint64_t)p.owner_row[(int64_t)t * K + lane] * g.yrow, (uint64_t)H * dtype_width(WT));
         const bool ok0 = cbase < nch, ok1 = cbase + 32 < nch;
         const uint8_t* my_row =
             p.pull ? reinterpret_cast<const uint8_t*>(my_pull)
@@ -1488,7 +1513,15 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
       if (s_fail) return;
       for (int t = blockIdx.x; t < p.b; t += gridDim.x) {
         __syncthreads();
-        if ((int)threadIdx.x < K) s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
+        if ((int)threadIdx.x < K) {
+          s_w[threadIdx.x] = p.w[(int64_t)t * K + threadIdx.x];
+          const int k = threadIdx.x;
+          const int e = (int)p.topk[(int64_t)t * K + k];
+          const int ow = (int)(((uint64_t)e * g.Lmagic) >> 32);
+          if (p.pull && ow != me)
+            op_record(p.ops, EPB_OP_GET, me, ow, g.yout + (uint64_t)p.owner_row[(int64_t)t * K + k] * g.yrow,
+                      (uint64_t)H * dtype_width(WT));
+        }
         __syncthreads();
         uint8_t* orow = reinterpret_cast<uint8_t*>(p.out) + (int64_t)t * H * dtype_width(OT);
         for (int el = threadIdx.x; el < H; el += blockDim.x) {
@@ -1717,6 +1750,7 @@ int epb_ll_dispatch(epb_group* g, uint32_t* hseq, int32_t phases, const epb_ll_d
   p.src_info = a->src_info; p.self_row = a->self_row; p.owner_row = a->owner_row;
   p.peers = g->d_peers; p.win = g->window; p.err = g->d_err;
   p.dseq = g->d_seq; p.done = reinterpret_cast<unsigned*>(g->d_scratch) + 4; p.trace = g->trace;
+  p.ops.ring = g->op_ring; p.ops.cap = g->op_cap;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;
   const int E = g->ll.E, N = g->ll.N, K = g->ll.K;
@@ -1762,6 +1796,7 @@ int epb_ll_combine(epb_group* g, const uint32_t* hseq, int32_t phases, const epb
                  g->ll.yout_rows == 0 || a->expert_out != g->window + g->ll.yout))
     return fail(EPB_INVALID_ARGUMENT, "pulled combine needs bf16 rows in the window's expert-output region");
   p.hseq = hseq; p.peers = g->d_peers; p.win = g->window; p.err = g->d_err; p.trace = g->trace;
+  p.ops.ring = g->op_ring; p.ops.cap = g->op_cap;
   p.done = reinterpret_cast<unsigned*>(g->d_scratch) + 5;
   p.g = g->ll; p.timeout_ns = g->timeout_ns; p.b = b; p.rank = g->rank; p.phases = phases;
   p.sys = g->sys_scope;

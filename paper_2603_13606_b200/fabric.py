@@ -14,6 +14,11 @@ kernels; what remains on the host is:
   barriers its rank threads;
 * `stream(rank)`         — where a rank's kernels go.
 
+* `trace`                — optional op log (the reference fabric's trace
+  sink, fabric.py:83-111): a callable receiving one CSV line per transport
+  op, or a file path.  The kernels record their window transfers on the
+  device (epb_group_set_op_trace); the groups drain them after each call.
+
 Two fabrics:
   Fabric(topology)                       N ranks as threads on one GPU
                                          (the reference's test model,
@@ -30,6 +35,68 @@ from dataclasses import dataclass
 import torch
 
 from .core import EpError, ErrorCode
+
+# op codes of the device op-trace records (include/epb200.h)
+OP_PUT, OP_SIGNAL, OP_GET = 1, 2, 3
+DEFAULT_TRACE_CAPACITY = 1 << 17  # records per group per call
+
+
+class TraceSink:
+    """Where op-trace lines go: a callable or a file path, like the
+    reference fabric's `trace` argument (fabric.py:83-111).  Lines follow the
+    reference's columns `op,src,dst,window,offset,len,signal_id,value,seq`:
+      put,src,dst,window,offset,len,,,seq     row record / count row stored
+                                              into dst's window by src
+      get,src,dst,window,offset,len,,,seq     row read from dst's window by
+                                              src (pulled transports; B200)
+      signal,src,dst,,,,signal_id,value,seq   arrival counter add or flag
+                                              store into dst's window
+    `seq` numbers the lines of the whole fabric in the order they were
+    drained (within one kernel the device append order)."""
+
+    def __init__(self, trace, capacity: int = DEFAULT_TRACE_CAPACITY):
+        self._file = None
+        self.capacity = int(capacity)
+        if trace is None:
+            self.fn = None
+        elif callable(trace):
+            self.fn = trace
+        else:
+            self._file = open(trace, "w")
+            self.fn = lambda line: self._file.write(line + "\n")
+        self.seq = 0
+        self.dropped = 0
+        self._lock = threading.Lock()
+
+    @property
+    def active(self) -> bool:
+        return self.fn is not None
+
+    @staticmethod
+    def format(rec, seq: int) -> str:
+        w0, off, ln, val = (int(x) for x in rec)
+        op, wid = w0 & 0xF, (w0 >> 4) & 0xF
+        src, dst, sig = (w0 >> 8) & 0xFFF, (w0 >> 20) & 0xFFF, w0 >> 32
+        if op == OP_SIGNAL:
+            return f"signal,{src},{dst},,,,{sig},{val},{seq}"
+        name = "put" if op == OP_PUT else "get" if op == OP_GET else f"op{op}"
+        return f"{name},{src},{dst},{wid},{off},{ln},,,{seq}"
+
+    def emit(self, records, dropped: int = 0) -> None:
+        """records: [n, 4] uint64 device records (w0, offset, len, value)."""
+        if self.fn is None:
+            return
+        with self._lock:
+            self.dropped += dropped
+            for rec in records:
+                self.seq += 1
+                self.fn(self.format(rec, self.seq))
+
+    def close(self) -> None:
+        if self._file is not None:
+            self._file.close()
+            self._file = None
+            self.fn = None
 
 
 @dataclass(frozen=True)
@@ -82,11 +149,14 @@ class Fabric:
 
     process_mode = False
 
-    def __init__(self, topology: NodeTopology, seed: int = 0, device=None, timeout: float = 120.0, devices=None):
+    def __init__(self, topology: NodeTopology, seed: int = 0, device=None, timeout: float = 120.0, devices=None,
+                 trace=None, trace_capacity: int = DEFAULT_TRACE_CAPACITY):
         """`devices`: one CUDA device per rank — ranks on several GPUs of one
         process (threads; peer windows through peer access, system-scope
-        ordering); default: every rank on `device` (the current one)."""
+        ordering); default: every rank on `device` (the current one).
+        `trace`: op-trace sink (callable or path; TraceSink)."""
         self.topology = topology
+        self.trace = TraceSink(trace, trace_capacity)
         self.seed = seed
         n = topology.num_ranks
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -140,6 +210,7 @@ class Fabric:
     def shutdown(self) -> None:
         self._closed = True
         self._barrier.abort()
+        self.trace.close()
 
 
 class ProcessFabric:
@@ -148,10 +219,12 @@ class ProcessFabric:
 
     process_mode = True
 
-    def __init__(self, topology: NodeTopology, process_group=None):
+    def __init__(self, topology: NodeTopology, process_group=None, trace=None,
+                 trace_capacity: int = DEFAULT_TRACE_CAPACITY):
         import torch.distributed as dist
 
         self.topology = topology
+        self.trace = TraceSink(trace, trace_capacity)
         self.group = process_group
         self._dist = dist
         world = dist.get_world_size(process_group)
@@ -183,4 +256,4 @@ class ProcessFabric:
         return self.registered[rank] if rank == self.rank else 0
 
     def shutdown(self) -> None:
-        return None
+        self.trace.close()

@@ -48,12 +48,13 @@ def dispatch_inputs(cfg, tokens, weights, mode="reference"):
 
 
 def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="reference",
-           wire_out=False, bf16_expert=False, rounds=1, layout="optimized", zero_copy=False):
-    """Returns per rank dict(recv, counts, out, recv_total)."""
+           wire_out=False, bf16_expert=False, rounds=1, layout="optimized", zero_copy=False, trace=None):
+    """Returns per rank dict(recv, counts, out, recv_total).  `trace`: the
+    fabric's op-trace sink."""
     n = cfg.num_ranks
     bmax, h = cfg.max_tokens_per_rank, cfg.hidden
     ell = cfg.experts_per_rank
-    fabric = ep.Fabric(ep.NodeTopology(n, cfg.ranks_per_node))
+    fabric = ep.Fabric(ep.NodeTopology(n, cfg.ranks_per_node), trace=trace)
 
     def body(rank):
         g = ep.create_group(fabric, rank, cfg, layout=layout)
@@ -109,10 +110,10 @@ def run_ll(cfg, tokens, routing, weights, expert_fn, staged=False, mode="referen
         fabric.shutdown()
 
 
-def run_ht(cfg, tokens, routing, weights, expert_fn, bf16_expert=False, zero_copy=False):
+def run_ht(cfg, tokens, routing, weights, expert_fn, bf16_expert=False, zero_copy=False, trace=None):
     n = cfg.num_ranks
     h = cfg.hidden
-    fabric = ep.Fabric(ep.NodeTopology(n, cfg.ranks_per_node))
+    fabric = ep.Fabric(ep.NodeTopology(n, cfg.ranks_per_node), trace=trace)
 
     def body(rank):
         g = ep.create_group(fabric, rank, cfg)
