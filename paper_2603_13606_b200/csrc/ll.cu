@@ -599,9 +599,6 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
         if (lane < 2 + 2 * K)
           reinterpret_cast<uint32_t*>(peer_base(p.peers, dd) + slot_off + (int64_t)jj * g.slot_stride + g.RBp +
                                       g.SBp)[lane] = word;
-        if (lane == 0)  // one record per (token, destination): row, scales, header
-          op_record(p.ops, EPB_OP_PUT, me, dd, slot_off + (uint64_t)jj * g.slot_stride,
-                    (uint64_t)g.RBp + g.SBp + 4ull * (2 + 2 * K));
       }
     }
     // chunk c to every destination slot and every own-expert output row
@@ -687,9 +684,7 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
       const uint32_t v = bad ? kPoison : (l < L ? (d2 * L + l < E ? (uint32_t)s_m[d2 * L + l] : 0u) : (uint32_t)s_q[d2]);
       reinterpret_cast<uint32_t*>(peer_base(p.peers, d2) + parity_off + g.cnt_row)[me * R + l] = v;
     }
-    if (tid == 0)
-      for (int d2 = 0; d2 < N; ++d2)
-        if (d2 != me) op_record(p.ops, EPB_OP_PUT, me, d2, parity_off + g.cnt_row + 4ull * me * R, 4ull * R);
+
 #pragma unroll 1
     for (int l = tid; l < L; l += BD) {
       const int m = l < nloc && !bad ? s_m[lo + l] : 0;
@@ -706,7 +701,7 @@ EPB_DEV bool ll_send_fast(const LLDisp& p, int* smem, uint32_t seq_ld, uint32_t&
 // receive) — a compact kernel keeps the instruction footprint small (cold
 // i-cache after an L2 flush was the largest stall of the combined kernel);
 // everything else (top-k > 8, batches above the block size, unaligned
-// hidden, the legacy layout) runs the general kernel.
+// hidden, the legacy layout, op-traced launches) runs the general kernel.
 template <int XT, int WT, bool SC, int OT, bool FAST>
 __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
   extern __shared__ int smem[];
@@ -756,7 +751,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const bool bad = ll_send_fast<XT, WT, SC, OT>(p, smem, seq_ld, seq, parity_off);
       // publish: one system-scope release per rank, one arrival per destination
       ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns,
-                fast_units(p.b, gridDim.x, g.H / Elems<WT>::n), p.ops, (seq & 1) * N);
+                fast_units(p.b, gridDim.x, g.H / Elems<WT>::n), OpTrace{nullptr, 0u}, 0u);
       LL_STAMP(p, 4);
       if (bad) return;
     }
@@ -1628,8 +1623,23 @@ cudaError_t launch(void (*kern)(Params), int grid, size_t smem, bool coop, const
     // other GPUs' CTAs publish, so all CTAs must be co-resident
     if (per_sm * sm_count() < grid) return cudaErrorCooperativeLaunchTooLarge;
     if (!coop_attr_enabled()) {
-      kern<<<grid, kThreads, smem, s>>>(p);
-      return cudaGetLastError();
+      // co-residency from grid <= SMs x occupancy alone: may overlap its
+      // predecessor's drain like the unfused launches
+      if (!pdl_enabled()) {
+        kern<<<grid, kThreads, smem, s>>>(p);
+        return cudaGetLastError();
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kern, p);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -1667,7 +1677,10 @@ cudaError_t run_disp(const LLDisp& p, size_t smem, cudaStream_t s) {
   // fused send + receive across GPUs: receivers spin on arrivals from peer
   // GPUs' CTAs, which must all be resident -> cooperative launch
   const bool coop = p.phases == 3 && p.g.N > 1;
-  const bool fast = p.g.K <= 8 && p.b <= kThreads && (p.g.H & 15) == 0 && p.g.layout == EPB_LAYOUT_OPTIMIZED;
+  // (an op-traced launch takes the general kernel: the decode kernel
+  // carries no trace code)
+  const bool fast = p.g.K <= 8 && p.b <= kThreads && (p.g.H & 15) == 0 && p.g.layout == EPB_LAYOUT_OPTIMIZED &&
+                    p.ops.ring == nullptr;
   return fast ? launch(ll_dispatch_kernel<XT, WT, SC, OT, true>, p.g.grid, smem, coop, p, s)
               : launch(ll_dispatch_kernel<XT, WT, SC, OT, false>, p.g.grid, smem, coop, p, s);
 }
