@@ -204,6 +204,58 @@ def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert, zero_copy=False):
     g.destroy()
 
 
+def traced_rounds(world, rank):
+    """The op trace in process mode (one GPU per rank, CUDA-IPC windows):
+    every line this rank's kernels record is one it initiated, with the
+    multiplicities the routing implies (tests/test_op_trace.py for the
+    emulated form)."""
+    e, k, h, b = 4 * world, 3, 512, 16
+    wl = owl.make_workload(e, world, b, k, h, seed=77)
+    for algo in ("ll", "ht"):
+        lines = []
+        fab = ep.ProcessFabric(ep.NodeTopology(world, world), trace=lines.append)
+        if algo == "ll":
+            cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, b, ep.Dtype.BF16)
+        else:
+            cfg = ep.EpConfig(ep.Algorithm.HT, world, world, e, k, h, b, ep.Dtype.BF16)
+        g = ep.create_group(fab, rank, cfg)
+        ell = cfg.experts_per_rank
+        hd = g.create_handle(wl.routing[rank])
+        x = ep.tensor_from_f32(wl.tokens[rank], ep.Dtype.BF16, T.TOKENS)
+        w = ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)
+        if algo == "ll":
+            out = ep.tensor_create((ell, world * b, h), ep.Dtype.F32, T.TOKENS)
+            cnt = ep.tensor_create((ell, world), ep.Dtype.F32, T.RECV_EXPERT_COUNTER_HOST)
+            hd.dispatch([x], [out, cnt])
+            y = ep.tensor_from_f32(out.read_f32(), ep.Dtype.BF16, T.TOKENS)
+        else:
+            tot = hd.get_num_recv_tokens()
+            out = ep.tensor_create((tot, h), ep.Dtype.F32, T.TOKENS)
+            cnt = ep.tensor_create((ell, world), ep.Dtype.F32, T.TOKENS_PER_EXPERTS)
+            hd.dispatch([x, w], [out, cnt])
+            y = ep.tensor_from_f32(out.read_f32(), ep.Dtype.BF16, T.TOKENS)
+        hd.combine([y, w], [ep.tensor_create((b, h), ep.Dtype.F32, T.TOKENS)])
+        hd.destroy()
+        g.destroy()
+        ops = [ln.split(",") for ln in lines]
+        assert ops and all(int(o[1]) == rank for o in ops), "a record names another initiator"
+        owners = [set(int(v) // ell for v in row) for row in wl.routing[rank]]
+        for d in range(world):
+            q = sum(d in os_ for os_ in owners)
+            sig = [o for o in ops if o[0] == "signal" and int(o[2]) == d]
+            if algo == "ll":
+                rec_len = h * 2 + 4 * (2 + 2 * k)
+                puts = [o for o in ops if o[0] == "put" and int(o[2]) == d and int(o[5]) == rec_len]
+                assert len(puts) == (q if d != rank else 0), (algo, d, len(puts), q)
+                if d != rank:
+                    assert sum(int(o[7]) for o in sig) == 2 * 148 or os.environ.get("EPB_LL_CTAS"), (d, sig)
+            else:
+                gets = [o for o in ops if o[0] == "get" and int(o[2]) == d and int(o[5]) == h * 2]
+                srcq = sum(rank in set(int(v) // ell for v in row) for row in wl.routing[d])
+                assert len(gets) == srcq, (algo, d, len(gets), srcq)  # rows pulled from d's stage
+                assert len([o for o in sig if int(o[6]) // world == 0]) == 1  # metadata tag to d
+
+
 def ll_stress(world, rank, rounds):
     """`rounds` back-to-back LL rounds (C2 path: bf16 -> FP8 + scales, bf16
     combine) on one handle per round, every round checked bit-for-bit on the
@@ -337,6 +389,7 @@ def main():
         ("ht bf16 single node", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 4, False)),
         ("ht zero-copy combine (pull)", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 8, True, zero_copy=True)),
         ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
+        ("op trace ll + ht (process mode)", lambda: traced_rounds(world, rank)),
     ]
     stress = int(os.environ.get("EPB_MP_STRESS", "0"))
     if stress:

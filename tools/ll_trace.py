@@ -75,6 +75,12 @@ def main():
                   f"{[round((t - t0s[0]) / 1e3, 2) for t in t0s]} us")
             show("dispatch", tr_d, DISP)
             show("combine", tr_c, COMB)
+            td = tr_d.view(-1, 16).cpu().numpy().astype(np.int64)
+            tc = tr_c.view(-1, 16).cpu().numpy().astype(np.int64)
+            d0 = td[:, 0][td[:, 0] > 0].min()
+            c0 = tc[:, 0][tc[:, 0] > 0].min()
+            print(f"  dispatch span {(td.max() - d0) / 1e3:.2f} us; combine starts {(c0 - d0) / 1e3:.2f} us after "
+                  f"the dispatch start, ends {(tc.max() - d0) / 1e3:.2f} us after it")
         bench.barrier(world)
 
 
