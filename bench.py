@@ -64,9 +64,12 @@ def parse():
     p.add_argument("--no-extra", action="store_true", help="skip the C4/C5 configs (extra_configs key)")
     p.add_argument("--cpu-sample-steps", type=int, default=3)
     p.add_argument("--no-sweep", action="store_true", help="skip the LL token sweep 1..128 (ll_sweep_us key)")
-    p.add_argument("--ll-zero-copy", action="store_true",
-                   help="headline LL step with the expert outputs in the registered window (pulled combine)")
-    return p.parse_args()
+    p.add_argument("--ll-push", action="store_true",
+                   help="headline LL step with the expert outputs in an ordinary tensor (pushed combine); default: "
+                        "in the group's registered window (EpHandle.expert_out_buffer, pulled combine)")
+    a = p.parse_args()
+    a.ll_zero_copy = not a.ll_push
+    return a
 
 
 def workload_config(args, world) -> dict:

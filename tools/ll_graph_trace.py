@@ -19,6 +19,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import bench  # noqa: E402
 from paper_2603_13606_b200 import _lib  # noqa: E402
 
@@ -70,6 +71,10 @@ def main():
         c0 = tc[:, 0][tc[:, 0] > 0].min()
         if rep >= 2:
             rows.append(((td.max() - d0) / 1e3, (c0 - td.max()) / 1e3, (tc.max() - c0) / 1e3, (tc.max() - d0) / 1e3))
+    if os.environ.get("LL_GRAPH_TRACE_STAMPS") and rank == 0:
+        import ll_trace  # noqa: E402  (tools/)
+        ll_trace.show("dispatch (last replay)", tr_d, ll_trace.DISP)
+        ll_trace.show("combine (last replay)", tr_c, ll_trace.COMB)
     r = np.array(rows)
     med = np.median(r, axis=0)
     res = bench.allgather_f(float(med[3]), world)
