@@ -440,6 +440,7 @@ struct HTRecv {
   int rank;
   uint32_t tag;
   OpTrace ops;
+  int stages;  // bulk receive: ring depth per warp (<= kMaxStages)
 };
 
 // Receive: every record names a source token and the output rows of this
@@ -566,6 +567,7 @@ __global__ void __launch_bounds__(kHTThreads) ht_dispatch_recv_kernel(HTRecv p) 
 // outputs as ht_dispatch_recv_kernel (wire-dtype output only).
 // ---------------------------------------------------------------------------
 constexpr int kBulkWarps = 8;
+constexpr int kMaxStages = 4;  // row-load ring depth per warp (HTRecv::stages)
 
 EPB_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 EPB_DEV void mbar_init(uint64_t* m, int count) {
@@ -598,7 +600,8 @@ EPB_DEV void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 
 EPB_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(HTRecv p) {
-  extern __shared__ __align__(128) uint8_t s_buf[];  // [warps][2][hb] then [warps][2] mbarriers
+  extern __shared__ __align__(128) uint8_t s_buf[];  // [warps][stages][hb] then [warps][kMaxStages] mbarriers
+  __shared__ int s_ring[kBulkWarps][kMaxStages];       // item held by each stage, in issue order
   __shared__ int s_q[kMaxRanks];
   __shared__ int s_maxq;
   const HTGeom& g = p.g;
@@ -606,11 +609,11 @@ __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(
   const int me = p.rank;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t hb = (uint32_t)g.RBp / 2;
-  uint8_t* buf = s_buf + (size_t)warp * 2 * hb;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(s_buf + (size_t)nw * 2 * hb) + warp * 2;
+  const int S = p.stages;
+  uint8_t* buf = s_buf + (size_t)warp * S * hb;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_buf + (size_t)nw * S * hb) + warp * kMaxStages;
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int st = 0; st < S; ++st) mbar_init(&bar[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // the mbarrier initialisation
@@ -649,8 +652,9 @@ __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(
       if (resolve(f2, s, j)) return f2;
     return items;
   };
-  uint32_t phase[2] = {0u, 0u};
-  int cur = next_item(warp * gridDim.x + blockIdx.x);
+  // an S-stage ring per warp: S-1 row loads in flight ahead of the item
+  // being fanned out (the NVLink round trip is hidden behind S-1 items)
+  uint32_t phase = 0u;  // bit st: parity of stage st's next completion
   auto issue = [&](int f2, int stg) {
     int s, j;
     resolve(f2, s, j);
@@ -659,16 +663,29 @@ __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(
       const uint8_t* row = hpeer(p.peers, s) + g.stage + (int64_t)hdr[0] * g.RBp + (f2 & 1) * hb;
       mbar_expect_tx(&bar[stg], hb);
       bulk_load(buf + stg * hb, row, hb, &bar[stg]);
+      s_ring[warp][stg] = f2;
     }
   };
-  if (cur < items) issue(cur, 0);
-  for (int q = 0; cur < items; ++q) {
-    const int stg = q & 1;
-    const int nxt = next_item(cur + gridDim.x * nw);
-    // the other buffer's stores (task q-1) must have read it before reuse
+  const int stride = gridDim.x * nw;
+  int nxt = next_item(warp * gridDim.x + blockIdx.x);
+  int head = 0, tail = 0;  // items fanned out / issued
+  while (tail < S - 1 && nxt < items) {
+    issue(nxt, tail % S);
+    nxt = next_item(nxt + stride);
+    ++tail;
+  }
+  while (head < tail) {
+    const int stg = head % S;
+    // the previous item's stores must have read its stage before it is refilled
     bulk_wait_read_all();
     __syncwarp();
-    if (nxt < items) issue(nxt, stg ^ 1);
+    if (nxt < items) {
+      issue(nxt, tail % S);
+      nxt = next_item(nxt + stride);
+      ++tail;
+    }
+    __syncwarp();
+    const int cur = s_ring[warp][stg];
     int s, j;
     resolve(cur, s, j);
     const int half = cur & 1;
@@ -689,14 +706,14 @@ __global__ void __launch_bounds__(kBulkWarps * 32) ht_dispatch_recv_bulk_kernel(
       p.origin[(int64_t)pos * 4 + 3] = lane;
       p.origin_w[pos] = reinterpret_cast<const float*>(rec)[lane];
     }
-    while (!mbar_try_wait(&bar[stg], phase[stg])) {
+    while (!mbar_try_wait(&bar[stg], (phase >> stg) & 1u)) {
     }
-    phase[stg] ^= 1u;
+    phase ^= 1u << stg;
     if (loc) {
       bulk_store(reinterpret_cast<uint8_t*>(p.out) + (int64_t)pos * g.RBp + half * hb, buf + stg * hb, hb);
       bulk_commit();
     }
-    cur = nxt;
+    ++head;
   }
   bulk_wait_all();
 }
@@ -1162,13 +1179,21 @@ template <int WT, int OT>
 cudaError_t launch_hrecv(const HTRecv& p, cudaStream_t s) {
   // wire-dtype output, half rows of 16-B multiples: the bulk-copy receive
   static const int bulk = [] { const char* v = getenv("EPB_HT_BULK"); return v ? atoi(v) : 1; }();
+  // ring depth: EPB_HT_STAGES (default 2: 3 measured no faster at C3, N=1/2), as deep as 220 KB of
+  // shared memory allows
+  static const int want = [] { const char* v = getenv("EPB_HT_STAGES"); return v ? atoi(v) : 2; }();
   const size_t hb = (size_t)p.g.RBp / 2;
-  const size_t bsm = (size_t)kBulkWarps * 2 * hb + (size_t)kBulkWarps * 2 * 8;
-  if (bulk && OT == WT && p.g.RB == p.g.RBp && (p.g.RBp % 32) == 0 && bsm <= 200 * 1024 && p.g.K <= 32) {
+  int stages = std::max(2, std::min(want, kMaxStages));
+  auto bytes = [&](int st) { return (size_t)kBulkWarps * st * hb + (size_t)kBulkWarps * kMaxStages * 8; };
+  while (stages > 2 && bytes(stages) > 220 * 1024) --stages;
+  const size_t bsm = bytes(stages);
+  if (bulk && OT == WT && p.g.RB == p.g.RBp && (p.g.RBp % 32) == 0 && bsm <= 220 * 1024 && p.g.K <= 32) {
     cudaError_t e = cudaFuncSetAttribute(ht_dispatch_recv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bsm);
     if (e != cudaSuccess) return e;
-    ht_dispatch_recv_bulk_kernel<<<bulk * hsm_count(), kBulkWarps * 32, bsm, s>>>(p);
+    HTRecv q = p;
+    q.stages = stages;
+    ht_dispatch_recv_bulk_kernel<<<bulk * hsm_count(), kBulkWarps * 32, bsm, s>>>(q);
     return cudaGetLastError();
   }
   ht_dispatch_recv_kernel<WT, OT><<<2 * hsm_count(), kHTThreads, 0, s>>>(p);
