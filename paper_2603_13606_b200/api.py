@@ -46,6 +46,10 @@ LAYOUTS = ("optimized", "legacy")
 # PCIe reads measured slower than the copy engine (e2e 152 vs 116-132 us).
 _HOST_MAPPED = os.environ.get("EPB_HOST_MAPPED", "1") != "0"
 _HOST_MAPPED_IN = os.environ.get("EPB_HOST_MAPPED_IN", "0") == "1"
+# HT create_handle in one launch (epb_ht_open) where every rank's kernel can
+# run concurrently; EPB_HT_OPEN_FUSED=0 keeps the separate layout / metadata
+# launches
+_HT_OPEN_FUSED = os.environ.get("EPB_HT_OPEN_FUSED", "1") != "0"
 
 
 # entry points that never read or write a window (local routing layout)
@@ -694,7 +698,7 @@ class EpHandle:
                           ctypes.c_void_p(mt.data_ptr()), ctypes.c_void_p(mt.data_ptr() + nm * 4))
         mt, offsets, meta_p, total_p = g._ht_bufs
         host = g._pinned_i32(nm + 2)
-        if g._fused_ok():
+        if g._fused_ok() and _HT_OPEN_FUSED:
             # layout + metadata all-gather in one launch, the shapes written
             # straight into pinned host memory with the error word after them
             g._launch("epb_ht_open", g._g, rnd, _ptr(self.routing), self._b, ctypes.byref(self._lay),

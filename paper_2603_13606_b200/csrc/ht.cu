@@ -92,6 +92,12 @@ EPB_DEV void meta_send_block(const HTMetaSend& p) {
                 p.parity * g.N + p.rank, p.tag);
     }
   }
+  // the flags are out before any thread of the block starts waiting for the
+  // peers' (the fused open waits next in the same block: a lane of warp 0
+  // spinning on a peer's flag could otherwise starve thread 0's sends while
+  // the peer's block does the same — a cross-GPU deadlock seen under
+  // EPB_CHAOS_NS)
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) ht_meta_send_kernel(HTMetaSend p) {
