@@ -28,9 +28,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", type=int, default=128)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--push", action="store_true", help="expert outputs in an ordinary tensor (pushed combine)")
     a = ap.parse_args()
     world, rank = bench.init_dist()
-    st = bench.LLStep(world, rank, a.tokens)
+    st = bench.LLStep(world, rank, a.tokens, zero_copy=not a.push)
     g = st.g
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     tr_d = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")

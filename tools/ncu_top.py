@@ -1,3 +1,7 @@
+"""Top SASS lines of one kernel in an ncu report by warp-stall samples.
+
+    python tools/ncu_top.py REPORT.ncu-rep KERNEL_REGEX [N]
+"""
 import csv, sys, subprocess, io
 rep, kern = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 30
