@@ -1116,16 +1116,17 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       LL_STAMP(p, 7);
       return;
     }
-    // warp tasks (source, slot j, half row), sources interleaved so a warp's
+    // warp tasks (source, slot j, quarter row), sources interleaved so a warp's
     // successive tasks visit different sources; each warp waits only for
     // its task's source.  The header is read once, the row loaded once and
     // stored to every local expert the slot names (the fan-out of
     // ll.py:378-400).  Task (s, 0, 0) also writes the counts of pairs (l, s).
     const bool fan = (H & 15) == 0;
     uint64_t seen = 0;
-    const int tasks = 2 * B * nsrc;
+    constexpr int kRP = 4;  // row parts per slot: 4 x B x (N-1) warp tasks
+    const int tasks = kRP * B * nsrc;
     for (int f2 = warp * gridDim.x + blockIdx.x; f2 < tasks; f2 += gridDim.x * nw) {
-      const int half = f2 & 1, r = f2 >> 1;
+      const int part = f2 % kRP, r = f2 / kRP;
       const int j = r / nsrc, so = r - j * nsrc;
       const int s = me + 1 + so < N ? me + 1 + so : me + 1 + so - N;
       if (!warp_wait_sources(1ull << s, seen, arr, target, sys, p.timeout_ns, p.err, lane)) return;
@@ -1137,8 +1138,8 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const uint8_t* slot = p.win + parity_off + g.disp_slot + ((int64_t)s * B + j) * g.slot_stride;
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(slot + g.RBp + g.SBp);
       const int nch2 = H / EPC;
-      const int per = (nch2 + 1) / 2;
-      const int c0 = half * per, c1 = min(nch2, c0 + per);
+      const int per = (nch2 + kRP - 1) / kRP;
+      const int c0 = part * per, c1 = min(nch2, c0 + per);
       int4 v0[kUnroll];
       if (FAST || fan) {
 #pragma unroll
@@ -1158,7 +1159,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         if (lane == 0) raise_err(p.err, EPB_TRANSPORT_CLOSED);
         return;
       }
-      if (j == 0 && half == 0)
+      if (j == 0 && part == 0)
         for (int l = lane; l < L; l += 32) {
           const int m = l < nloc ? (int)crow[l] : 0;
           p.counts_i32[l * N + s] = m;
@@ -1168,12 +1169,12 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const bool loc = lane < K && e >= lo && e < lo + nloc;
       const int my_orow = (e - lo) * N * B + s * B + ci;
       const unsigned lm = __ballot_sync(0xffffffffu, loc);
-      if (half == 0 && loc) p.src_info[my_orow] = (int32_t)(tok * K + lane);
+      if (part == 0 && loc) p.src_info[my_orow] = (int32_t)(tok * K + lane);
       if (!FAST && !fan) {
         for (unsigned mm = lm; mm; mm &= mm - 1) {
           const int64_t row = __shfl_sync(0xffffffffu, my_orow, __ffs(mm) - 1);
           ll_copy_row<WT, SC, OT>(g, slot, reinterpret_cast<uint8_t*>(p.out) + row * orow_bytes,
-                                  SC ? p.out_scales + row * (H / 128) : nullptr, lane, half, 2);
+                                  SC ? p.out_scales + row * (H / 128) : nullptr, lane, part, kRP);
         }
         continue;
       }
@@ -1216,7 +1217,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
         }
       }
       if constexpr (SC && OT == WT) {
-        if (half == 0) {
+        if (part == 0) {
           for (unsigned mm = lm; mm; mm &= mm - 1) {
             const int64_t row = __shfl_sync(0xffffffffu, my_orow, __ffs(mm) - 1);
             for (int i = lane; i < H / 128; i += 32)
