@@ -712,6 +712,15 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
     g.check()
     barrier(world)
     t_h = allreduce_max(statistics.median(t_handle[-args.ht_steps:]), world)
+    # create_handle back to back (steady state: no host barrier or idle GPU
+    # before it): handle + destroy, the handle's wall time only
+    tb = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        h = g.create_handle(topk)
+        tb.append(time.perf_counter() - t0)
+        h.destroy()
+    t_hb = allreduce_max(statistics.median(tb), world)
     per_d = allgather_f(statistics.median(td), world)
     per_c = allgather_f(statistics.median(tc), world)
     t_d = max(per_d) / 1e3
@@ -730,13 +739,16 @@ def run_ht(args, world, rank, shape=None, zipf=False, seed=7):
         "tokens_per_rank": b, "dtype": "bf16", "recv_rows": tot, "parity": parity,
         "dispatch_us": round(t_d * 1e6, 1), "combine_us": round(t_c * 1e6, 1),
         "create_handle_us": round(t_h * 1e6, 1),
+        "create_handle_back_to_back_us": round(t_hb * 1e6, 1),
         "combine_push_us": round(t_push * 1e6, 1),
         "dispatch_staged_input_us": round(t_stg * 1e6, 1),
         "dispatch_input": "tokens in the registered token stage (EpGroup.token_in_view, read in place by peers); "
                           "dispatch_staged_input_us = from an ordinary tensor (copied into the stage first)",
         "combine_push_note": "combine input in an ordinary tensor: rows pushed to the homes' slots, then reduced",
         "create_handle_timing": "host wall clock of EpGroup.create_handle (routing snapshot + layout + metadata "
-                                "all-gather, receive count on the host on return; ht.py open_round)",
+                                "all-gather, receive count on the host on return; ht.py open_round): "
+                                "create_handle_us right after a host barrier with the GPU idle (each timed step), "
+                                "create_handle_back_to_back_us = median of 20 consecutive handle + destroy calls",
         "dispatch_payload_GBps": round(d_all / t_d / 1e9, 1),
         "combine_payload_GBps": round(c_all / t_c / 1e9, 1),
         "dispatch_nvlink_GBps": round(d_remote / t_d / 1e9, 1) if nv else None,
