@@ -463,7 +463,69 @@ def run_ll(args, world, rank, shape=None, zipf=False, light=False, zero_copy=Fal
                              "node before every launch (send phase, then receive phase of each op)"}
     del gs
     st.g.check()
+    res["in_kernel"] = in_kernel_spans(st, flush, world)
     return res
+
+
+def in_kernel_spans(st, flush, world, reps=10):
+    """Each LL kernel's own duration inside the step graph: first CTA start
+    to the last per-CTA %globaltimer checkpoint (the kernels' diagnostic
+    stamps, epb_group_set_trace; tools/ll_graph_trace.py), one step per
+    replay after the L2 flush and device barrier, median over replays, max
+    over ranks.  Separates the kernels from the graph skeleton (event nodes,
+    launch latency) that the event-timed figures include."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2603_13606_b200 import _lib
+    g = st.g
+    tr_d = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+    tr_c = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+
+    def step():
+        h = g.create_handle(st.topk)
+        _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(tr_d.data_ptr()))
+        h.dispatch([st.X], [st.RECV, st.RECV_SC, st.CNT])
+        _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(tr_c.data_ptr()))
+        h.combine([st.Y, st.W], [st.OUT])
+        _lib.call("epb_group_set_trace", g._g, ctypes.c_void_p(0))
+        h.destroy()
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        flush.zero_()
+        g.device_barrier()
+        step()
+    torch.cuda.synchronize()
+    rows = []
+    for _ in range(reps):
+        tr_d.zero_()
+        tr_c.zero_()
+        barrier(world)
+        graph.replay()
+        torch.cuda.synchronize()
+        td = tr_d.view(-1, 16).cpu().numpy().astype(np.int64)
+        tc = tr_c.view(-1, 16).cpu().numpy().astype(np.int64)
+        d0 = td[:, 0][td[:, 0] > 0].min()
+        c0 = tc[:, 0][tc[:, 0] > 0].min()
+        rows.append(((td.max() - d0) / 1e3, (tc.max() - c0) / 1e3, (tc.max() - d0) / 1e3))
+    del graph
+    g.check()
+    med = np.median(np.array(rows), axis=0)
+    return {"epb_ll_dispatch": round(allreduce_max(float(med[0]), world), 2),
+            "epb_ll_combine": round(allreduce_max(float(med[1]), world), 2),
+            "dispatch_start_to_combine_end": round(allreduce_max(float(med[2]), world), 2),
+            "note": "µs, first CTA start to last per-CTA %globaltimer checkpoint of each kernel inside the step "
+                    "graph (L2 flushed before the step), median of 10 replays, max over ranks; the step adds "
+                    "the graph skeleton (event nodes, first-launch latency)"}
 
 
 def run_e2e(args, world, rank, st):
@@ -876,12 +938,15 @@ def roofline(world, res, st, peaks):
            "step_over_floor": round(step_us / res["floor"]["two_tiny_kernels_us"], 2),
            "note": "floor = the same graph skeleton (L2 flush, barrier, start/end events) with two tiny kernels "
                    "in place of dispatch and combine"}
+    span = res.get("in_kernel", {}).get(dom)
     if world == 1:
         peak = peaks.get("hbm_gbs", 6650.0)
         ach = hbm_b[dom] / (dur * 1e-6) / 1e9
         return {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": int(hbm_b[dom]),
                 "duration_us": round(dur, 2), "regime": "latency-bound (N=1: no transport, bytes mostly L2-resident)",
+                "in_kernel_span_us": span,
+                "achieved_over_in_kernel_span": round(hbm_b[dom] / (span * 1e-6) / 1e9, 1) if span else None,
                 "latency": lat,
                 "duration": "event node before the launch to the next one (includes one event-node interval)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
@@ -889,6 +954,8 @@ def roofline(world, res, st, peaks):
     return {"kernel": dom, "bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_GBPS, "unit": "GB/s",
             "frac": round(ach / NVLINK_GBPS, 4), "traffic": traffic, "algorithmic_bytes": int(nv_b[dom]),
             "duration_us": round(dur, 2), "latency": lat,
+            "in_kernel_span_us": span,
+            "achieved_over_in_kernel_span": round(nv_b[dom] / (span * 1e-6) / 1e9, 1) if span else None,
             "hbm_bytes": int(hbm_b[dom]),
             "duration": "event node before the launch to the next one (includes one event-node interval)",
             "peak_source": "B200_PROFILING.md measured peer copy, 770 GB/s per direction (900 nominal)"}
@@ -935,6 +1002,7 @@ def main():
                           "floor.events_only_us is that interval with nothing between)",
         "floor": res["floor"],
         "ll_staged": res["staged"],
+        "kernel_in_kernel_us": res["in_kernel"],
         "gpu_launches": res["launches"],
         "roofline": roofline(world, res, st, peaks),
         "nvlink_bytes_per_step": st.algo_bytes()[1] if world > 1 else None,
