@@ -48,6 +48,7 @@ struct LLGeom {
   uint64_t yout, yout_rows, yrow;  // registered expert-output region [L][N*B] bf16 rows (expert_out_window)
   int sys_fence;                   // release fences at system scope (peers on other GPUs)
   uint32_t chaos_ns;               // stress mode: random delays before stores / releases (EPB_CHAOS_NS)
+  int direct_max;                  // ll_arrive: per-CTA arrivals up to this many storing CTAs (EPB_LL_DIRECT)
 };
 
 // HT:

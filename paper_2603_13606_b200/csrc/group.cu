@@ -154,6 +154,8 @@ int epb_group_create(const epb_config* cfg, int rank, void* window, uint64_t win
   }
   g->ll.chaos_ns = g->ht.chaos_ns = 0;
   if (const char* c = getenv("EPB_CHAOS_NS")) g->ll.chaos_ns = g->ht.chaos_ns = (uint32_t)strtoul(c, nullptr, 10);
+  g->ll.direct_max = 0;  // last-CTA publish at every batch size (direct arrivals measured no faster)
+  if (const char* c = getenv("EPB_LL_DIRECT")) g->ll.direct_max = atoi(c);
   // LL grid (identical on every rank: receivers count one arrival per
   // source CTA); EPB_LL_CTAS < 148 leaves SMs free for concurrent compute
   if (const char* c = getenv("EPB_LL_CTAS")) {

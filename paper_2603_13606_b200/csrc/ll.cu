@@ -102,24 +102,26 @@ EPB_DEV bool wait_arrivals(const uint64_t* c, uint64_t need, bool sys, uint64_t 
 // peer's arrival counter for this rank, after a system-scope release that
 // covers every payload store of the round.  Two schemes, chosen per launch
 // by the sender alone (the receiver only waits for grid*(rounds)):
-//  * few CTAs stored (W <= 32, e.g. a small decode batch): each of CTAs
+//  * W <= direct_max storing CTAs (EPB_LL_DIRECT, default 0): each of CTAs
 //    0..W-1 releases its own stores and adds 1; CTA grid-1 (which is not
-//    one of them) releases and adds grid - W for itself and the idle CTAs;
+//    one of them) releases and adds grid - W for itself and the idle CTAs
+//    (W = 0, the pulled combine's announcement: CTA grid-1 alone);
 //  * otherwise every CTA releases at GPU scope and counts in at a local
 //    counter; the last one issues the rank's single system-scope release
 //    (cumulative over all CTAs' stores: each CTA's GPU-scope release is
 //    acquired by the last CTA's RMW on the counter) and adds grid.
 // Concurrent system-scope fences from every SM measured several us; the
-// last-CTA chain costs a local atomic round trip, which a small batch avoids.
+// per-CTA scheme measured no faster than the last-CTA chain even at 1-4
+// tokens (N=2: 35.6 vs 32.8 us at 4 tokens), hence direct_max = 0.
 // All threads call.  `done`: this kind's local counter (reset by the last).
-constexpr int kDirectArrive = 32;
 EPB_DEV void ll_arrive(const uint64_t* peers, uint64_t off, int N, int me, bool fence_sys, bool sys,
-                       unsigned* done, uint32_t chaos_ns, int W, const OpTrace& ops, uint32_t sig_base) {
+                       unsigned* done, uint32_t chaos_ns, int W, const OpTrace& ops, uint32_t sig_base,
+                       int direct_max) {
   __syncthreads();
   if (threadIdx.x != 0 || N == 1) return;
   const int G = gridDim.x, c = blockIdx.x;
   uint64_t add = 0;
-  if (W <= kDirectArrive && W < G) {
+  if (W <= direct_max && W < G) {
     add = c < W ? 1ull : (c == G - 1 ? (uint64_t)(G - W) : 0ull);
     if (add == 0) return;
     chaos_delay(chaos_ns, 0x53u);
@@ -751,7 +753,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       const bool bad = ll_send_fast<XT, WT, SC, OT>(p, smem, seq_ld, seq, parity_off);
       // publish: one system-scope release per rank, one arrival per destination
       ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns,
-                fast_units(p.b, gridDim.x, g.H / Elems<WT>::n), OpTrace{nullptr, 0u}, 0u);
+                fast_units(p.b, gridDim.x, g.H / Elems<WT>::n), OpTrace{nullptr, 0u}, 0u, g.direct_max);
       LL_STAMP(p, 4);
       if (bad) return;
     }
@@ -1047,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads) ll_dispatch_kernel(LLDisp p) {
       if (bad && threadIdx.x == 0) raise_err(p.err, EPB_INVALID_ARGUMENT);
     }
     // publish: one release per CTA, one arrival per destination
-    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, G, p.ops, (seq & 1) * N);
+    ll_arrive(p.peers, parity_off + g.d_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, G, p.ops, (seq & 1) * N, g.direct_max);
     LL_STAMP(p, 4);
     if (bad) return;
   }
@@ -1377,7 +1379,7 @@ __global__ void __launch_bounds__(kThreads) ll_combine_kernel(LLComb p) {
     // expert outputs were written by earlier kernels on this stream — the
     // arrival announces them)
     ll_arrive(p.peers, parity_off + g.c_arr, N, me, g.sys_fence, sys, p.done, g.chaos_ns, send_ctas, p.ops,
-              2 * N + (seq & 1) * N);
+              2 * N + (seq & 1) * N, g.direct_max);
     LL_STAMP(p, 3);
   }
 
