@@ -148,7 +148,7 @@ def ll_pipelined(world, rank):
 def buffer_ll(world, rank):
     """Buffer wrapper, one process per GPU: own comm stream, pinned mapped
     counters, cached dispatch."""
-    e, k, h, b = 256, 8, 7168, 64
+    e, k, h = 256, 8, 7168
     cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, b, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
     wl = owl.make_workload(e, world, b, k, h, 70)
     wl.tokens = [bf16r(t) for t in wl.tokens]
@@ -256,7 +256,7 @@ def traced_rounds(world, rank):
                 assert len([o for o in sig if int(o[6]) // world == 0]) == 1  # metadata tag to d
 
 
-def ll_stress(world, rank, rounds):
+def ll_stress(world, rank, rounds, b=64):
     """`rounds` back-to-back LL rounds (C2 path: bf16 -> FP8 + scales, bf16
     combine) on one handle per round, every round checked bit-for-bit on the
     device against oracle-derived expectations; mismatches accumulate on the
@@ -395,6 +395,8 @@ def main():
     if stress:
         cases = [(f"ll stress {stress} rounds (chaos {os.environ.get('EPB_CHAOS_NS', '0')} ns)",
                   lambda: ll_stress(world, rank, stress)),
+                 (f"ll stress {max(1, stress // 2)} rounds, 2 tokens (chaos {os.environ.get('EPB_CHAOS_NS', '0')} ns)",
+                  lambda: ll_stress(world, rank, max(1, stress // 2), b=2)),
                  (f"ht stress {max(1, stress // 20)} rounds (chaos {os.environ.get('EPB_CHAOS_NS', '0')} ns)",
                   lambda: ht_stress(world, rank, max(1, stress // 20)))]
     failures = []
