@@ -179,16 +179,19 @@ __global__ void __launch_bounds__(1024) ht_meta_recv_kernel(HTMetaRecv p) {
 
 // ---------------------------------------------------------------------------
 // K1 + K5a fused: HTRank.open_round (ht.py:335-368) in ONE launch.  CTA c
-// lays out tokens [c*kLayChunk, (c+1)*kLayChunk) (validation, local ranks
-// and slots, per-chunk column histogram); grid barrier; the column prefix
-// over chunks is spread over every warp of the grid (m, q); grid barrier;
-// every CTA adds its chunk bases while CTA 0 sends this rank's metadata row,
-// waits for every source's and writes the receive shapes straight into
-// host-mapped pinned memory, followed by the group's error word, so the
-// host reads the round's shapes after one stream synchronisation and no
-// copy.  Same integers as the three-kernel K1 + the K5a pair.  All CTAs are
-// co-resident (cooperative launch); the two barrier words are reset by the
-// last CTA out.
+// owns tokens [c*kLayChunk, (c+1)*kLayChunk): it validates them and builds
+// per-warp column histograms (shared memory), writes the chunk's column
+// totals, and after ONE grid barrier takes its chunk base per column from
+// the totals of the earlier chunks and ranks its tokens (final ranks and
+// slots, no fix-up pass).  CTA 0 also sums every chunk (m, q), sends this
+// rank's metadata row before ranking its own chunk (the peers' rows travel
+// meanwhile), then waits for every source's row and writes the receive
+// shapes straight into host-mapped pinned memory, followed by the group's
+// error word: the host reads the round's shapes after one stream
+// synchronisation and no copy.  Top-k > 8 keeps the two-barrier form (chunk
+// layouts, column prefix, chunk bases added).  Same integers as the
+// three-kernel K1 + the K5a pair.  All CTAs are co-resident (cooperative
+// launch); the barrier words are reset by the last CTA out.
 struct HTOpen {
   const int64_t* topk;
   int b, K, L, chunk;  // tokens per CTA (one CTA: chunk = b)
@@ -224,66 +227,101 @@ __global__ void __launch_bounds__(1024) ht_open_kernel(HTOpen p) {
   const int E = g.E, N = g.N, C = E + N;
   const int G = gridDim.x;
   OPEN_STAMP(0);
-  // (1) chunk layout (one CTA: the whole routing, final m / q directly)
   const int t0 = blockIdx.x * p.chunk, bc = max(0, min(p.chunk, p.b - t0));
   const int64_t* tk = p.topk + (int64_t)t0 * p.K;
   int32_t* h = p.hist + (int64_t)blockIdx.x * C;
-  int32_t* m_out = G == 1 ? const_cast<int32_t*>(p.ms.m) : h;
-  int32_t* q_out = G == 1 ? const_cast<int32_t*>(p.ms.q) : h + E;
-  const BlockLayoutSmem sm = BlockLayoutSmem::carve(smem, blockDim.x >> 5, E, N);
-  if (!block_layout_checked(tk, bc, p.K, E, N, p.L, sm, m_out, q_out, p.tok_rank + (int64_t)t0 * p.K,
-                            p.tok_slot + (int64_t)t0 * N, p.stamps ? p.stamps + blockIdx.x * 16 + 10 : nullptr) &&
-      threadIdx.x == 0)
-    raise_err(p.mr.err, EPB_INVALID_ARGUMENT);
-  OPEN_STAMP(1);
-  if (G > 1) grid_arrive_wait(p.bar, G);
-  else __syncthreads();
-  OPEN_STAMP(2);
-  // (2) exclusive prefix of every column over the chunks: one warp per column
-  if (G > 1) {
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < C; c += G * wpb) {
-      int carry = 0;
-      for (int j0 = 0; j0 < G; j0 += 32) {
-        const int j = j0 + lane;
-        const int v = j < G ? __ldcg(&p.hist[(int64_t)j * C + c]) : 0;
-        int incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-          const int u = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += u;
+  int32_t* ranks = p.tok_rank + (int64_t)t0 * p.K;
+  int32_t* slots = p.tok_slot + (int64_t)t0 * N;
+  const int nw = blockDim.x >> 5;
+  const BlockLayoutSmem sm = BlockLayoutSmem::carve(smem, nw, E, N);
+  uint64_t* lst = p.stamps ? p.stamps + blockIdx.x * 16 + 10 : nullptr;
+  bool bad;
+  if (G > 1 && p.K <= 8) {
+    // (1) validated per-warp histograms of the chunk, its column totals out;
+    // one grid barrier; (2) the chunk's base per column = the totals of the
+    // earlier chunks (CTA 0 also sums all of them: m and q, and sends the
+    // metadata row at once); (3) ranks and slots seeded with the bases
+    if (!block_hist8(tk, bc, p.K, E, N, p.L, sm, h, lst) && threadIdx.x == 0)
+      raise_err(p.mr.err, EPB_INVALID_ARGUMENT);
+    OPEN_STAMP(1);
+    grid_arrive_wait(p.bar, G);
+    OPEN_STAMP(2);
+    bad = *reinterpret_cast<const volatile int*>(p.mr.err) != 0;
+    if (!bad) {
+      int* s_base = smem + BlockLayoutSmem::bytes(nw, E, N) / 4;
+      for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        int base = 0;
+        for (int j = 0; j < (int)blockIdx.x; ++j) base += __ldcg(&p.hist[(int64_t)j * C + c]);
+        s_base[c] = base;
+        if (blockIdx.x == 0) {  // m and q: the totals over every chunk
+          int tot = 0;
+          for (int j = 0; j < G; ++j) tot += __ldcg(&p.hist[(int64_t)j * C + c]);
+          if (c < E) const_cast<int32_t*>(p.ms.m)[c] = tot;
+          else const_cast<int32_t*>(p.ms.q)[c - E] = tot;
         }
-        if (j < G) p.hist[(int64_t)j * C + c] = carry + incl - v;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
-      if (lane == 0) {
-        if (c < E) const_cast<int32_t*>(p.ms.m)[c] = carry;
-        else const_cast<int32_t*>(p.ms.q)[c - E] = carry;
+      __syncthreads();
+      OPEN_STAMP(3);
+      if (blockIdx.x == 0) meta_send_block(p.ms);  // the peers' flags travel while the ranks are computed
+      OPEN_STAMP(4);
+      block_rank8(tk, bc, p.K, E, N, p.L, sm, s_base, nullptr, nullptr, ranks, slots, lst);
+    }
+  } else {
+    // one chunk (final m / q directly), or top-k > 8: per-chunk layouts, a
+    // column prefix over the chunks between two grid barriers, then the
+    // chunk bases added to the ranks and slots
+    int32_t* m_out = G == 1 ? const_cast<int32_t*>(p.ms.m) : h;
+    int32_t* q_out = G == 1 ? const_cast<int32_t*>(p.ms.q) : h + E;
+    if (!block_layout_checked(tk, bc, p.K, E, N, p.L, sm, m_out, q_out, ranks, slots, lst) && threadIdx.x == 0)
+      raise_err(p.mr.err, EPB_INVALID_ARGUMENT);
+    OPEN_STAMP(1);
+    if (G > 1) grid_arrive_wait(p.bar, G);
+    else __syncthreads();
+    OPEN_STAMP(2);
+    if (G > 1) {
+      const int lane = threadIdx.x & 31;
+      for (int c = blockIdx.x * nw + (threadIdx.x >> 5); c < C; c += G * nw) {
+        int carry = 0;
+        for (int j0 = 0; j0 < G; j0 += 32) {
+          const int j = j0 + lane;
+          const int v = j < G ? __ldcg(&p.hist[(int64_t)j * C + c]) : 0;
+          int incl = v;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+          }
+          if (j < G) p.hist[(int64_t)j * C + c] = carry + incl - v;
+          carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) {
+          if (c < E) const_cast<int32_t*>(p.ms.m)[c] = carry;
+          else const_cast<int32_t*>(p.ms.q)[c - E] = carry;
+        }
+      }
+      grid_arrive_wait(p.bar, 2 * G);
+    }
+    OPEN_STAMP(3);
+    bad = *reinterpret_cast<const volatile int*>(p.mr.err) != 0;
+    if (!bad && bc > 0 && G > 1) {
+      const int32_t* base = p.hist + (int64_t)blockIdx.x * C;
+      for (int i = threadIdx.x; i < bc * p.K; i += blockDim.x) {
+        const int e = (int)tk[i];
+        ranks[i] += __ldcg(&base[e]);
+      }
+      for (int i = threadIdx.x; i < bc * N; i += blockDim.x) {
+        const int v = slots[i];
+        if (v >= 0) slots[i] = v + __ldcg(&base[E + i % N]);
       }
     }
+    __syncthreads();
+    if (blockIdx.x == 0 && !bad) meta_send_block(p.ms);
+    OPEN_STAMP(4);
   }
-  OPEN_STAMP(3);
-  if (G > 1) grid_arrive_wait(p.bar, 2 * G);
-  OPEN_STAMP(4);
-  const bool bad = *reinterpret_cast<const volatile int*>(p.mr.err) != 0;
-  // (3) chunk bases into this CTA's ranks and slots
-  if (!bad && bc > 0 && G > 1) {
-    const int32_t* base = p.hist + (int64_t)blockIdx.x * C;
-    for (int i = threadIdx.x; i < bc * p.K; i += blockDim.x) {
-      const int e = (int)tk[i];
-      p.tok_rank[(int64_t)t0 * p.K + i] += __ldcg(&base[e]);
-    }
-    for (int i = threadIdx.x; i < bc * N; i += blockDim.x) {
-      int32_t* sl = p.tok_slot + (int64_t)t0 * N + i;
-      const int v = *sl;
-      if (v >= 0) *sl = v + __ldcg(&base[E + i % N]);
-    }
-  }
-  // (4) CTA 0: the metadata all-gather (a rejected routing sends nothing)
+  // (4) CTA 0: every source's metadata row, the offsets and the receive
+  // shapes (a rejected routing sent nothing and waits for nothing)
   OPEN_STAMP(5);
   if (blockIdx.x == 0) {
     if (!bad) {
-      meta_send_block(p.ms);
       OPEN_STAMP(6);
       meta_recv_block(p.mr, smem);
     }
@@ -1258,7 +1296,8 @@ int epb_ht_open(epb_group* g, uint32_t round, const int64_t* topk_idx, int32_t b
   const bool single = b <= kOpenSingle;
   int thr = single ? 1024 : 256;
   while (thr > 128 && BlockLayoutSmem::bytes(thr / 32, E, N) > 200 * 1024) thr >>= 1;
-  const size_t smem = std::max(BlockLayoutSmem::bytes(thr / 32, E, N), sizeof(int32_t) * ((size_t)N * C + E));
+  const size_t smem = std::max(BlockLayoutSmem::bytes(thr / 32, E, N) + sizeof(int32_t) * C,
+                               sizeof(int32_t) * ((size_t)N * C + E));
   if (smem > 200 * 1024) return fail(EPB_CAPACITY_EXCEEDED, "metadata too large");
   HTOpen p;
   p.topk = topk_idx; p.b = b; p.K = g->cfg.top_k; p.L = g->ht.L;

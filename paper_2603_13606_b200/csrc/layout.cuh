@@ -20,7 +20,7 @@ struct BlockLayoutSmem {
   int* hist;        // [nwarps][E+N]
   uint32_t* ballot; // [nwarps][E+N]
   int* ids;         // [nwarps][kIdsStride] coalesced-load staging of expert ids
-  static size_t bytes(int nwarps, int E, int N) {
+  __host__ __device__ static size_t bytes(int nwarps, int E, int N) {
     return (size_t)nwarps * (E + N) * 8 + (size_t)nwarps * kIdsStride * 4;
   }
   EPB_DEV static BlockLayoutSmem carve(int* base, int nwarps, int E, int N) {
@@ -226,14 +226,17 @@ EPB_DEV bool block_validate(const TopkT* topk, int b, int K, int E, int* s_bad) 
 
 // Validation (ids in [0, E), distinct within a row; api.py:150-170) fused
 // with the layout for K <= 8: the expert ids are loaded once per pass, with
-// coalesced loads, and a rejected routing writes no output.  Returns false
-// for a rejected routing (one verdict per block).
+// coalesced loads, and a rejected routing writes no output.  Two halves so
+// a multi-CTA caller can put a grid-wide exchange between them:
+//   block_hist8: validation + per-warp column histograms (shared memory),
+//                the block's column totals into `tot_out` (if given);
+//                false for a rejected routing (one verdict per block);
+//   block_rank8: exclusive scan of the histograms across warps seeded with
+//                `col_base` (the counts of earlier blocks, or none), the
+//                totals + base into m_out / q_out, then ranks and slots.
 template <typename TopkT>
-EPB_DEV bool block_layout_valid8(const TopkT* topk, int b, int K, int E, int N, int L, BlockLayoutSmem sm,
-                                 int32_t* m_out, int32_t* q_out, int32_t* rank_out, int32_t* slot_out,
-                                 uint64_t* stamps) {
-#define LAY_STAMP(I) \
-  do { if (stamps && threadIdx.x == 0) stamps[I] = globaltimer(); } while (0)
+EPB_DEV bool block_hist8(const TopkT* topk, int b, int K, int E, int N, int L, BlockLayoutSmem sm, int32_t* tot_out,
+                         uint64_t* stamps) {
   const int C = E + N;
   const int nwarps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -245,7 +248,6 @@ EPB_DEV bool block_layout_valid8(const TopkT* topk, int b, int K, int E, int N, 
   const int seg = (b + nwarps - 1) / nwarps;
   const int t0 = min(b, warp * seg), t1 = min(b, t0 + seg);
   int* h = sm.hist + warp * C;
-  uint32_t* bw = sm.ballot + warp * C;
   int* st = sm.ids + warp * kIdsStride;
   int ev[8];
   bool bad = false;
@@ -276,11 +278,26 @@ EPB_DEV bool block_layout_valid8(const TopkT* topk, int b, int K, int E, int N, 
       }
     }
   }
-  LAY_STAMP(0);
+  if (stamps && threadIdx.x == 0) stamps[0] = globaltimer();
   if (__syncthreads_or(bad)) return false;
-  LAY_STAMP(1);
+  if (tot_out)
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      int tot = 0;
+      for (int w = 0; w < nwarps; ++w) tot += sm.hist[w * C + c];
+      tot_out[c] = tot;
+    }
+  return true;
+}
+
+template <typename TopkT>
+EPB_DEV void block_rank8(const TopkT* topk, int b, int K, int E, int N, int L, BlockLayoutSmem sm,
+                         const int32_t* col_base, int32_t* m_out, int32_t* q_out, int32_t* rank_out,
+                         int32_t* slot_out, uint64_t* stamps) {
+  const int C = E + N;
+  const int nwarps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    int run = 0;
+    int run = col_base ? col_base[c] : 0;
     for (int w = 0; w < nwarps; ++w) {
       const int v = sm.hist[w * C + c];
       sm.hist[w * C + c] = run;
@@ -290,7 +307,13 @@ EPB_DEV bool block_layout_valid8(const TopkT* topk, int b, int K, int E, int N, 
     else if (q_out) q_out[c - E] = run;
   }
   __syncthreads();
-  LAY_STAMP(2);
+  if (stamps && threadIdx.x == 0) stamps[2] = globaltimer();
+  const int seg = (b + nwarps - 1) / nwarps;
+  const int t0 = min(b, warp * seg), t1 = min(b, t0 + seg);
+  int* h = sm.hist + warp * C;
+  uint32_t* bw = sm.ballot + warp * C;
+  int* st = sm.ids + warp * kIdsStride;
+  int ev[8];
   const uint32_t lt = (1u << lane) - 1u;
   for (int base = t0; base < t1; base += 32) {
     const int nt = min(32, t1 - base);
@@ -342,9 +365,16 @@ EPB_DEV bool block_layout_valid8(const TopkT* topk, int b, int K, int E, int N, 
     }
     __syncwarp();
   }
-  LAY_STAMP(3);
+  if (stamps && threadIdx.x == 0) stamps[3] = globaltimer();
   __syncthreads();
-#undef LAY_STAMP
+}
+
+template <typename TopkT>
+EPB_DEV bool block_layout_valid8(const TopkT* topk, int b, int K, int E, int N, int L, BlockLayoutSmem sm,
+                                 int32_t* m_out, int32_t* q_out, int32_t* rank_out, int32_t* slot_out,
+                                 uint64_t* stamps) {
+  if (!block_hist8(topk, b, K, E, N, L, sm, nullptr, stamps)) return false;
+  block_rank8(topk, b, K, E, N, L, sm, nullptr, m_out, q_out, rank_out, slot_out, stamps);
   return true;
 }
 

@@ -148,7 +148,7 @@ def ll_pipelined(world, rank):
 def buffer_ll(world, rank):
     """Buffer wrapper, one process per GPU: own comm stream, pinned mapped
     counters, cached dispatch."""
-    e, k, h = 256, 8, 7168
+    e, k, h, b = 256, 8, 7168, 64
     cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, b, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
     wl = owl.make_workload(e, world, b, k, h, 70)
     wl.tokens = [bf16r(t) for t in wl.tokens]
@@ -263,7 +263,7 @@ def ll_stress(world, rank, rounds, b=64):
     device and are read once at the end.  Run under EPB_CHAOS_NS the kernels
     sleep a random time before stores and releases (test_acceptance.py:286-292
     analogue: ordering must not depend on timing)."""
-    e, k, h, b = 256, 8, 7168, 64
+    e, k, h = 256, 8, 7168
     cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, b, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
     fab = ep.ProcessFabric(ep.NodeTopology(world, world))
     g = ep.create_group(fab, rank, cfg, strict=False)
