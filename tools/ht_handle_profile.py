@@ -66,8 +66,9 @@ def main():
 
             from paper_2603_13606_b200 import _lib
             tr = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
-            labels = ["start", "laid-out", "barrier1", "prefix", "barrier2", "fixed", "meta-sent", "meta-recv",
-                      "end", "validated", "pass1", "pass1-sync", "scanned", "ranked"]
+            # checkpoints of ht_open_kernel (csrc/ht.cu OPEN_STAMP, block_hist8 / block_rank8)
+            labels = ["start", "histograms", "barrier", "bases", "meta-sent", "ranked+", "meta-wait", "meta-recv",
+                      "end", "", "pass1", "", "scanned", "ranked"]
             for rep in range(3):
                 tr.zero_()
                 torch.cuda.synchronize()
