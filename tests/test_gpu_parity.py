@@ -316,13 +316,15 @@ def test_ht_zero_copy_combine_pulls_from_window(n, rpn):
         np.testing.assert_array_equal(res[r]["out"], comb[r])
 
 
+@pytest.mark.parametrize("n,k", [(2, 4), (1, 4), (1, 10)])
 @pytest.mark.parametrize("b", [1500, 4096])
-def test_ht_multi_cta_routing_layout(b):
-    """Batches above 512 tokens take the multi-CTA routing layout (per-chunk
-    histograms, column prefix, rebase): same receive order and rows."""
-    n = 2
-    cfg = make_cfg("ht", n, n, 32, b, 4, 256, "bf16")
-    wl = owl.make_workload(32, n, b, 4, 256, seed=21)
+def test_ht_multi_cta_routing_layout(b, n, k):
+    """Batches over several 128-token chunks: emulated ranks (N=2) take the
+    three-kernel layout (per-chunk histograms, column prefix, rebase); one
+    rank (N=1) the fused open — one grid barrier for top-k <= 8, the
+    two-barrier form above — same receive order and rows either way."""
+    cfg = make_cfg("ht", n, n, 32, b, k, 256, "bf16")
+    wl = owl.make_workload(32, n, b, k, 256, seed=21)
     res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale)
     dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, 32, n, 256, "bf16")
     ys = [oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_scale) for r in range(n)]
