@@ -698,13 +698,22 @@ class EpHandle:
                           ctypes.c_void_p(mt.data_ptr()), ctypes.c_void_p(mt.data_ptr() + nm * 4))
         mt, offsets, meta_p, total_p = g._ht_bufs
         host = g._pinned_i32(nm + 2)
-        if g._fused_ok() and _HT_OPEN_FUSED:
+        fused = g._fused_ok() and _HT_OPEN_FUSED
+        if fused:
             # layout + metadata all-gather in one launch, the shapes written
             # straight into pinned host memory with the error word after them
-            g._launch("epb_ht_open", g._g, rnd, _ptr(self.routing), self._b, ctypes.byref(self._lay),
-                      ctypes.c_void_p(host.data_ptr()), _ptr(offsets), self._sp())
-            g.check()  # one synchronisation: receive shapes are host-known on return (api.py:235-237)
-        else:
+            try:
+                g._launch("epb_ht_open", g._g, rnd, _ptr(self.routing), self._b, ctypes.byref(self._lay),
+                          ctypes.c_void_p(host.data_ptr()), _ptr(offsets), self._sp())
+            except EpError as err:
+                # more chunks than can be co-resident (refused before any
+                # launch): the separate launches speak the same protocol
+                if err.code is not ErrorCode.CAPACITY_EXCEEDED:
+                    raise
+                fused = False
+            else:
+                g.check()  # one synchronisation: receive shapes are host-known on return (api.py:235-237)
+        if not fused:
             # ranks emulated on one GPU: every rank's row is sent before any
             # rank waits for its peers'
             self._run_layout()

@@ -337,6 +337,23 @@ def test_ht_multi_cta_routing_layout(b, n, k):
         np.testing.assert_array_equal(res[r]["out"], comb[r])
 
 
+def test_ht_open_beyond_coresident_chunks_uses_separate_launches():
+    """More 128-token chunks than fit on the GPU at once (E=2048: one
+    layout CTA per SM): the one-launch open is refused before any work and
+    create_handle takes the separate layout / metadata launches."""
+    n, e, b, k, h = 1, 2048, 20000, 2, 16
+    cfg = make_cfg("ht", n, n, e, b, k, h, "bf16")
+    wl = owl.make_workload(e, n, b, k, h, seed=41)
+    res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale)
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, e, n, h, "bf16")
+    ys = [oht.apply_experts(dd[0]["rows"], dd[0]["origin"], owl.expert_scale)]
+    comb = oht.combine(ys, wl.routing, wl.weights, e, n, n)
+    np.testing.assert_array_equal(res[0]["m"], m)
+    np.testing.assert_array_equal(res[0]["origin"], dd[0]["origin"])
+    np.testing.assert_array_equal(res[0]["rows"], dd[0]["rows"])
+    np.testing.assert_array_equal(res[0]["out"], comb[0])
+
+
 # BASELINE configs[3] / [4] shapes: Mixtral (E=8, K=2, H=4096, one expert per
 # rank at N=8) and Qwen3-MoE (E=128, K=8, H=4096, Zipf routing)
 @pytest.mark.parametrize("n", [2, 8])
