@@ -194,6 +194,28 @@ def test_ll_fewer_tokens_zipf_and_empty_rank():
     _check_ll(cfg, res, d, comb)
 
 
+@pytest.mark.parametrize("n", [1, 3])
+def test_ht_empty_and_ragged_ranks(n):
+    """HT with a rank that routes no token (and, at N=1, an empty batch:
+    the one-launch open with no chunk), the others ragged."""
+    e, k, h = 12, 3, 256
+    cfg = make_cfg("ht", n, n, e, 9, k, h, "bf16")
+    wl = owl.make_workload(e, n, 9, k, h, seed=13)
+    for r, keep in enumerate([0, 9, 4][:n]):
+        wl.tokens[r] = wl.tokens[r][:keep]
+        wl.routing[r] = wl.routing[r][:keep]
+        wl.weights[r] = wl.weights[r][:keep]
+    res = run_ht(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_affine)
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, e, n, h, "bf16")
+    ys = [oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_affine) for r in range(n)]
+    comb = oht.combine(ys, wl.routing, wl.weights, e, n, n)
+    for r in range(n):
+        np.testing.assert_array_equal(res[r]["m"], m)
+        np.testing.assert_array_equal(res[r]["rows"], dd[r]["rows"])
+        np.testing.assert_array_equal(res[r]["origin"], dd[r]["origin"])
+        np.testing.assert_array_equal(res[r]["out"], comb[r])
+
+
 def test_ll_unaligned_hidden_element_path():
     cfg = make_cfg("ll", 2, 2, 8, 4, 3, 12, "fp8", False)
     wl = owl.make_workload(8, 2, 4, 3, 12, seed=1)
