@@ -204,6 +204,34 @@ def ht_case(world, rank, rpn, e, k, h, b, seed, bf16_expert, zero_copy=False):
     g.destroy()
 
 
+def ht_ragged(world, rank):
+    """HT in process mode with rank 0 routing no token and the others ragged
+    (the one-launch open with one chunk on some ranks, several on others)."""
+    e, k, h, bmax = 8 * world, 4, 512, 700
+    cfg = ep.EpConfig(ep.Algorithm.HT, world, world, e, k, h, bmax, ep.Dtype.BF16)
+    wl = owl.make_workload(e, world, bmax, k, h, 57)
+    for r in range(world):
+        keep = 0 if r == 0 else (bmax if r == 1 else 300 + 37 * r)
+        wl.tokens[r], wl.routing[r], wl.weights[r] = wl.tokens[r][:keep], wl.routing[r][:keep], wl.weights[r][:keep]
+    dd, m, q = oht.dispatch(wl.tokens, wl.routing, wl.weights, e, world, h, "bf16")
+    ys = [oht.apply_experts(dd[r]["rows"], dd[r]["origin"], owl.expert_affine) for r in range(world)]
+    want = oht.combine(ys, wl.routing, wl.weights, e, world, world)[rank]
+    g = ep.create_group(ep.ProcessFabric(ep.NodeTopology(world, world)), rank, cfg)
+    hd = g.create_handle(wl.routing[rank])
+    tot = hd.get_num_recv_tokens()
+    assert tot == dd[rank]["recv_total"], (tot, dd[rank]["recv_total"])
+    out = ep.tensor_create((tot, h), ep.Dtype.F32, T.TOKENS)
+    cnt = ep.tensor_create((cfg.experts_per_rank, world), ep.Dtype.F32, T.TOKENS_PER_EXPERTS)
+    w = ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)
+    hd.dispatch([ep.tensor_from_f32(wl.tokens[rank], ep.Dtype.BF16, T.TOKENS), w], [out, cnt])
+    np.testing.assert_array_equal(out.read_f32(), dd[rank]["rows"])
+    co = ep.tensor_create((wl.routing[rank].shape[0], h), ep.Dtype.F32, T.TOKENS)
+    hd.combine([ep.tensor_from_f32(ys[rank], ep.Dtype.F32, T.TOKENS), w], [co])
+    np.testing.assert_array_equal(co.read_f32(), want)
+    hd.destroy()
+    g.destroy()
+
+
 def traced_rounds(world, rank):
     """The op trace in process mode (one GPU per rank, CUDA-IPC windows):
     every line this rank's kernels record is one it initiated, with the
@@ -389,6 +417,7 @@ def main():
         ("ht bf16 single node", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 4, False)),
         ("ht zero-copy combine (pull)", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 8, True, zero_copy=True)),
         ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
+        ("ht empty + ragged ranks", lambda: ht_ragged(world, rank)),
         ("op trace ll + ht (process mode)", lambda: traced_rounds(world, rank)),
     ]
     stress = int(os.environ.get("EPB_MP_STRESS", "0"))
