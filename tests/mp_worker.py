@@ -45,7 +45,7 @@ def bf16r(x):
 
 
 def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, staged, mode, rounds=1,
-            layout="optimized", zero_copy=False, host_io=False):
+            layout="optimized", zero_copy=False, host_io=False, ragged=False):
     cfg = ep.EpConfig(ep.Algorithm.LL, world, world, e, k, h, bmax, dtype, scales, combine_dtype=combine_dtype,
                       expert_out_window=zero_copy)
     fab = ep.ProcessFabric(ep.NodeTopology(world, world))
@@ -53,6 +53,11 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
     ell = cfg.experts_per_rank
     for rnd in range(rounds):
         wl = owl.make_workload(e, world, bmax, k, h, seed + rnd)
+        if ragged:  # rank 0 routes no token, rank 1 a full batch, the rest part of one
+            for r in range(world):
+                keep = 0 if r == 0 else (bmax if r == 1 else (bmax * r) // (world + 1))
+                wl.tokens[r], wl.routing[r], wl.weights[r] = (wl.tokens[r][:keep], wl.routing[r][:keep],
+                                                              wl.weights[r][:keep])
         if mode == "bf16":
             wl.tokens = [bf16r(t) for t in wl.tokens]
         d = oll.dispatch(wl.tokens, wl.routing, e, world, bmax, h, dtype.value, scales)
@@ -95,10 +100,11 @@ def ll_case(world, rank, e, k, h, bmax, dtype, scales, combine_dtype, seed, stag
         else:
             yin = ep.tensor_from_f32(y, ep.Dtype.BF16, T.TOKENS)
         comb_in = [yin, ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, T.TOPK_WEIGHTS)]
+        b_me = wl.routing[rank].shape[0]
         if host_io:  # pinned host output: written by the combine kernel in place over PCIe
-            comb_out = ep.tensor_from_torch(torch.zeros((bmax, h), dtype=torch.float32).pin_memory(), T.TOKENS)
+            comb_out = ep.tensor_from_torch(torch.zeros((b_me, h), dtype=torch.float32).pin_memory(), T.TOKENS)
         else:
-            comb_out = ep.tensor_create((bmax, h), ep.Dtype.F32, T.TOKENS)
+            comb_out = ep.tensor_create((b_me, h), ep.Dtype.F32, T.TOKENS)
         hd.combine(comb_in, [comb_out], send_only=staged)
         if staged:
             hd.complete()
@@ -418,6 +424,9 @@ def main():
         ("ht zero-copy combine (pull)", lambda: ht_case(world, rank, world, 64, 8, 2048, 256, 8, True, zero_copy=True)),
         ("ht bf16 rpn=2 hierarchical order", lambda: ht_case(world, rank, max(1, world // 2), 32, 4, 512, 64, 5, True)),
         ("ht empty + ragged ranks", lambda: ht_ragged(world, rank)),
+        ("ll c2 hot path, empty + ragged ranks", lambda: ll_case(world, rank, 256, 8, 7168, 128, ep.Dtype.FP8, True,
+                                                                  ep.Dtype.BF16, 61, False, "bf16", rounds=2,
+                                                                  ragged=True)),
         ("op trace ll + ht (process mode)", lambda: traced_rounds(world, rank)),
     ]
     stress = int(os.environ.get("EPB_MP_STRESS", "0"))
