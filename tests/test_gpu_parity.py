@@ -170,6 +170,22 @@ def test_ll_dsv3_fp8_matches_oracle(n, b):
     _check_ll(cfg, res, d, comb)
 
 
+@pytest.mark.parametrize("b", [512, 600, 1024])
+def test_ll_batch_at_and_beyond_the_decode_kernel(b):
+    """512 tokens per rank is the largest batch the decode (FAST) kernel
+    takes — one routing row per thread; 600 and 1024 run the general kernel
+    — bit-exact with the oracle either way (N=2, bf16 in, FP8 + scales on
+    the wire)."""
+    n, e, k, h = 2, 32, 8, 512
+    cfg = ep.EpConfig(ep.Algorithm.LL, n, n, e, k, h, b, ep.Dtype.FP8, True, combine_dtype=ep.Dtype.BF16)
+    wl = owl.make_workload(e, n, b, k, h, seed=b)
+    wl.tokens = [bf16_round(t) for t in wl.tokens]
+    res = run_ll(cfg, wl.tokens, wl.routing, wl.weights, owl.expert_scale, mode="bf16", wire_out=True,
+                 bf16_expert=True)
+    d, comb = _ll_oracle(cfg, wl, owl.expert_scale, bf16_expert=True)
+    _check_ll(cfg, res, d, comb)
+
+
 @pytest.mark.parametrize("n", [1, 4])
 def test_ll_c2_hot_path_bf16_in_fp8_wire_bf16_combine(n):
     """North-star path: bf16 tokens, in-kernel FP8 quantisation, wire-dtype
