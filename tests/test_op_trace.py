@@ -166,3 +166,38 @@ def test_ht_round_trace():
     flags = [o for o in ops if o["op"] == "signal" and o["sig"] // n == 2]
     for o in flags:
         assert o["val"] & 0xFFFFFFFF == q[o["src"]][o["dst"]]  # flag value carries the record count
+
+
+@pytest.mark.gpu
+@pytest.mark.filterwarnings("ignore:op trace")
+def test_trace_ring_overflow_keeps_the_first_records_and_warns():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from tests.gpu_util import make_cfg
+    n, e, b, k, h = 2, 8, 6, 2, 64
+    cfg = make_cfg("ll", n, n, e, b, k, h)
+    wl = owl.make_workload(e, n, b, k, h, seed=3)
+    lines = []
+    fabric = ep.Fabric(ep.NodeTopology(n, n), trace=lines.append, trace_capacity=3)
+    from tests.rank_threads import run_ranks
+
+    def body(rank):
+        g = ep.create_group(fabric, rank, cfg)
+        hd = g.create_handle(wl.routing[rank])
+        out = ep.tensor_create((cfg.experts_per_rank, n * b, h), ep.Dtype.F32, ep.TensorTag.TOKENS)
+        cnt = ep.tensor_create((cfg.experts_per_rank, n), ep.Dtype.F32, ep.TensorTag.RECV_EXPERT_COUNTER_HOST)
+        hd.dispatch([ep.tensor_from_f32(wl.tokens[rank], ep.Dtype.F32, ep.TensorTag.TOKENS)], [out, cnt])
+        y = ep.tensor_from_f32(out.read_f32(), ep.Dtype.F32, ep.TensorTag.TOKENS)
+        w = ep.tensor_from_f32(wl.weights[rank], ep.Dtype.F32, ep.TensorTag.TOPK_WEIGHTS)
+        hd.combine([y, w], [ep.tensor_create((b, h), ep.Dtype.F32, ep.TensorTag.TOKENS)])
+        hd.destroy()
+        g.destroy()
+
+    try:
+        run_ranks(n, body, on_error=fabric.shutdown)
+    finally:
+        fabric.shutdown()
+    assert fabric.trace.dropped > 0  # counted (and warned about) when a call overflows its ring
+    assert lines and all(len(ln.split(",")) == 9 for ln in lines)
+    assert [int(ln.split(",")[-1]) for ln in lines] == list(range(1, len(lines) + 1))
